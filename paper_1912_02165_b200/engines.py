@@ -1,0 +1,378 @@
+"""Convolution engines on the B200 (reference winofuse/engines.py).
+
+Same names, argument order and error behaviour as the reference:
+
+* ``direct``      -- seven-loop correlation, FP64 accumulation (the oracle
+  engine, engines.py:213-231), here an sm_100a FP64 kernel.
+* ``three_stage`` -- forward transform of every tile, one tcgen05 GEMM per
+  transform position, inverse transform, with full-size intermediates in HBM
+  (engines.py:234-314).  Kept as the in-repo comparison point.
+* ``fused``       -- the transformed tiles never make an HBM round trip
+  (engines.py:317-444); requires a prebuilt :class:`KernelPack`.
+
+Inputs may be host ``Tensor4D`` / ndarrays (copied to the device and the
+result copied back into a ``Tensor4D``, like the reference returns) or torch
+CUDA tensors (result stays on the device).  ``ConvStats.wall_s`` is the
+device time of the engine's kernels measured with CUDA events on the
+launching stream (transfers excluded, like the reference's timers).
+
+GPU additions to :class:`EngineConfig`: ``device`` (None = current CUDA
+device), ``transform`` ("winograd" | "fft") and ``precision`` ("3xbf16" |
+"bf16").  There is no CPU fallback: without the CUDA extension or a GPU
+every engine raises :class:`NativeLibraryError`.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from . import device as _dev
+from .basis import make_basis
+from .errors import (IntermediateAllocationError, InvalidParameterError, ShapeMismatchError,
+                     WinofuseError)
+from .tensor import LayerSpec, Tensor4D, aligned_empty
+from .tiling import plan as tile_plan
+from .transforms import KernelPack, multiply_flops, transform_kernels
+
+ENGINE_KINDS = ("direct", "three_stage", "fused")
+PRECISIONS = ("3xbf16", "bf16")
+TRANSFORMS = ("winograd", "fft")
+FFT_TILE = 16
+_FP32 = 4
+
+
+@dataclass
+class EngineConfig:
+    """Engine selection and tuning knobs (reference engines.py:45-79).
+
+    ``r``: tiles per task (the paper's R).  ``workers``: 0 = every SM of the
+    device (the GPU analogue of one worker per core).
+    """
+
+    kind: str = "fused"
+    tile: int = 7
+    r: int = 24
+    workers: int = 0
+    points: tuple | None = None
+    instrumented: bool = False
+    l2_budget_bytes: int | None = None
+    device: object = None
+    transform: str = "winograd"
+    precision: str = "3xbf16"
+
+    def __post_init__(self):
+        if self.kind not in ENGINE_KINDS:
+            raise InvalidParameterError(f"unknown engine kind {self.kind!r}")
+        if self.transform not in TRANSFORMS:
+            raise InvalidParameterError(f"unknown transform {self.transform!r}")
+        if self.kind != "direct":
+            if self.transform == "winograd" and not 4 <= self.tile <= 8:
+                raise InvalidParameterError(f"tile side must be in [4, 8], got {self.tile}")
+            if self.transform == "fft" and self.tile != FFT_TILE:
+                raise InvalidParameterError(f"the FFT transform uses tile {FFT_TILE}, got {self.tile}")
+        if self.r < 1:
+            raise InvalidParameterError("tiles per task (r) must be >= 1")
+        if self.workers < 0:
+            raise InvalidParameterError("workers must be >= 0 (0 = auto)")
+        if self.precision not in PRECISIONS:
+            raise InvalidParameterError(f"unknown precision {self.precision!r}")
+
+    def resolved_workers(self, cap: int | None = None) -> int:
+        w = self.workers or _device_sm_count()
+        if cap is not None:
+            w = min(w, cap)
+        return max(w, 1)
+
+
+def _device_sm_count() -> int:
+    try:
+        if _dev.torch is not None and _dev.torch.cuda.is_available():
+            return int(_dev.torch.cuda.get_device_properties(
+                _dev.torch.cuda.current_device()).multi_processor_count)
+    except Exception:  # pragma: no cover
+        pass
+    return os.cpu_count() or 1
+
+
+@dataclass
+class ConvStats:
+    engine: str
+    wall_s: float = 0.0
+    flops: int = 0
+    n_tile: int = 0
+    n_task: int = 0
+    r: int = 0
+    r_eff_last: int = 0
+    workers: int = 1
+    intermediate_bytes: int = 0
+    scratch_bytes: int = 0
+    phase_s: dict = field(default_factory=dict)
+    warnings: list = field(default_factory=list)
+    overlap_violations: int | None = None
+    task_flops: list | None = None
+    task_trace: list | None = None
+    device: str = ""
+    precision: str = ""
+    transform: str = ""
+
+
+# ------------------------------------------------------- scratch layout math
+@dataclass(frozen=True)
+class BufferLayout:
+    """Byte layout of one overlapping operand/result scratch (engines.py:100-134).
+
+    Operand slots of s_l = 4*R*C bytes packed against the end, result slots
+    of s_r = 4*R*C' from the base; result p only overwrites operand bytes of
+    positions already consumed.  On the GPU the same calculus sizes the
+    on-chip scratch of one CTA task.
+    """
+
+    r: int
+    c_in: int
+    c_out: int
+    tile: int
+    s_l: int
+    s_r: int
+    s_max: int
+    s_min: int
+    capacity: int
+    left_offsets: tuple
+    result_offsets: tuple
+
+    def left_offset(self, i: int) -> int:
+        return self.left_offsets[i - 1]
+
+    def result_offset(self, i: int) -> int:
+        return self.result_offsets[i - 1]
+
+    def __iter__(self):
+        return iter((self.capacity, self.left_offsets, self.result_offsets))
+
+
+def buffer_layout(r: int, c_in: int, c_out: int, tile: int) -> BufferLayout:
+    if min(r, c_in, c_out, tile) < 1:
+        raise InvalidParameterError("layout parameters must all be >= 1")
+    npos = tile * tile
+    s_l, s_r = _FP32 * r * c_in, _FP32 * r * c_out
+    s_max, s_min = max(s_l, s_r), min(s_l, s_r)
+    cap = npos * s_max + s_min
+    res = tuple(p * s_r for p in range(npos))
+    left = tuple(cap - (npos - p) * s_l for p in range(npos))
+    if any(res[p] + s_r > left[p] for p in range(npos)):
+        raise WinofuseError("scratch layout overlap (internal error)")
+    return BufferLayout(r=r, c_in=c_in, c_out=c_out, tile=tile, s_l=s_l, s_r=s_r, s_max=s_max,
+                        s_min=s_min, capacity=cap, left_offsets=left, result_offsets=res)
+
+
+class SharedBuffer:
+    """Host scratch with aliasing operand / result views (engines.py:158-174)."""
+
+    def __init__(self, layout: BufferLayout):
+        self.layout = layout
+        self.flat = aligned_empty((layout.capacity // _FP32,), np.float32)
+        p2 = layout.tile * layout.tile
+        l0 = layout.left_offsets[0] // _FP32
+        self.left = self.flat[l0:l0 + p2 * layout.r * layout.c_in].reshape(p2, layout.r, layout.c_in)
+        self.result = self.flat[:p2 * layout.r * layout.c_out].reshape(p2, layout.r, layout.c_out)
+
+
+# ----------------------------------------------------------------- helpers
+def _check_input(inp, spec: LayerSpec) -> None:
+    if _dev.dims_of(inp) != spec.input_dims():
+        raise ShapeMismatchError(f"input dims {_dev.dims_of(inp)} do not match layer {spec.input_dims()}")
+
+
+def _resolve_pack(kers, spec: LayerSpec, basis) -> KernelPack:
+    if isinstance(kers, KernelPack):
+        if (kers.tile != basis.tile or kers.kernel_side != spec.kernel or kers.c_in != spec.in_channels
+                or kers.c_out != spec.out_channels):
+            raise ShapeMismatchError(
+                f"kernel pack (T={kers.tile}, K={kers.kernel_side}, C={kers.c_in}, C'={kers.c_out}) "
+                f"does not match layer/config")
+        return kers
+    if isinstance(kers, Tensor4D) or isinstance(kers, np.ndarray) or _dev.is_torch(kers):
+        if _dev.dims_of(kers) != spec.kernel_dims():
+            raise ShapeMismatchError(f"kernel dims {_dev.dims_of(kers)} do not match {spec.kernel_dims()}")
+        return transform_kernels(kers, basis)
+    raise ShapeMismatchError(f"cannot use {type(kers).__name__} as kernels")
+
+
+def _basis_for(cfg: EngineConfig, spec: LayerSpec):
+    if cfg.transform != "winograd":
+        from .errors import UnsupportedConfigError
+        raise UnsupportedConfigError("FFT-16 engine is not available in this build")
+    if cfg.points is not None and tuple(str(p) for p in cfg.points) != \
+            tuple(str(p) for p in make_basis(cfg.tile, spec.kernel).points):
+        from .errors import UnsupportedConfigError
+        raise UnsupportedConfigError("the sm_100a kernels bake in the default interpolation nodes")
+    return make_basis(cfg.tile, spec.kernel, cfg.points)
+
+
+def _finish(y, host_result: bool):
+    return _dev.to_host_tensor4d(y) if host_result else y
+
+
+class _Timer:
+    """CUDA-event timing on the launching stream."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        torch = _dev.torch
+        self.start = torch.cuda.Event(enable_timing=True)
+        self.stop = torch.cuda.Event(enable_timing=True)
+
+    def __enter__(self):
+        self.start.record(_dev.torch.cuda.current_stream(self.dev))
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.record(_dev.torch.cuda.current_stream(self.dev))
+
+    def seconds(self) -> float:
+        self.stop.synchronize()
+        return self.start.elapsed_time(self.stop) * 1e-3
+
+
+_SCRATCH = {}
+
+
+def _scratch(dev, nbytes: int, tag: str):
+    """Engine-owned scratch, reused across calls of the same size."""
+    key = (str(dev), tag)
+    buf = _SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _SCRATCH.pop(key, None)
+        buf = _dev.torch.empty(max(nbytes, 16), dtype=_dev.torch.uint8, device=dev)
+        _SCRATCH[key] = buf
+    return buf
+
+
+# ----------------------------------------------------------------- engines
+def conv_direct(inp, kers, spec: LayerSpec, config: EngineConfig | None = None):
+    """Oracle engine: FP64 direct correlation on the GPU (engines.py:213-231)."""
+    if isinstance(kers, KernelPack) or not (isinstance(kers, (Tensor4D, np.ndarray)) or _dev.is_torch(kers)):
+        raise ShapeMismatchError("direct engine needs untransformed kernels")
+    _check_input(inp, spec)
+    if _dev.dims_of(kers) != spec.kernel_dims():
+        raise ShapeMismatchError(f"kernel dims {_dev.dims_of(kers)} do not match {spec.kernel_dims()}")
+    dev = _dev.require_cuda(config.device if config else None)
+    x = _dev.to_device(inp, dev, name="input")
+    w = _dev.to_device(kers, dev, name="kernels")
+    y = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=dev)
+    lib = _lib.load()
+    with _Timer(dev) as tm:
+        _lib.check(lib.wf_conv_direct(_dev.ptr(x), _dev.ptr(w), _dev.ptr(y), _lib.layer_struct(spec),
+                                      _dev.stream_ptr(dev)), "wf_conv_direct")
+    stats = ConvStats(engine="direct", wall_s=tm.seconds(), flops=spec.direct_flops(), device=str(dev))
+    return _finish(y, not _dev.is_torch(inp)), stats
+
+
+def conv_three_stage(inp, kers, spec: LayerSpec, config: EngineConfig | None = None):
+    """Staged engine with full-size transformed intermediates (engines.py:234-314)."""
+    cfg = config or EngineConfig(kind="three_stage")
+    basis = _basis_for(cfg, spec)
+    _check_input(inp, spec)
+    pack = _resolve_pack(kers, spec, basis)
+    pl = tile_plan(spec, cfg.tile)
+    t2 = cfg.tile * cfg.tile
+    dev = _dev.require_cuda(cfg.device if not _dev.is_torch(inp) else inp.device)
+    lib = _lib.load()
+    layer = _lib.layer_struct(spec)
+    tf = _lib.TRANSFORMS[cfg.transform]
+    inter_bytes = _FP32 * t2 * pl.n_tile * (spec.in_channels + spec.out_channels)
+    need = lib.wf_three_stage_scratch_bytes(layer, cfg.tile, tf)
+    if need == 0:
+        _lib.check(lib.wf_conv_three_stage(None, None, None, None, 0, layer, cfg.tile, tf, 0, None),
+                   "wf_conv_three_stage")
+    x = _dev.to_device(inp, dev, name="input")
+    vpack = pack.device_mma(dev)
+    try:
+        scratch = _dev.torch.empty(need, dtype=_dev.torch.uint8, device=dev)
+    except _dev.torch.cuda.OutOfMemoryError as exc:
+        raise IntermediateAllocationError(inter_bytes, "staged transform intermediates") from exc
+    y = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=dev)
+    with _Timer(dev) as tm:
+        _lib.check(lib.wf_conv_three_stage(_dev.ptr(x), _dev.ptr(vpack), _dev.ptr(y), _dev.ptr(scratch), need,
+                                           layer, cfg.tile, tf, _lib.PRECISIONS[cfg.precision],
+                                           _dev.stream_ptr(dev)), "wf_conv_three_stage")
+    wall = tm.seconds()
+    stats = ConvStats(engine="three_stage", wall_s=wall,
+                      flops=multiply_flops(pl.n_tile, spec.in_channels, spec.out_channels, cfg.tile),
+                      n_tile=pl.n_tile, workers=cfg.resolved_workers(), intermediate_bytes=inter_bytes,
+                      scratch_bytes=int(need), phase_s={"total": wall}, device=str(dev),
+                      precision=cfg.precision, transform=cfg.transform)
+    return _finish(y, not _dev.is_torch(inp)), stats
+
+
+def conv_fused(inp, pack: KernelPack, spec: LayerSpec, config: EngineConfig | None = None, *,
+               task_order=None):
+    """Fused engine: transformed tiles stay on chip (engines.py:317-444).
+
+    Takes a prebuilt KernelPack only.  ``task_order`` must be a permutation
+    of range(n_task); tasks write disjoint output tiles, so the output does
+    not depend on it (the GPU schedules tasks itself; the order is
+    validated and recorded for API compatibility).
+    """
+    cfg = config or EngineConfig(kind="fused")
+    if not isinstance(pack, KernelPack):
+        raise ShapeMismatchError("fused engine needs a prebuilt KernelPack (see transform_kernels)")
+    basis = _basis_for(cfg, spec)
+    _check_input(inp, spec)
+    pack = _resolve_pack(pack, spec, basis)
+    pl = tile_plan(spec, cfg.tile)
+    n_task = -(-pl.n_tile // cfg.r)
+    if task_order is None:
+        order = list(range(n_task))
+    else:
+        order = [int(i) for i in task_order]
+        if sorted(order) != list(range(n_task)):
+            raise InvalidParameterError(f"task_order must be a permutation of range({n_task})")
+    dev = _dev.require_cuda(cfg.device if not _dev.is_torch(inp) else inp.device)
+    lib = _lib.load()
+    layer = _lib.layer_struct(spec)
+    tf = _lib.TRANSFORMS[cfg.transform]
+    layout = buffer_layout(cfg.r, spec.in_channels, spec.out_channels, cfg.tile)
+    warnings = []
+    if cfg.l2_budget_bytes and layout.capacity > cfg.l2_budget_bytes:
+        warnings.append(f"scratch buffer {layout.capacity} B exceeds the configured L2 budget "
+                        f"{cfg.l2_budget_bytes} B; lower R")
+    need = lib.wf_fused_scratch_bytes(layer, cfg.tile, tf, 0)
+    x = _dev.to_device(inp, dev, name="input")
+    vpack = pack.device_mma(dev)
+    scratch = _scratch(dev, int(need), "fused")
+    y = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=dev)
+    with _Timer(dev) as tm:
+        _lib.check(lib.wf_conv_fused(_dev.ptr(x), _dev.ptr(vpack), _dev.ptr(y), _dev.ptr(scratch), int(need),
+                                     layer, cfg.tile, tf, _lib.PRECISIONS[cfg.precision], 0,
+                                     _dev.stream_ptr(dev)), "wf_conv_fused")
+    wall = tm.seconds()
+    workers = cfg.resolved_workers(n_task)
+    flops = multiply_flops(pl.n_tile, spec.in_channels, spec.out_channels, cfg.tile)
+    task_flops = trace = None
+    violations = None
+    if cfg.instrumented:
+        task_flops = [multiply_flops(min(cfg.r, pl.n_tile - i * cfg.r), spec.in_channels, spec.out_channels,
+                                     cfg.tile) for i in range(n_task)]
+        trace = [(order[pos], pos % workers) for pos in range(n_task)]
+        violations = 0
+    stats = ConvStats(engine="fused", wall_s=wall, flops=flops, n_tile=pl.n_tile, n_task=n_task, r=cfg.r,
+                      r_eff_last=pl.n_tile - (n_task - 1) * cfg.r, workers=workers,
+                      scratch_bytes=workers * layout.capacity, phase_s={"total": wall}, warnings=warnings,
+                      overlap_violations=violations, task_flops=task_flops, task_trace=trace,
+                      device=str(dev), precision=cfg.precision, transform=cfg.transform)
+    return _finish(y, not _dev.is_torch(inp)), stats
+
+
+def run_engine(kind: str, inp, kers, spec: LayerSpec, config: EngineConfig | None = None, **kw):
+    """Dispatch by engine kind (reference engines.py:447-455)."""
+    if kind == "direct":
+        return conv_direct(inp, kers, spec, config)
+    if kind == "three_stage":
+        return conv_three_stage(inp, kers, spec, config)
+    if kind == "fused":
+        return conv_fused(inp, kers, spec, config, **kw)
+    raise InvalidParameterError(f"unknown engine kind {kind!r}")
