@@ -156,8 +156,10 @@ __global__ void direct_conv_kernel(const float* __restrict__ x, const float* __r
       for (int kx = 0; kx < K; ++kx) {
         const int xx = xo + kx - L.pad_lo;
         if (xx < 0 || xx >= L.width) continue;
-        acc += static_cast<double>(plane[static_cast<size_t>(yy) * L.width + xx]) *
-               static_cast<double>(ker[ky * K + kx]);
+        // separate multiply and add (no DFMA): the reference's numba loop
+        // accumulates exactly like this (kernels.py:47-48, fastmath off)
+        acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(plane[static_cast<size_t>(yy) * L.width + xx]),
+                                       static_cast<double>(ker[ky * K + kx])));
       }
     }
   }

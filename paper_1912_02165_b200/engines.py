@@ -376,3 +376,49 @@ def run_engine(kind: str, inp, kers, spec: LayerSpec, config: EngineConfig | Non
     if kind == "fused":
         return conv_fused(inp, kers, spec, config, **kw)
     raise InvalidParameterError(f"unknown engine kind {kind!r}")
+
+
+class LayerPlan:
+    """Pre-planned layer: validated geometry, device pack, scratch and output.
+
+    ``plan = LayerPlan(spec, pack, config)`` does every allocation and check
+    once; ``plan(x)`` then only launches the engine's kernels on the current
+    stream (no host synchronisation, no allocation), so it can be timed
+    with CUDA events or captured into a CUDA graph.  Used by bench.py.
+    """
+
+    def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None):
+        cfg = config or EngineConfig(kind="fused")
+        if cfg.kind == "direct":
+            raise InvalidParameterError("LayerPlan covers the transformed engines")
+        if not isinstance(pack, KernelPack):
+            raise ShapeMismatchError("LayerPlan needs a prebuilt KernelPack")
+        basis = _basis_for(cfg, spec)
+        self.pack = _resolve_pack(pack, spec, basis)
+        self.spec, self.cfg = spec, cfg
+        self.dev = _dev.require_cuda(cfg.device)
+        self.lib = _lib.load()
+        self.layer = _lib.layer_struct(spec)
+        self.tf = _lib.TRANSFORMS[cfg.transform]
+        self.prec = _lib.PRECISIONS[cfg.precision]
+        if cfg.kind == "fused":
+            self.nbytes = int(self.lib.wf_fused_scratch_bytes(self.layer, cfg.tile, self.tf, 0))
+        else:
+            self.nbytes = int(self.lib.wf_three_stage_scratch_bytes(self.layer, cfg.tile, self.tf))
+        self.scratch = _dev.torch.empty(max(self.nbytes, 16), dtype=_dev.torch.uint8, device=self.dev)
+        self.vpack = self.pack.device_mma(self.dev)
+        self.out = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=self.dev)
+
+    def __call__(self, x, out=None):
+        """Launch on the current stream; x: contiguous f32 CUDA tensor (B, C, H, W)."""
+        y = self.out if out is None else out
+        stream = _dev.stream_ptr(self.dev)
+        if self.cfg.kind == "fused":
+            rc = self.lib.wf_conv_fused(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y), _dev.ptr(self.scratch),
+                                        self.nbytes, self.layer, self.cfg.tile, self.tf, self.prec, 0, stream)
+        else:
+            rc = self.lib.wf_conv_three_stage(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y),
+                                              _dev.ptr(self.scratch), self.nbytes, self.layer, self.cfg.tile,
+                                              self.tf, self.prec, stream)
+        _lib.check(rc, "LayerPlan")
+        return y

@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a engines against the CPU oracle (run on a B200).
+
+Tolerance (the north star's bar, in the reference's metric bench.py:59-64):
+max|y_gpu - y_fp64| / max|y_fp64| <= 1e-3 for every tile size in the
+default precision mode "3xbf16" (bf16 hi/lo split operands, three tcgen05
+passes, f32 accumulation).  The single-pass "bf16" mode is a speed knob
+with a documented looser bound (TOL_BF16) -- it does NOT meet 1e-3 for
+T >= 6.  Everything here calls the C ABI through the public API.
+"""
+import numpy as np
+import pytest
+
+import paper_1912_02165_b200 as wf
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {t: 1e-3 for t in range(4, 9)}          # 3xbf16, vs FP64 direct
+TOL_BF16 = {4: 2e-2, 5: 5e-2, 6: 2e-1, 7: 5e-1, 8: 1.0}
+
+
+def _he(rng, spec):
+    return (rng.standard_normal(spec.kernel_dims()) * np.sqrt(2.0 / (9 * spec.in_channels))).astype(np.float32)
+
+
+def _run(kind, x, pack_or_w, spec, t, **kw):
+    cfg = wf.EngineConfig(kind=kind, tile=t, **kw)
+    out, stats = wf.run_engine(kind, wf.Tensor4D(x), pack_or_w, spec, cfg)
+    return out.data, stats
+
+
+# ----------------------------------------------------------- golden cases
+def test_golden_cases_all_engines(golden_cases):
+    for c in golden_cases:
+        spec = wf.LayerSpec(*c["dims"])
+        t = c["tile"]
+        pack = wf.transform_kernels(wf.Tensor4D(c["w"]), wf.make_basis(t))
+        ref64 = O.direct_conv_f64(c["x"], c["w"], spec)
+        d, _ = _run("direct", c["x"], wf.Tensor4D(c["w"]), spec, t)
+        assert np.array_equal(d, c["direct"]), c["name"]          # FP64 engine: bitwise
+        f, fs = _run("fused", c["x"], pack, spec, t, r=c["r"])
+        s, _ = _run("three_stage", c["x"], pack, spec, t)
+        assert np.array_equal(f, s), c["name"]                    # fused == staged, bitwise
+        assert O.max_rel_error(f, ref64) <= TOL[t], (c["name"], O.max_rel_error(f, ref64))
+        assert O.max_rel_error(f, c["fused"]) <= TOL[t], c["name"]  # vs the reference's f32 output
+        assert fs.n_tile == c["n_tile"] and fs.n_task == c["n_task"] and fs.r_eff_last == c["r_eff_last"]
+
+
+def test_all_ones_layer_exact():
+    spec = wf.LayerSpec(1, 1, 1, 3, 3, 3, 1, 1)
+    pack = wf.transform_kernels(wf.new_tensor(spec.kernel_dims(), fill=1), wf.make_basis(4))
+    out, _ = wf.conv_fused(wf.new_tensor(spec.input_dims(), fill=1), pack, spec, wf.EngineConfig(tile=4))
+    assert np.allclose(out.data[0, 0], [[4, 6, 4], [6, 9, 6], [4, 6, 4]], rtol=0, atol=1e-5)
+
+
+# ------------------------------------------------- shapes and edge cases
+EDGE = [
+    ((1, 1, 1, 1, 1, 3, 1, 1), 4),          # 1x1 input, pure padding
+    ((1, 1, 1, 3, 3, 3, 1, 1), 8),          # tile much larger than the layer
+    ((2, 1, 7, 9, 5, 3, 1, 1), 6),          # C = 1
+    ((2, 7, 1, 9, 5, 3, 1, 1), 6),          # C' = 1
+    ((1, 17, 33, 11, 13, 3, 0, 0), 5),      # no padding, channels not multiple of 16
+    ((1, 8, 8, 10, 10, 3, 2, 2), 7),        # padding 2
+    ((1, 8, 8, 12, 9, 3, 0, 2), 4),         # pad_lo 0, pad_hi 2
+    ((3, 130, 300, 14, 14, 3, 1, 1), 6),    # K blocks 64+64+16, N chunks > 256
+    ((1, 80, 48, 6, 6, 3, 1, 1), 8),        # partial last K block (80 = 64 + 16)
+    ((2, 3, 64, 32, 32, 3, 1, 1), 6),       # VGG layer-1 style C = 3
+]
+
+
+@pytest.mark.parametrize("dims,t", EDGE)
+def test_edge_shapes_vs_fp64(dims, t):
+    rng = np.random.default_rng(hash(dims) % (1 << 32))
+    spec = wf.LayerSpec(*dims)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
+    ref = O.direct_conv_f64(x, w, spec)
+    f, _ = _run("fused", x, pack, spec, t)
+    s, _ = _run("three_stage", x, pack, spec, t)
+    assert np.array_equal(f, s)
+    assert O.max_rel_error(f, ref) <= TOL[t], O.max_rel_error(f, ref)
+    assert np.isfinite(f).all()
+
+
+@pytest.mark.parametrize("t", [4, 5, 6, 7, 8])
+def test_every_tile_against_oracle_f32(t):
+    rng = np.random.default_rng(100 + t)
+    spec = wf.LayerSpec(2, 24, 40, 19, 17, 3, 1, 1)
+    x = wf.new_tensor(spec.input_dims(), seed=int(rng.integers(1 << 30))).data
+    w = wf.new_tensor(spec.kernel_dims(), seed=int(rng.integers(1 << 30))).data
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
+    ref32 = O.conv_fused(x, pack.data, spec, t, 24, threads=4)      # the reference's f32 algorithm
+    ref64 = O.direct_conv_f64(x, w, spec)
+    f, _ = _run("fused", x, pack, spec, t)
+    assert O.max_rel_error(f, ref64) <= TOL[t]
+    assert O.max_rel_error(f, ref32) <= TOL[t]
+
+
+@pytest.mark.parametrize("t", [4, 6, 8])
+def test_bf16_single_pass_mode_documented_bound(t):
+    rng = np.random.default_rng(7 + t)
+    spec = wf.LayerSpec(1, 64, 64, 20, 20, 3, 1, 1)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
+    f, st = _run("fused", x, pack, spec, t, precision="bf16")
+    assert st.precision == "bf16"
+    assert O.max_rel_error(f, O.direct_conv_f64(x, w, spec)) <= TOL_BF16[t]
+
+
+# ---------------------------------------------------- BASELINE configs
+def test_config1_f23_full_layer():
+    # c1: B=1, C=C'=64, 56x56, F(2x2,3x3); weights N(0, 1/sqrt(9C))
+    rng = np.random.default_rng(1234)
+    spec = wf.LayerSpec(1, 64, 64, 56, 56, 3, 1, 1)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = (rng.standard_normal(spec.kernel_dims()) / np.sqrt(9 * 64)).astype(np.float32)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(4))
+    f, _ = _run("fused", x, pack, spec, 4)
+    s, _ = _run("three_stage", x, pack, spec, 4)
+    assert np.array_equal(f, s)
+    assert O.max_rel_error(f, O.direct_conv_f64(x, w, spec)) <= TOL[4]
+    assert O.max_rel_error(f, O.conv_fused(x, pack.data, spec, 4, 24, threads=8)) <= TOL[4]
+
+
+def test_config2_full_batch_f43_sharding_and_subset_parity():
+    # c2: B=64, C=C'=64, 56x56, F(4x4,3x3), He weights.  Full-batch GPU run;
+    # images 0..1 checked against FP64, and every 16-image shard run on its
+    # own must reproduce its slice of the full run bitwise (batch sharding).
+    rng = np.random.default_rng(2234)
+    spec = wf.LayerSpec(64, 64, 64, 56, 56, 3, 1, 1)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
+    full, _ = _run("fused", x, pack, spec, 6)
+    sub = wf.LayerSpec(2, 64, 64, 56, 56, 3, 1, 1)
+    assert O.max_rel_error(full[:2], O.direct_conv_f64(x[:2], w, sub)) <= TOL[6]
+    shard = wf.LayerSpec(16, 64, 64, 56, 56, 3, 1, 1)
+    for k in range(4):
+        part, _ = _run("fused", np.ascontiguousarray(x[16 * k:16 * (k + 1)]), pack, shard, 6)
+        assert np.array_equal(part, full[16 * k:16 * (k + 1)])
+    staged, _ = _run("three_stage", x, pack, spec, 6)
+    assert np.array_equal(staged, full)
+
+
+VGG = [(3, 64, 224), (64, 64, 224), (64, 128, 112), (128, 128, 112), (128, 256, 56), (256, 256, 56),
+       (256, 512, 28), (512, 512, 28), (512, 512, 14)]
+
+
+@pytest.mark.parametrize("c,cp,hw", VGG)
+def test_config3_vgg_layers_reduced_batch(c, cp, hw):
+    rng = np.random.default_rng(c * 7 + cp + hw)
+    spec = wf.LayerSpec(1, c, cp, hw, hw, 3, 1, 1)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
+    f, _ = _run("fused", x, pack, spec, 6)
+    assert O.max_rel_error(f, O.direct_conv_f64(x, w, spec)) <= TOL[6]
+
+
+@pytest.mark.parametrize("c", [16, 32, 64, 128])
+@pytest.mark.parametrize("hw", [28, 56])
+def test_config5_f63_sweep_reduced_batch(c, hw):
+    spec = wf.LayerSpec(2, c, c, hw, hw, 3, 1, 1)
+    x = wf.new_tensor(spec.input_dims(), seed=c + hw).data     # U(-1, 1) like the reference
+    rng = np.random.default_rng(c * hw)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(8))
+    f, _ = _run("fused", x, pack, spec, 8)
+    assert O.max_rel_error(f, O.direct_conv_f64(x, w, spec)) <= TOL[8]
+
+
+# -------------------------------------------------- properties / API paths
+def test_determinism_and_linearity():
+    rng = np.random.default_rng(5)
+    spec = wf.LayerSpec(4, 32, 48, 30, 26, 3, 1, 1)
+    x1 = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
+    a, _ = _run("fused", x1, pack, spec, 6)
+    for _ in range(3):
+        b, _ = _run("fused", x1, pack, spec, 6)
+        assert np.array_equal(a, b)
+    twice, _ = _run("fused", 2 * x1, pack, spec, 6)        # scaling by 2 is exact in every stage
+    assert np.array_equal(twice, 2 * a)
+
+
+def test_torch_cuda_tensors_in_and_out(cuda_dev):
+    import torch
+    rng = np.random.default_rng(9)
+    spec = wf.LayerSpec(2, 16, 24, 20, 20, 3, 1, 1)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    xt = torch.from_numpy(x).to(cuda_dev)
+    wt = torch.from_numpy(w).to(cuda_dev)
+    pack_dev = wf.transform_kernels(wt, wf.make_basis(6))           # device filter transform
+    pack_host = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
+    # f64 summation order may differ from numpy's matmul: rare 1-ulp f32 flips only
+    ulp = np.abs(pack_dev.data.view(np.int32).astype(np.int64) - pack_host.data.view(np.int32).astype(np.int64))
+    assert np.mean(ulp == 0) > 0.99 and ulp.max() <= 1
+    y, st = wf.conv_fused(xt, pack_dev, spec, wf.EngineConfig(tile=6))
+    assert isinstance(y, torch.Tensor) and y.is_cuda and st.wall_s > 0
+    ref = O.direct_conv_f64(x, w, spec)
+    assert O.max_rel_error(y.cpu().numpy(), ref) <= TOL[6]
+    d, _ = wf.conv_direct(xt, wt, spec)
+    assert O.max_rel_error(d.cpu().numpy(), ref) <= 1e-6
+
+
+def test_stage_functions_on_gpu_match_oracle(golden_cases):
+    c = next(c for c in golden_cases if c["name"] == "t5_workers")
+    spec = wf.LayerSpec(*c["dims"])
+    t = c["tile"]
+    basis = wf.make_basis(t)
+    pl = wf.tile_plan(spec, t)
+    n = pl.n_tile
+    blk = wf.LeftHandBlock.empty(t, n + 2, spec.in_channels)
+    blk.data[...] = 7.0
+    wf.forward_transform_tiles(wf.Tensor4D(c["x"]), spec, pl, basis, range(0, n), blk, row0=2)
+    want = O.forward_tiles(c["x"], spec, t, 0, n, n + 2, row0=2)
+    assert np.all(blk.data[:, :2] == 7.0)
+    assert np.allclose(blk.data[:, 2:], want[:, 2:], rtol=0, atol=1e-5 * np.abs(want).max())
+    left = np.ascontiguousarray(want[:, 2:])
+    res = np.zeros((t * t, n, spec.out_channels), np.float32)
+    pack = wf.transform_kernels(wf.Tensor4D(c["w"]), basis)
+    flops = wf.multiply_block(left, pack, res)
+    assert flops == wf.multiply_flops(n, spec.in_channels, spec.out_channels, t)
+    assert np.array_equal(res, O.multiply_positions(left, c["pack"], n))   # f32, ascending c: bitwise
+    out = wf.new_tensor(spec.output_dims())
+    wf.inverse_transform_tiles(res, basis, pl, range(0, n), out)
+    assert O.max_rel_error(out.data, c["three_stage"]) <= 1e-5
+
+
+def test_unsupported_configs_fail_loudly():
+    spec5 = wf.LayerSpec(1, 2, 2, 9, 9, 5, 2, 2)
+    pack5 = wf.transform_kernels(wf.new_tensor(spec5.kernel_dims(), seed=1), wf.make_basis(7, 5))
+    with pytest.raises(wf.UnsupportedConfigError):
+        wf.conv_fused(wf.new_tensor(spec5.input_dims()), pack5, spec5, wf.EngineConfig(tile=7))
+    spec = wf.LayerSpec(1, 2, 2, 9, 9, 3, 1, 1)
+    pack = wf.transform_kernels(wf.new_tensor(spec.kernel_dims()), wf.make_basis(5, 3, points=(0, 1, -1, 3)))
+    with pytest.raises(wf.UnsupportedConfigError):
+        wf.conv_fused(wf.new_tensor(spec.input_dims()), pack, spec,
+                      wf.EngineConfig(tile=5, points=(0, 1, -1, 3)))
+
+
+def test_fused_task_order_and_instrumented_accounting(golden_cases):
+    c = next(c for c in golden_cases if c["name"] == "t5_workers")
+    spec = wf.LayerSpec(*c["dims"])
+    pack = wf.transform_kernels(wf.Tensor4D(c["w"]), wf.make_basis(5))
+    cfg = wf.EngineConfig(tile=5, r=5, instrumented=True)
+    n_task = -(-c["n_tile"] // 5)
+    a, st = wf.conv_fused(wf.Tensor4D(c["x"]), pack, spec, cfg, task_order=list(reversed(range(n_task))))
+    b, _ = wf.conv_fused(wf.Tensor4D(c["x"]), pack, spec, cfg)
+    assert np.array_equal(a.data, b.data)
+    assert st.overlap_violations == 0 and sum(st.task_flops) == st.flops
+    assert sorted(tk for tk, _ in st.task_trace) == list(range(n_task))
+    with pytest.raises(wf.InvalidParameterError):
+        wf.conv_fused(wf.Tensor4D(c["x"]), pack, spec, cfg, task_order=[0] * n_task)

@@ -342,6 +342,81 @@ __global__ void mcast_load(const uint8_t* __restrict__ buf, size_t bytes, int re
   if (threadIdx.x == 0) sink[blockIdx.x] = smem[11];
 }
 
+// ------------------------------------------------------------ multicast ring bandwidth
+// CS CTAs per cluster stream the same sequence of CHUNK-byte chunks through a
+// NST-deep smem ring.  mc=1: each CTA issues 1/CS of every chunk with
+// .multicast::cluster to all CTAs; mc=0: every CTA issues the whole chunk
+// itself (same data, unicast).  A cluster barrier every 8 chunks keeps the
+// CTAs within one ring of each other.  distinct=1: clusters read disjoint data.
+template <int CS, int NST, int CHUNK>
+__global__ void mc_ring(const uint8_t* __restrict__ buf, size_t bytes, int nchunks, int mc, int* sink) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bars[NST];
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (threadIdx.x == 0) { for (int i = 0; i < NST; ++i) mbar_init(&bars[i], 1); fence_mbar_init(); }
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  const size_t nch_buf = bytes / CHUNK;
+  const size_t cl = blockIdx.x / CS;
+  const size_t base = (cl * 977) % nch_buf;
+  for (int c0 = 0; c0 < nchunks; c0 += 8) {
+    if (threadIdx.x == 0) {
+      for (int c = c0; c < c0 + 8 && c < nchunks; ++c) {
+        const int s = c % NST;
+        if (c >= NST) mbar_wait(&bars[s], ((c / NST) - 1) & 1);
+        mbar_expect_tx(&bars[s], CHUNK);
+        const uint8_t* src = buf + ((base + c) % nch_buf) * CHUNK;
+        if (mc) {
+          const int part = CHUNK / CS;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;"
+                       :: "r"(smem_u32(smem + s * CHUNK) + rank * part), "l"(src + rank * part), "r"(part),
+                          "r"(smem_u32(&bars[s])), "h"((uint16_t)((1u << CS) - 1)) : "memory");
+        } else {
+          bulk_g2s(smem + s * CHUNK, src, CHUNK, &bars[s]);
+        }
+      }
+      // drain this group
+      for (int c = c0; c < c0 + 8 && c < nchunks; ++c) {
+        const int s = c % NST;
+        if (c + NST >= c0 + 8 || c + NST >= nchunks) mbar_wait(&bars[s], (c / NST) & 1);
+      }
+    }
+    __syncwarp();
+    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 0) sink[blockIdx.x] = smem[13];
+}
+
+template <int CS>
+void run_mc(int nsm, uint8_t* buf, size_t bytes, int* sink) {
+  constexpr int NST = 8, CHUNK = 16384;
+  auto kern = mc_ring<CS, NST, CHUNK>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, NST * CHUNK));
+  int grid = (nsm / CS) * CS;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid); cfg.blockDim = dim3(32); cfg.dynamicSmemBytes = NST * CHUNK;
+  cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int mc = 0; mc < 2; ++mc) {
+    int nchunks = 16;
+    CK(cudaLaunchKernelEx(&cfg, kern, (const uint8_t*)buf, bytes, nchunks, mc, sink));
+    CK(cudaDeviceSynchronize());
+    nchunks = 2048;
+    cudaEventRecord(e0);
+    CK(cudaLaunchKernelEx(&cfg, kern, (const uint8_t*)buf, bytes, nchunks, mc, sink));
+    cudaEventRecord(e1); CK(cudaDeviceSynchronize());
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double delivered = (double)CHUNK * nchunks * grid;
+    double l2_unique = delivered / CS;
+    printf("cluster%d %s: delivered to SMEM %.2f TB/s (%.1f GB/s/SM), unique-data rate %.2f TB/s\n", CS,
+           mc ? "MULTICAST" : "unicast  ", delivered / (ms * 1e-3) / 1e12, delivered / grid / (ms * 1e-3) / 1e9,
+           l2_unique / (ms * 1e-3) / 1e12);
+  }
+}
+
 int main(int argc, char** argv) {
   setvbuf(stdout, NULL, _IONBF, 0);
   cudaDeviceProp p;
@@ -447,6 +522,10 @@ int main(int argc, char** argv) {
       printf("cluster4 %s load of shared 64KB chunks: delivered %.2f TB/s to SMEM (%.1f GB/s per SM)\n",
              mc ? "MULTICAST" : "unicast  ", delivered / (ms * 1e-3) / 1e12, delivered / grid / (ms * 1e-3) / 1e9);
     }
+    run_mc<1>(nsm, buf, bytes, sink);
+    run_mc<2>(nsm, buf, bytes, sink);
+    run_mc<4>(nsm, buf, bytes, sink);
+    run_mc<8>(nsm, buf, bytes, sink);
     cudaFree(buf);
     cudaFree(sink);
   }
