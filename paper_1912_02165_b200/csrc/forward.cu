@@ -1,0 +1,188 @@
+// forward.cu -- stage A, shared-memory-staged forward transform.
+//
+// One CTA = one 128-tile block x CPC channels.  The input rows the block's
+// tile rows need are staged into shared memory with coalesced loads and
+// explicit zero fill (implicit padding, reference kernels.py:73-86), so the
+// per-thread window reads need no bounds checks.  Thread = (tile, channel
+// pair); a warp covers 32/(CPC/2) consecutive tiles x CPC/2 pairs, so each
+// store instruction writes whole rows of the UMMA core matrices of the U
+// slab (csrc/common.cuh layout).  Launched with programmatic dependent
+// launch: the prologue overlaps the previous kernel's tail.
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "sm100.cuh"
+#include "staged.cuh"
+
+namespace wf {
+
+__device__ __forceinline__ void grid_dependency_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_dependents_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+struct FwdStage {
+  int wreg;      // staged row width  = (tiles_x - 1) * m + T
+  int trows;     // max tile rows touched by one block
+  int plane;     // floats per staged channel (padded)
+};
+
+template <int T, int CPC>
+__global__ void __launch_bounds__(64 * CPC, (T <= 6 && CPC <= 4) ? 2 : 1)
+forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo g, int blk0,
+                      int nblk_local, FwdStage S) {
+  extern __shared__ float xs[];
+  constexpr int PAIRS = CPC / 2;
+  constexpr int TPW = 32 / PAIRS;  // tiles per warp
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bl = blockIdx.x;
+  const int t0 = (blk0 + bl) * kBlockTiles;
+  const int cbase = blockIdx.y * CPC;
+  const int per_img = g.tiles_y * g.tiles_x;
+  const int gr0 = t0 / g.tiles_x;  // global tile-row index (b * tiles_y + ty)
+  const int tlast = min(t0 + kBlockTiles, g.n_tile) - 1;
+  const int nrows = tlast / g.tiles_x - gr0 + 1;
+
+  grid_dependency_wait();
+
+  // ---- stage the input rows of this block's tile rows, zero padded; one
+  // warp per staged row, lanes along the row (coalesced 128-byte loads)
+  const int row_elems = T * S.wreg;
+  const int total_rows = CPC * nrows * T;
+  for (int row = warp; row < total_rows; row += blockDim.x / 32) {
+    const int r = row % T;
+    const int j = (row / T) % nrows;
+    const int cl = row / (T * nrows);
+    const int gr = gr0 + j;
+    const int b = gr / g.tiles_y, ty = gr - b * g.tiles_y;
+    const int yy = ty * g.m - g.pad_lo + r;
+    const int c = cbase + cl;
+    const bool rok = c < g.C && yy >= 0 && yy < g.H && b < g.B;
+    const float* src = x + ((static_cast<size_t>(b) * g.C + c) * g.H + yy) * g.W - g.pad_lo;
+    float* dst = xs + cl * S.plane + j * row_elems + r * S.wreg;
+    for (int s = lane; s < S.wreg; s += 32) {
+      const int xx = s - g.pad_lo;
+      dst[s] = (rok && xx >= 0 && xx < g.W) ? __ldg(src + s) : 0.0f;
+    }
+  }
+  __syncthreads();
+
+  // ---- transform: thread = (tile tl, channel pair q)
+  const int tl = (warp % (kBlockTiles / TPW)) * TPW + lane % TPW;
+  const int q = (warp / (kBlockTiles / TPW)) * PAIRS + lane / TPW;  // always 0..PAIRS-1 here
+  const int tile = t0 + tl;
+  const int c0 = cbase + 2 * q;
+  float ua[T][T], ub[T][T];
+  if (tile < g.n_tile) {
+    const int b = tile / per_img;
+    const int rem = tile - b * per_img;
+    const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+    const int j = b * g.tiles_y + ty - gr0;
+    const float* base = xs + j * row_elems + tx * g.m;
+    float w[T][T];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float* pl = base + (2 * q + h) * S.plane;
+#pragma unroll
+      for (int r = 0; r < T; ++r)
+#pragma unroll
+        for (int s = 0; s < T; ++s) w[r][s] = pl[r * S.wreg + s];
+      if (h == 0) forward_transform<T>(w, ua);
+      else forward_transform<T>(w, ub);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < T; ++r)
+#pragma unroll
+      for (int s = 0; s < T; ++s) ua[r][s] = ub[r][s] = 0.0f;
+  }
+  const size_t slab = static_cast<size_t>(kBlockTiles) * g.Cpad * 2;
+  const uint32_t off = slab_off(tl, c0, kBlockTiles, g.Cpad);
+  uint8_t* dst = u + static_cast<size_t>(bl) * 2 * slab + off;
+  const size_t pstride = static_cast<size_t>(nblk_local) * 2 * slab;
+#pragma unroll
+  for (int r = 0; r < T; ++r)
+#pragma unroll
+    for (int s = 0; s < T; ++s) {
+      uint32_t hi, lo;
+      split_bf16x2(ua[r][s], ub[r][s], hi, lo);
+      uint8_t* p = dst + (r * T + s) * pstride;
+      *reinterpret_cast<uint32_t*>(p) = hi;
+      *reinterpret_cast<uint32_t*>(p + slab) = lo;
+    }
+}
+
+static FwdStage stage_geometry(const Geo& g) {
+  FwdStage S;
+  S.wreg = (g.tiles_x - 1) * g.m + g.T;
+  S.trows = ceil_div(kBlockTiles - 1, g.tiles_x) + 1;
+  if (S.trows > g.B * g.tiles_y) S.trows = g.B * g.tiles_y;
+  S.plane = round_up(S.trows * g.T * S.wreg, 32) + 4;
+  return S;
+}
+
+// Channels per CTA for the staged kernel (0 = does not fit: use the v1 kernel).
+int forward_staged_cpc(const Geo& g) {
+  const FwdStage S = stage_geometry(g);
+  // 8 channels (512 threads, <= 128 registers) only while the two T x T
+  // transforms of a thread fit; larger tiles use 256-thread CTAs.
+  // 4 channels per CTA first: 256-thread CTAs, two per SM, finer work items
+  // (better wave balance than 512-thread CTAs).
+  for (int cpc : {4, 8, 2})
+    if ((cpc < 8 || g.T <= 6) && static_cast<size_t>(cpc) * S.plane * 4 <= 100 * 1024 && g.Cpad % cpc == 0)
+      return cpc;
+  for (int cpc : {2})
+    if (static_cast<size_t>(cpc) * S.plane * 4 <= 200 * 1024) return cpc;
+  return 0;
+}
+
+template <int T, int CPC>
+static cudaError_t launch_staged(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk,
+                                 cudaStream_t st) {
+  const FwdStage S = stage_geometry(g);
+  const int smem = CPC * S.plane * 4;
+  auto kern = forward_staged_kernel<T, CPC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nblk, g.Cpad / CPC);
+  cfg.blockDim = dim3(64 * CPC);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, x, u, g, blk0, nblk, S);
+}
+
+template <int T>
+static cudaError_t launch_staged_t(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc,
+                                   cudaStream_t st) {
+  switch (cpc) {
+    case 8: return launch_staged<T, 8>(x, u, g, blk0, nblk, st);
+    case 4: return launch_staged<T, 4>(x, u, g, blk0, nblk, st);
+    case 2: return launch_staged<T, 2>(x, u, g, blk0, nblk, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_forward_staged(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc,
+                                  cudaStream_t st) {
+  switch (g.T) {
+    case 4: return launch_staged_t<4>(x, u, g, blk0, nblk, cpc, st);
+    case 5: return launch_staged_t<5>(x, u, g, blk0, nblk, cpc, st);
+    case 6: return launch_staged_t<6>(x, u, g, blk0, nblk, cpc, st);
+    case 7: return launch_staged_t<7>(x, u, g, blk0, nblk, cpc, st);
+    case 8: return launch_staged_t<8>(x, u, g, blk0, nblk, cpc, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace wf

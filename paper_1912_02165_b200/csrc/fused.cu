@@ -1,17 +1,27 @@
-// fused.cu -- conv_fused, version 1: L2-resident staged fusion.
+// fused.cu -- conv_fused: L2-resident staged fusion, wave-pipelined.
 //
 // The layer is processed in waves of 128-tile blocks sized so that a wave's
 // transformed tiles U (bf16 hi/lo) and transform-domain products M (f32)
-// stay resident in the 126 MB L2; the three stage kernels of staged.cu run
-// back to back on the stream for each wave.  The transformed data is written
-// and re-read inside L2 and never makes an HBM round trip, which is the
-// GPU analogue of the reference's shared-cache fusion (engines.py:317-444,
-// PAPER.md section 4: right-hand matrices and transformed tiles stay in the
-// shared last-level cache).  HBM traffic is therefore input + output + pack.
+// stay resident in the 126 MB L2; the three stage kernels (forward, position
+// GEMM, inverse) run back to back for each wave.  The transformed data is
+// written and re-read inside L2 and never makes an HBM round trip: HBM
+// traffic = input + output + pack.  This is the GPU analogue of the
+// reference's shared-cache fusion (engines.py:317-444; section 4:
+// transformed tiles stay in the shared last-level cache).
+//
+// Waves alternate between the caller's stream and one auxiliary stream, each
+// with its own U/M buffers, so wave w+1's forward transform runs on the SMs
+// left idle by wave w's GEMM / inverse tails (stage overlap without a
+// device-wide scheduler).  Fork/join through events keeps the call
+// stream-ordered for the caller.
+#include <mutex>
 #include "fused.cuh"
 #include "staged.cuh"
 
 namespace wf {
+
+static constexpr int kLanes = 2;                    // concurrent wave pipelines
+static constexpr size_t kL2Budget = 56ull << 20;    // U + M of all in-flight waves
 
 // Bytes of U + M for one 128-tile block.
 static size_t block_bytes(const Geo& g) {
@@ -20,33 +30,72 @@ static size_t block_bytes(const Geo& g) {
 }
 
 static int wave_blocks(const Geo& g) {
-  const size_t budget = 48ull << 20;  // well inside the 126 MB L2 next to the x / y streams
-  size_t nb = budget / block_bytes(g);
+  size_t nb = kL2Budget / kLanes / block_bytes(g);
   if (nb < 1) nb = 1;
   if (nb > static_cast<size_t>(g.n_blk)) nb = g.n_blk;
   return static_cast<int>(nb);
 }
 
 size_t fused_scratch_bytes(const Geo& g, int /*r*/) {
-  return static_cast<size_t>(wave_blocks(g)) * block_bytes(g);
+  if (persistent_fits(g)) return persistent_scratch_bytes(g);
+  return static_cast<size_t>(kLanes) * wave_blocks(g) * block_bytes(g);
+}
+
+struct LaneResources {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static LaneResources& lane_resources() {
+  static LaneResources res[64];
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  LaneResources& r = res[dev & 63];
+  if (!r.aux) {
+    cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
+  }
+  return r;
 }
 
 cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
                       int passes, int /*r*/, int sm_count, cudaStream_t st) {
+  if (persistent_fits(g)) return run_fused_persistent(x, vpack, y, scratch, g, passes, sm_count, st);
   const int wb = wave_blocks(g);
   const size_t P = static_cast<size_t>(g.T) * g.T;
-  uint8_t* U = scratch;
-  float* M = reinterpret_cast<float*>(scratch + P * wb * 2 * kBlockTiles * g.Cpad * 2);
-  for (int b0 = 0; b0 < g.n_blk; b0 += wb) {
+  const size_t lane_bytes = static_cast<size_t>(wb) * block_bytes(g);
+  const int n_waves = ceil_div(g.n_blk, wb);
+  const int lanes = n_waves > 1 ? kLanes : 1;
+  LaneResources& res = lane_resources();
+  cudaStream_t streams[kLanes] = {st, res.aux};
+  if (lanes > 1) {
+    cudaError_t e = cudaEventRecord(res.fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(res.aux, res.fork, 0);
+    if (e != cudaSuccess) return e;
+  }
+  for (int w = 0; w < n_waves; ++w) {
+    const int lane = w % lanes;
+    cudaStream_t s = streams[lane];
+    uint8_t* U = scratch + lane * lane_bytes;
+    float* M = reinterpret_cast<float*>(U + P * wb * 2 * kBlockTiles * g.Cpad * 2);
+    const int b0 = w * wb;
     const int nb = (g.n_blk - b0) < wb ? (g.n_blk - b0) : wb;
     const int tile0 = b0 * kBlockTiles;
     const int nvalid = (g.n_tile - tile0) < nb * kBlockTiles ? (g.n_tile - tile0) : nb * kBlockTiles;
     const int ldm = nb * kBlockTiles;
-    cudaError_t e = launch_forward_slab(x, U, g, b0, nb, st);
+    cudaError_t e = launch_forward_slab(x, U, g, b0, nb, s);
     if (e != cudaSuccess) return e;
-    e = launch_position_gemm(U, vpack, M, g, nb, ldm, nvalid, passes, sm_count, st);
+    e = launch_position_gemm(U, vpack, M, g, nb, ldm, nvalid, passes, sm_count, s);
     if (e != cudaSuccess) return e;
-    e = launch_inverse(M, y, g, tile0, nvalid, ldm, st);
+    e = launch_inverse(M, y, g, tile0, nvalid, ldm, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (lanes > 1) {
+    cudaError_t e = cudaEventRecord(res.join, res.aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, res.join, 0);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -8,6 +8,11 @@
 namespace wf {
 
 size_t fused_scratch_bytes(const Geo& g, int r);
+// Persistent dataflow kernel (fused_persistent.cu), used when C'pad <= 128.
+bool persistent_fits(const Geo& g);
+size_t persistent_scratch_bytes(const Geo& g);
+cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
+                                 int passes, int sm_count, cudaStream_t st);
 cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
                       int passes, int r, int sm_count, cudaStream_t st);
 

@@ -1,0 +1,687 @@
+// fused_persistent.cu -- conv_fused as ONE persistent dataflow kernel.
+//
+// The reference's fused engine (engines.py:317-444) hands tasks of R tiles
+// to worker threads from a locked cursor; each task runs forward ->
+// multiply -> inverse while its transformed tiles stay in cache.  Here one
+// CTA per SM pulls work items from a global atomic queue.  Three item kinds
+// per 128-tile block b:
+//   F(b, cg)  forward transform of CPC channels -> U ring slot (bf16 hi/lo
+//             UMMA slabs); input rows staged in smem with cp.async zero-fill
+//   G(b, gg)  tcgen05 GEMM for GP transform positions: M[p] = U[p] * V[p]
+//             (3xBF16, f32 accumulation in TMEM) -> M ring slot (f32)
+//   I(b, ig)  inverse transform + clipped store of a group of output channels
+// Items are dispensed in a lagged order -- F for block s, G for block s-L1,
+// I for block s-L2 at "step" s -- and each item waits (acquire on a
+// per-block counter) only on items dispensed earlier, so the queue can
+// never deadlock (an unscheduled CTA holds no item).  The rings (U: NU
+// slots, M: NM slots) are sized to stay resident in the 126 MB L2, so the
+// transformed tiles and products never make an HBM round trip, and all
+// three stages of different blocks run concurrently on different SMs with
+// no per-stage launch or tail.
+#include <cstdlib>
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "sm100.cuh"
+#include "fused.cuh"
+#include "staged.cuh"
+
+namespace wf {
+
+struct PersistParams {
+  const float* x;
+  float* y;
+  const uint8_t* vpack;   // MMA pack: per position hi / lo slabs of Cppad x Cpad
+  uint8_t* uring;         // NU slots x T^2 x (hi, lo) x 128 x Cpad bf16
+  float* mring;           // NM slots x T^2 x Cp x 128 f32
+  int* counters;          // [0] queue head, then doneF, doneG, doneI (n_blk each)
+  Geo g;
+  int n_cg, n_gg, n_ig;   // items per block of each kind
+  int cpc, gp, igc;       // channels per F item, positions per G item, c' per I item
+  int NU, NM, L1, L2;
+  int passes;
+  int n_steps, n_items;
+  int wreg, trows, plane; // F staging geometry
+  int wo_pad;             // I staging row pitch (floats)
+  int f_desc_off, f_max_rows;  // F row-descriptor table (bytes into smem, capacity)
+  int stages;                  // G smem pipeline depth
+  int f_bulk, f_shift;         // F staging by bulk copies; staged column of x = 0
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const int* p, int target) {
+  if (ld_acquire(p) >= target) return;
+  while (ld_acquire(p) < target) __nanosleep(64);
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Optional per-CTA item accounting (wait / run cycles per item kind) for
+// tuning; off unless WF_PROFILE is set.  Read with wf_debug_fused_profile().
+constexpr int kProfCtas = 512, kProfSlots = 16;
+__device__ unsigned long long g_prof[kProfCtas * kProfSlots];
+__constant__ int g_prof_on;
+// sub-phase marks (thread 0): slot 9 F staging, 10 F transform+store,
+// 11 I loads, 12 I transform+smem, 13 I write-back
+__device__ __forceinline__ void prof_mark(int slot, long long& t) {
+  if (g_prof_on && threadIdx.x == 0) {
+    const long long now = clock64();
+    g_prof[(blockIdx.x % kProfCtas) * kProfSlots + slot] += now - t;
+    t = now;
+  }
+}
+
+// Items active in step s, and the item -> (step, kind, sub) decode.
+__device__ __forceinline__ int items_in_step(const PersistParams& P, int s, int& nf, int& ng) {
+  const int nb = P.g.n_blk;
+  nf = (s < nb) ? P.n_cg : 0;
+  ng = (s >= P.L1 && s - P.L1 < nb) ? P.n_gg : 0;
+  const int ni = (s >= P.L2 && s - P.L2 < nb) ? P.n_ig : 0;
+  return nf + ng + ni;
+}
+
+struct GemmSync {
+  uint64_t full[3], empty[3], tfull[8];
+  uint64_t fbar;            // F-item staging (bulk copies)
+};
+
+// ------------------------------------------------------------------ F item
+template <int T, int NT>
+__device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t* smem, GemmSync& sy,
+                                 int fparity) {
+  const Geo& g = P.g;
+  float* xs = reinterpret_cast<float*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int CPC = P.cpc;
+  const int t0 = b * kBlockTiles;
+  const int cbase = cg * CPC;
+  const int gr0 = t0 / g.tiles_x;
+  const int tlast = min(t0 + kBlockTiles, g.n_tile) - 1;
+  const int nrows = tlast / g.tiles_x - gr0 + 1;
+  const int row_elems = T * P.wreg;
+  const int total_rows = CPC * nrows * T;
+  long long tprof = 0;
+  if (g_prof_on && tid == 0) tprof = clock64();
+  if (P.f_bulk) {
+    // Rows are 16-byte aligned in global memory (W % 4 == 0): every staged
+    // row is one bulk async copy of its W interior floats (column 4 of the
+    // staged row = x 0), completing on an mbarrier; pad columns and rows
+    // outside the image are zeroed with plain stores.  All copies are in
+    // flight at once -- one memory latency per item.
+    fence_proxy_async_smem();
+    for (int row = tid; row < total_rows; row += NT) {
+      const int r = row % T;
+      const int rest = row / T;
+      const int j = rest % nrows;
+      const int cl = rest / nrows;
+      const int gr = gr0 + j;
+      const int bi = gr / g.tiles_y, ty = gr - bi * g.tiles_y;
+      const int yy = ty * g.m - g.pad_lo + r;
+      const int c = cbase + cl;
+      float* dst = xs + cl * P.plane + j * row_elems + r * P.wreg;
+      if (c < g.C && yy >= 0 && yy < g.H && bi < g.B) {
+        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sy.fbar)),
+                     "r"(g.W * 4) : "memory");
+        bulk_g2s(dst + 4, P.x + ((static_cast<size_t>(bi) * g.C + c) * g.H + yy) * g.W, g.W * 4, &sy.fbar);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) dst[s] = 0.0f;
+        for (int s = 4 + g.W; s < P.wreg; ++s) dst[s] = 0.0f;
+      } else {
+        for (int s = 0; s < P.wreg; ++s) dst[s] = 0.0f;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) mbar_arrive(&sy.fbar);
+    mbar_wait(&sy.fbar, fparity);
+  } else {
+  // stage input rows (zero padded): one warp per row, lanes along the row
+  // (coalesced); ROWS rows per iteration so every thread has several
+  // independent loads in flight before it stores to shared memory
+  // (1) one descriptor per staged row (global row offset or -1 for a zero
+  // row, smem offset): the index divisions happen once per row, in parallel
+  long long* rsrc = reinterpret_cast<long long*>(smem + P.f_desc_off);
+  int* rdst = reinterpret_cast<int*>(rsrc + P.f_max_rows);
+  for (int row = tid; row < total_rows; row += NT) {
+    const int r = row % T;
+    const int rest = row / T;
+    const int j = rest % nrows;
+    const int cl = rest / nrows;
+    const int gr = gr0 + j;
+    const int bi = gr / g.tiles_y, ty = gr - bi * g.tiles_y;
+    const int yy = ty * g.m - g.pad_lo + r;
+    const int c = cbase + cl;
+    const bool rok = c < g.C && yy >= 0 && yy < g.H && bi < g.B;
+    rsrc[row] = rok ? ((static_cast<long long>(bi) * g.C + c) * g.H + yy) * g.W : -1;
+    rdst[row] = cl * P.plane + j * row_elems + r * P.wreg;
+  }
+  __syncthreads();
+  // (2) one warp per row, lanes along the row (coalesced), ROWS rows per
+  // iteration so each thread has several independent loads in flight
+  constexpr int ROWS = 4;
+  constexpr int NW = NT / 32;
+  const int lo_ok = g.pad_lo, hi_ok = g.pad_lo + g.W;       // staged column s holds x = s - pad_lo
+  for (int row0 = warp * ROWS; row0 < total_rows; row0 += NW * ROWS) {
+    for (int s0 = 0; s0 < P.wreg; s0 += 64) {
+      float v[ROWS][2];
+#pragma unroll
+      for (int k = 0; k < ROWS; ++k) {
+        const int row = row0 + k;
+        const long long src = row < total_rows ? rsrc[row] : -1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int s = s0 + lane + 32 * h;
+          v[k][h] = (src >= 0 && s >= lo_ok && s < hi_ok) ? __ldg(P.x + src + (s - g.pad_lo)) : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < ROWS; ++k) {
+        const int row = row0 + k;
+        if (row >= total_rows) break;
+        float* d = xs + rdst[row];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int s = s0 + lane + 32 * h;
+          if (s < P.wreg) d[s] = v[k][h];
+        }
+      }
+    }
+  }
+  }  // staging path
+  __syncthreads();
+  prof_mark(9, tprof);
+
+  const int pairs = CPC / 2;
+  const int tpw = 32 / pairs;
+  const int tl = (warp % (kBlockTiles / tpw)) * tpw + lane % tpw;
+  const int q = lane / tpw;
+  const int tile = t0 + tl;
+  const int c0 = cbase + 2 * q;
+  float ua[T][T], ub[T][T];
+  if (tile < g.n_tile && warp < 4 * pairs) {
+    const int per_img = g.tiles_y * g.tiles_x;
+    const int bi = tile / per_img;
+    const int rem = tile - bi * per_img;
+    const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+    const int j = bi * g.tiles_y + ty - gr0;
+    const float* base = xs + j * row_elems + tx * g.m - g.pad_lo + P.f_shift;
+    float w[T][T];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float* pl = base + (2 * q + h) * P.plane;
+#pragma unroll
+      for (int r = 0; r < T; ++r)
+#pragma unroll
+        for (int s = 0; s < T; ++s) w[r][s] = pl[r * P.wreg + s];
+      if (h == 0) forward_transform<T>(w, ua);
+      else forward_transform<T>(w, ub);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < T; ++r)
+#pragma unroll
+      for (int s = 0; s < T; ++s) ua[r][s] = ub[r][s] = 0.0f;
+  }
+  if (warp < 4 * pairs) {
+    const size_t slab = static_cast<size_t>(kBlockTiles) * g.Cpad * 2;
+    uint8_t* slot = P.uring + static_cast<size_t>(b % P.NU) * T * T * 2 * slab;
+    uint8_t* dst = slot + slab_off(tl, c0, kBlockTiles, g.Cpad);
+#pragma unroll
+    for (int r = 0; r < T; ++r)
+#pragma unroll
+      for (int s = 0; s < T; ++s) {
+        uint32_t hi, lo;
+        split_bf16x2(ua[r][s], ub[r][s], hi, lo);
+        uint8_t* p = dst + static_cast<size_t>(r * T + s) * 2 * slab;
+        *reinterpret_cast<uint32_t*>(p) = hi;
+        *reinterpret_cast<uint32_t*>(p + slab) = lo;
+      }
+  }
+  prof_mark(10, tprof);
+}
+
+// ------------------------------------------------------------------ G item
+// Pipeline over (position p of the group, K block j): stage = A K-block
+// (hi, lo) + V_p K-block (hi, lo).  Accumulator for position p = TMEM
+// columns [p_local * Cppad, +Cppad).
+
+
+// Barrier parities are derived from CTA-uniform counters (every thread keeps
+// identical copies): pipeline step K (over all G items of this CTA) uses
+// stage K % 3 with parity (K / 3) & 1; accumulator pl has been completed
+// tuse[pl] times before this item.
+template <int NT>
+__device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* smem, GemmSync& sy,
+                              uint32_t tmem, int gbase, const int (&tuse)[8]) {
+  const Geo& g = P.g;
+  const int warp = threadIdx.x >> 5;
+  const int n_kb = ceil_div(g.Cpad, kKBlock);
+  const int p0 = gg * P.gp;
+  const int np = min(P.gp, g.T * g.T - p0);
+  const uint32_t a_half = kBlockTiles * kKBlock * 2;
+  const uint32_t b_half = static_cast<uint32_t>(g.Cppad) * kKBlock * 2;
+  const uint32_t stage_bytes = 2 * a_half + 2 * b_half;
+  const size_t a_slab = static_cast<size_t>(kBlockTiles) * g.Cpad * 2;
+  const size_t v_slab = static_cast<size_t>(g.Cppad) * g.Cpad * 2;
+  const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * g.T * g.T * 2 * a_slab;
+  const int n_steps = np * n_kb;
+  if (warp == 0) {
+    if (lane_id() == 0) {
+      fence_proxy_async_smem();          // smem last written by generic stores (F items)
+      for (int k = 0; k < n_steps; ++k) {
+        const int K = gbase + k;
+        const int pl = k / n_kb, j = k - pl * n_kb;
+        const int p = p0 + pl;
+        const int st = K % P.stages;
+        mbar_wait(&sy.empty[st], ((K / P.stages) & 1) ^ 1);
+        const uint32_t kc = kblock_width(g.Cpad, j);
+        uint8_t* sb = smem + st * stage_bytes;
+        const uint32_t abytes = kBlockTiles * kc * 2, bbytes = g.Cppad * kc * 2;
+        mbar_expect_tx(&sy.full[st], 2 * abytes + (P.passes > 1 ? 2 : 1) * bbytes);
+        const uint8_t* a_src = uslot + static_cast<size_t>(p) * 2 * a_slab + kblock_off(j, kBlockTiles);
+        const uint8_t* b_src = P.vpack + static_cast<size_t>(p) * 2 * v_slab + kblock_off(j, g.Cppad);
+        bulk_g2s(sb, a_src, abytes, &sy.full[st]);
+        bulk_g2s(sb + a_half, a_src + a_slab, abytes, &sy.full[st]);
+        bulk_g2s(sb + 2 * a_half, b_src, bbytes, &sy.full[st]);
+        if (P.passes > 1) bulk_g2s(sb + 2 * a_half + b_half, b_src + v_slab, bbytes, &sy.full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16(kBlockTiles, g.Cppad);
+    for (int k = 0; k < n_steps; ++k) {
+      const int K = gbase + k;
+      const int pl = k / n_kb, j = k - pl * n_kb;
+      const int st = K % P.stages;
+      mbar_wait(&sy.full[st], (K / P.stages) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t kc = kblock_width(g.Cpad, j);
+        const uint32_t sa = smem_u32(smem + st * stage_bytes);
+        const uint32_t sbb = sa + 2 * a_half;
+        const uint32_t sbo = 16 * kc;
+        const uint32_t dcol = tmem + pl * g.Cppad;
+        for (uint32_t s = 0; s < kc / 16; ++s) {
+          const uint64_t ahi = smem_desc(sa + s * 256, 128, sbo);
+          const uint64_t alo = smem_desc(sa + a_half + s * 256, 128, sbo);
+          const uint64_t bhi = smem_desc(sbb + s * 256, 128, sbo);
+          const uint64_t blo = smem_desc(sbb + b_half + s * 256, 128, sbo);
+          const uint32_t first = (j == 0 && s == 0) ? 0u : 1u;
+          if (P.passes > 1) {
+            mma_bf16_ss(dcol, alo, bhi, idesc, first);
+            mma_bf16_ss(dcol, ahi, blo, idesc, 1u);
+            mma_bf16_ss(dcol, ahi, bhi, idesc, 1u);
+          } else {
+            mma_bf16_ss(dcol, ahi, bhi, idesc, first);
+          }
+        }
+        mma_commit(&sy.empty[st]);
+        if (j == n_kb - 1) mma_commit(&sy.tfull[pl]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 8) {
+    const int qd = warp & 3;
+    const int row = qd * 32 + lane_id();
+    const int tile = b * kBlockTiles + row;
+    float* mslot = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * g.Cp * kBlockTiles;
+    for (int pl = 0; pl < np; ++pl) {
+      mbar_wait(&sy.tfull[pl], tuse[pl] & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) + pl * g.Cppad;
+      float* mrow = mslot + static_cast<size_t>(p0 + pl) * g.Cp * kBlockTiles + row;
+      for (int c = 0; c < g.Cppad; c += 16) {
+        float v[16];
+        tmem_ld16(taddr + c, v);
+        tmem_ld_wait();
+        if (tile < g.n_tile) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c + i < g.Cp) __stcg(mrow + static_cast<size_t>(c + i) * kBlockTiles, v[i]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+}
+
+// ------------------------------------------------------------------ I item
+// Thread = (TPT consecutive tiles, c'): vector loads of the products, inverse
+// transform, then the m x m blocks are staged in shared memory in output-row
+// order and written back by whole warps along output rows (coalesced), only
+// for the columns this block's tiles own in each tile row.
+template <int T, int NT>
+__device__ void run_inverse_item(const PersistParams& P, int b, int ig, uint8_t* smem) {
+  const Geo& g = P.g;
+  constexpr int TPT = T <= 5 ? 4 : 2;        // tiles per thread (register budget)
+  constexpr int QUADS = kBlockTiles / TPT;
+  constexpr int MO = T - 2;
+  float* ys = reinterpret_cast<float*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = b * kBlockTiles;
+  const int gr0 = t0 / g.tiles_x;
+  const int tend = min(t0 + kBlockTiles, g.n_tile);
+  const int nrows = (tend - 1) / g.tiles_x - gr0 + 1;
+  const int wo_pad = P.wo_pad;
+  const int cpl = tid / QUADS;              // c' within the group
+  const int quad = tid % QUADS;
+  const int cp = ig * P.igc + cpl;
+  const int tl0 = quad * TPT;
+  const int tile0 = t0 + tl0;
+  long long tprof = 0;
+  if (g_prof_on && tid == 0) tprof = clock64();
+  if (cpl < P.igc && cp < g.Cp && tile0 < g.n_tile) {
+    const float* mslot = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * g.Cp * kBlockTiles;
+    const float* src = mslot + static_cast<size_t>(cp) * kBlockTiles + tl0;
+    const size_t pstride = static_cast<size_t>(g.Cp) * kBlockTiles;
+    float mm[TPT][T][T];
+#pragma unroll
+    for (int r = 0; r < T; ++r)
+#pragma unroll
+      for (int s = 0; s < T; ++s) {
+        if constexpr (TPT == 4) {
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(src + (r * T + s) * pstride));
+          mm[0][r][s] = v.x; mm[1][r][s] = v.y; mm[2][r][s] = v.z; mm[3][r][s] = v.w;
+        } else {
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(src + (r * T + s) * pstride));
+          mm[0][r][s] = v.x; mm[1][r][s] = v.y;
+        }
+      }
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+      const int tile = tile0 + k;
+      if (tile >= g.n_tile) break;
+      float out[MO][MO];
+      inverse_transform<T>(mm[k], out);
+      const int gr = tile / g.tiles_x;
+      const int tx = tile - gr * g.tiles_x;
+      float* dst = ys + ((cpl * nrows + (gr - gr0)) * MO) * wo_pad + tx * MO;
+#pragma unroll
+      for (int r = 0; r < MO; ++r)
+#pragma unroll
+        for (int s = 0; s < MO; ++s) dst[r * wo_pad + s] = out[r][s];
+    }
+  }
+  prof_mark(11, tprof);
+  __syncthreads();
+  prof_mark(12, tprof);
+  // coalesced write-back: one warp per (c', tile row), all MO output rows,
+  // lanes along x; only the columns this block's tiles own
+  const int total = P.igc * nrows;
+  for (int q = warp; q < total; q += NT / 32) {
+    const int j = q % nrows;
+    const int c = q / nrows;
+    const int cpo = ig * P.igc + c;
+    if (cpo >= g.Cp) continue;
+    const int gr = gr0 + j;
+    const int bi = gr / g.tiles_y, ty = gr - bi * g.tiles_y;
+    const int tlo = max(t0, gr * g.tiles_x), thi = min(tend, (gr + 1) * g.tiles_x);
+    const int xlo = (tlo - gr * g.tiles_x) * MO;
+    const int xhi = min((thi - gr * g.tiles_x) * MO, g.Wo);
+    const float* sbase = ys + (c * nrows + j) * MO * wo_pad;
+    float* dbase = P.y + ((static_cast<size_t>(bi) * g.Cp + cpo) * g.Ho + ty * MO) * g.Wo;
+#pragma unroll
+    for (int r = 0; r < MO; ++r) {
+      if (ty * MO + r >= g.Ho) break;
+      for (int xx = xlo + lane; xx < xhi; xx += 32) dbase[r * g.Wo + xx] = sbase[r * wo_pad + xx];
+    }
+  }
+  prof_mark(13, tprof);
+}
+
+// ------------------------------------------------------------------ kernel
+template <int T, int NT, int CPS>
+__global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ GemmSync sy;
+  __shared__ uint32_t tmem_slot;
+  __shared__ int item_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nb = P.g.n_blk;
+  int* head = P.counters;
+  int* doneF = P.counters + 1;
+  int* doneG = doneF + nb;
+  int* doneI = doneG + nb;
+  if (tid == 0) {
+    for (int s = 0; s < 3; ++s) { mbar_init(&sy.full[s], 1); mbar_init(&sy.empty[s], 1); }
+    for (int a = 0; a < 8; ++a) mbar_init(&sy.tfull[a], 1);
+    mbar_init(&sy.fbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512 / CPS>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  int fcount = 0;             // F items so far (staging-barrier parity)
+  int gsteps = 0;              // pipeline steps of all G items so far (CTA-uniform)
+  int tuse[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int n_kb = ceil_div(P.g.Cpad, kKBlock);
+
+  int step = 0, step_base = 0, nf = 0, ng = 0;
+  int next_item = 0;
+  if (tid == 0) next_item = atomicAdd(head, 1);
+  int step_items = items_in_step(P, 0, nf, ng);
+  for (;;) {
+    // the next item index is fetched while this one runs (hides the atomic's
+    // round trip); dependencies only point backwards, so holding one
+    // prefetched item cannot deadlock the queue
+    if (tid == 0) {
+      item_s = next_item;
+      next_item = atomicAdd(head, 1);
+    }
+    __syncthreads();
+    const int item = item_s;
+    __syncthreads();
+    if (item >= P.n_items) break;
+    while (item >= step_base + step_items) {   // items are handed out in increasing order
+      step_base += step_items;
+      ++step;
+      step_items = items_in_step(P, step, nf, ng);
+    }
+    const int k = item - step_base;
+    long long t_a = 0, t_b = 0;
+    const int kind = k < nf ? 0 : (k < nf + ng ? 1 : 2);
+    if (g_prof_on && tid == 0) t_a = clock64();
+    if (k < nf) {                                          // ---- F(step, k)
+      const int b = step;
+      if (tid == 0 && b >= P.NU) spin_until(doneG + (b - P.NU), P.n_gg);
+      if (g_prof_on && tid == 0) t_b = clock64();
+      __syncthreads();
+      run_forward_item<T, NT>(P, b, k, smem, sy, fcount & 1);
+      ++fcount;
+      __syncthreads();
+      if (tid == 0) { __threadfence(); atomicAdd(doneF + b, 1); }
+    } else if (k < nf + ng) {                              // ---- G(step - L1, k - nf)
+      const int b = step - P.L1;
+      if (tid == 0) {
+        spin_until(doneF + b, P.n_cg);
+        if (b >= P.NM) spin_until(doneI + (b - P.NM), P.n_ig);
+        fence_proxy_async_global();
+        if (g_prof_on) t_b = clock64();
+      }
+      __syncthreads();
+      tc_fence_after();
+      const int gg = k - nf;
+      run_gemm_item<NT>(P, b, gg, smem, sy, tmem, gsteps, tuse);
+      const int np = min(P.gp, P.g.T * P.g.T - gg * P.gp);
+      gsteps += np * n_kb;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tuse[i] += (i < np) ? 1 : 0;
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) { __threadfence(); atomicAdd(doneG + b, 1); }
+    } else {                                               // ---- I(step - L2, k - nf - ng)
+      const int b = step - P.L2;
+      if (tid == 0) spin_until(doneG + b, P.n_gg);
+      if (g_prof_on && tid == 0) t_b = clock64();
+      __syncthreads();
+      run_inverse_item<T, NT>(P, b, k - nf - ng, smem);
+      __syncthreads();
+      if (tid == 0) { __threadfence(); atomicAdd(doneI + b, 1); }
+    }
+    if (g_prof_on && tid == 0) {
+      unsigned long long* pr = g_prof + (blockIdx.x % kProfCtas) * kProfSlots + kind * 3;
+      pr[0] += t_b - t_a;
+      pr[1] += clock64() - t_b;
+      pr[2] += 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512 / CPS>(tmem);
+}
+
+// ------------------------------------------------------------------ host
+struct PersistPlan {
+  bool ok;
+  int cpc, gp, igc, n_cg, n_gg, n_ig, NU, NM, L1, L2, wreg, trows, plane, nt, wo_pad, f_desc_off, f_max_rows, cps, stages;
+  int f_bulk, f_shift;
+  size_t u_slot, m_slot, counters_bytes, smem;
+};
+
+static PersistPlan persist_plan(const Geo& g) {
+  PersistPlan pl = {};
+  pl.nt = 256;
+  pl.cps = g.T <= 6 ? 2 : 1;              // CTAs per SM (two overlap each other's latency)
+  pl.stages = pl.cps == 2 ? 2 : 3;
+  pl.cpc = pl.nt / 64;                     // 128 tiles x cpc/2 pairs = nt threads
+  if (g.Cpad % pl.cpc != 0 || g.Cppad > 128) return pl;
+  pl.gp = (512 / pl.cps) / g.Cppad;
+  if (pl.gp > 8) pl.gp = 8;
+  if (pl.gp > g.T * g.T) pl.gp = g.T * g.T;
+  pl.igc = pl.nt * (g.T <= 5 ? 4 : 2) / kBlockTiles;   // threads = 128/TPT tile groups x igc c'
+  pl.n_cg = g.Cpad / pl.cpc;
+  pl.n_gg = ceil_div(g.T * g.T, pl.gp);
+  pl.n_ig = ceil_div(g.Cp, pl.igc);
+  pl.wreg = (g.tiles_x - 1) * g.m + g.T;
+  // bulk-copy staging needs 16-byte aligned input rows; staged column 4 = x 0
+  pl.f_bulk = (g.W % 4 == 0) ? 1 : 0;
+  pl.f_shift = pl.f_bulk ? 4 : g.pad_lo;
+  if (pl.f_bulk) {
+    const int need = (g.W > pl.wreg - g.pad_lo ? g.W : pl.wreg - g.pad_lo) + 4;
+    pl.wreg = round_up(need, 4);
+  }
+  pl.trows = ceil_div(kBlockTiles - 1, g.tiles_x) + 1;
+  if (pl.trows > g.B * g.tiles_y) pl.trows = g.B * g.tiles_y;
+  // plane pitch = 1 (mod 32) words: the 4 channel pairs of a warp land on
+  // different banks (2-way instead of 4-way conflicts on the window reads)
+  // (bulk-copy staging needs 16-byte aligned rows: pitch = 4 mod 32 instead)
+  pl.plane = round_up(pl.trows * g.T * pl.wreg, 32) + (pl.f_bulk ? 4 : 1);
+  pl.f_max_rows = pl.cpc * pl.trows * g.T;
+  pl.f_desc_off = round_up(pl.cpc * pl.plane * 4, 16);
+  const size_t f_smem = pl.f_desc_off + static_cast<size_t>(pl.f_max_rows) * 12;
+  pl.wo_pad = round_up(pl.wreg, 4) + 1;     // >= tiles_x * m >= W'
+  const size_t i_smem = static_cast<size_t>(pl.igc) * pl.trows * g.m * pl.wo_pad * 4;
+  const size_t g_smem = pl.stages * (2 * kBlockTiles * kKBlock * 2 + 2 * static_cast<size_t>(g.Cppad) * kKBlock * 2);
+  pl.smem = f_smem > g_smem ? f_smem : g_smem;
+  if (i_smem > pl.smem) pl.smem = i_smem;
+  if (pl.smem > (pl.cps == 2 ? 108u : 200u) * 1024) return pl;
+  pl.u_slot = static_cast<size_t>(g.T) * g.T * 2 * kBlockTiles * g.Cpad * 2;
+  pl.m_slot = static_cast<size_t>(g.T) * g.T * g.Cp * kBlockTiles * 4;
+  // lags and ring sizes: ~a machine-full of items in flight between stages,
+  // rings within an L2 budget
+  // A "window" = the blocks whose items occupy all CTAs at once.  Producers
+  // run `lag` steps ahead of consumers; a ring slot is reused only after
+  // lag + window more steps, so neither side normally waits.
+  // measured on B200 (c2): rings below ~64 MB starve the pipeline; 100 MB of
+  // the 126 MB L2 with lag 8 was the best point (tools/item_profile.py sweep)
+  size_t budget = 100ull << 20;
+  if (const char* env = getenv("WF_L2_BUDGET_MB")) budget = static_cast<size_t>(atoi(env)) << 20;
+  const int items_per_block = pl.n_cg + pl.n_gg + pl.n_ig;
+  const int window = ceil_div(148 * pl.cps, items_per_block) + 1;
+  int lag = window < 8 ? window : 8;
+  if (const char* env = getenv("WF_LAG")) lag = atoi(env);
+  const int slots = static_cast<int>(budget / (pl.u_slot + pl.m_slot));
+  if (slots < 4) return pl;
+  if (2 * (lag + window) > slots) lag = slots / 2 - window;
+  if (lag < 1) lag = 1;
+  pl.L1 = lag;
+  pl.L2 = 2 * lag;
+  pl.NU = slots / 2;
+  pl.NM = slots - pl.NU;
+  if (pl.NU < pl.L1 + 1) pl.NU = pl.L1 + 1;
+  if (pl.NM < pl.L2 - pl.L1 + 1) pl.NM = pl.L2 - pl.L1 + 1;
+  if (pl.NU > g.n_blk) pl.NU = g.n_blk;
+  if (pl.NM > g.n_blk) pl.NM = g.n_blk;
+  if (pl.NU <= pl.L1 && pl.NU < g.n_blk) return pl;
+  pl.counters_bytes = static_cast<size_t>(1 + 3 * g.n_blk) * sizeof(int);
+  pl.ok = true;
+  return pl;
+}
+
+bool persistent_fits(const Geo& g) { return persist_plan(g).ok; }
+
+size_t persistent_scratch_bytes(const Geo& g) {
+  const PersistPlan pl = persist_plan(g);
+  if (!pl.ok) return 0;
+  return round_up(static_cast<int>(pl.counters_bytes), 1024) + pl.NU * pl.u_slot + pl.NM * pl.m_slot;
+}
+
+template <int T, int NT, int CPS>
+static cudaError_t launch_persist_t(const PersistParams& P, size_t smem, int grid, cudaStream_t st) {
+  auto kern = fused_persistent_kernel<T, NT, CPS>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<grid, NT, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
+                                 int passes, int sm_count, cudaStream_t st) {
+  const PersistPlan pl = persist_plan(g);
+  if (!pl.ok) return cudaErrorInvalidValue;
+  PersistParams P;
+  P.x = x; P.y = y; P.vpack = vpack;
+  P.counters = reinterpret_cast<int*>(scratch);
+  P.uring = scratch + round_up(static_cast<int>(pl.counters_bytes), 1024);
+  P.mring = reinterpret_cast<float*>(P.uring + pl.NU * pl.u_slot);
+  P.g = g;
+  P.n_cg = pl.n_cg; P.n_gg = pl.n_gg; P.n_ig = pl.n_ig;
+  P.cpc = pl.cpc; P.gp = pl.gp; P.igc = pl.igc;
+  P.NU = pl.NU; P.NM = pl.NM; P.L1 = pl.L1; P.L2 = pl.L2;
+  P.passes = passes;
+  P.n_steps = g.n_blk + pl.L2;
+  P.n_items = g.n_blk * (pl.n_cg + pl.n_gg + pl.n_ig);
+  P.wreg = pl.wreg; P.trows = pl.trows; P.plane = pl.plane; P.wo_pad = pl.wo_pad;
+  P.f_desc_off = pl.f_desc_off; P.f_max_rows = pl.f_max_rows;
+  P.f_bulk = pl.f_bulk; P.f_shift = pl.f_shift;
+  cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
+  if (e != cudaSuccess) return e;
+  {
+    static int prof_state = -1;
+    if (prof_state < 0) {
+      prof_state = getenv("WF_PROFILE") ? 1 : 0;
+      cudaMemcpyToSymbol(g_prof_on, &prof_state, sizeof(int));
+    }
+  }
+  const int grid = sm_count * pl.cps;
+  P.stages = pl.stages;
+  switch (g.T) {
+    case 4: return launch_persist_t<4, 256, 2>(P, pl.smem, grid, st);
+    case 5: return launch_persist_t<5, 256, 2>(P, pl.smem, grid, st);
+    case 6: return launch_persist_t<6, 256, 2>(P, pl.smem, grid, st);
+    case 7: return launch_persist_t<7, 256, 1>(P, pl.smem, grid, st);
+    case 8: return launch_persist_t<8, 256, 1>(P, pl.smem, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace wf
+
+// Debug/tuning hook (not part of the public ABI): copy the per-CTA item
+// accounting [cta][kind F,G,I][wait cycles, run cycles, count] and reset it.
+extern "C" int wf_debug_fused_profile(unsigned long long* host, int n) {
+  using namespace wf;
+  const int cnt = n < kProfCtas * kProfSlots ? n : kProfCtas * kProfSlots;
+  cudaError_t e = cudaMemcpyFromSymbol(host, wf::g_prof, cnt * sizeof(unsigned long long));
+  static unsigned long long zeros[kProfCtas * kProfSlots] = {0};
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(wf::g_prof, zeros, sizeof(zeros));
+  return e == cudaSuccess ? 0 : 4;
+}

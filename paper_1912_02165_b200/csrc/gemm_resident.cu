@@ -1,0 +1,292 @@
+// gemm_resident.cu -- stage B when a whole transformed-kernel position fits
+// in shared memory: position-major persistent tcgen05 GEMM.
+//
+// Work items (p, block) are ordered position-major and every CTA takes one
+// contiguous run of them, so a CTA keeps V_p (hi + lo, all K blocks) resident
+// in shared memory across all the blocks it multiplies for position p -- the
+// GPU form of the paper's "right-hand matrix stays in cache" (PAPER.md
+// section 4, reference engines.py:279-289 one position at a time).  Only the
+// transformed tiles U stream in, through a 4-deep mbarrier pipeline of
+// bulk async copies; accumulators rotate through 4 TMEM buffers so the
+// epilogue of block k overlaps the MMAs of block k+1.
+//   warp 0: producer, warp 1: TMEM alloc + MMA issuer, warps 2..5: epilogue.
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "sm100.cuh"
+#include "staged.cuh"
+
+namespace wf {
+
+constexpr int kResThreads = 192;
+constexpr int kResStages = 4;
+constexpr int kResAcc = 4;
+
+struct ResParams {
+  const uint8_t* U;
+  const uint8_t* V;
+  float* M;
+  int n_pos, n_blk, Cpad, Cppad, Cp;
+  int ldm, n_valid, passes;
+};
+
+__global__ void __launch_bounds__(kResThreads, 1) gemm_resident_kernel(ResParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full_bar[kResStages], empty_bar[kResStages], tfull[kResAcc], tempty[kResAcc];
+  __shared__ uint64_t vfull, vempty;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5;
+  const int n_kb = ceil_div(P.Cpad, kKBlock);
+  const uint32_t v_half = static_cast<uint32_t>(P.Cppad) * P.Cpad * 2;    // one of hi / lo
+  const uint32_t a_half = kBlockTiles * kKBlock * 2;
+  uint8_t* vbuf = smem;
+  uint8_t* abuf = smem + round_up(2 * v_half, 1024);
+  const int NC = P.Cppad;
+  const uint32_t tcols = NC * kResAcc <= 256 ? 256 : 512;
+  const int n_items = P.n_pos * P.n_blk;
+  const int lo_it = static_cast<int>((static_cast<long long>(n_items) * blockIdx.x) / gridDim.x);
+  const int hi_it = static_cast<int>((static_cast<long long>(n_items) * (blockIdx.x + 1)) / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kResStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int a = 0; a < kResAcc; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    mbar_init(&vfull, 1);
+    mbar_init(&vempty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    if (tcols == 256) tmem_alloc<256>(&tmem_slot);
+    else tmem_alloc<512>(&tmem_slot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  const size_t a_slab = static_cast<size_t>(kBlockTiles) * P.Cpad * 2;
+  if (warp == 0) {
+    if (lane_id() == 0) {
+      int stage = 0, cur_p = -1;
+      uint32_t phase = 0, vphase = 0;
+      for (int it = lo_it; it < hi_it; ++it) {
+        const int p = it / P.n_blk, blk = it - p * P.n_blk;
+        if (p != cur_p) {
+          if (cur_p >= 0) { mbar_wait(&vempty, vphase); vphase ^= 1; }
+          const uint8_t* vsrc = P.V + static_cast<size_t>(p) * 2 * v_half;
+          mbar_expect_tx(&vfull, (P.passes > 1 ? 2 : 1) * v_half);
+          bulk_g2s(vbuf, vsrc, v_half, &vfull);
+          if (P.passes > 1) bulk_g2s(vbuf + v_half, vsrc + v_half, v_half, &vfull);
+          cur_p = p;
+        }
+        const uint8_t* a_src = P.U + (static_cast<size_t>(p) * P.n_blk + blk) * 2 * a_slab;
+        for (int j = 0; j < n_kb; ++j) {
+          const uint32_t kc = kblock_width(P.Cpad, j);
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = abuf + stage * 2 * a_half;
+          const uint32_t bytes = kBlockTiles * kc * 2;
+          mbar_expect_tx(&full_bar[stage], 2 * bytes);
+          const size_t aoff = kblock_off(j, kBlockTiles);
+          bulk_g2s(st, a_src + aoff, bytes, &full_bar[stage]);
+          bulk_g2s(st + a_half, a_src + a_slab + aoff, bytes, &full_bar[stage]);
+          if (++stage == kResStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16(kBlockTiles, NC);
+    int stage = 0, acc = 0, cur_p = -1;
+    uint32_t phase = 0, acc_phase = 0, vphase = 0;
+    for (int it = lo_it; it < hi_it; ++it) {
+      const int p = it / P.n_blk;
+      if (p != cur_p) {
+        mbar_wait(&vfull, vphase);
+        vphase ^= 1;
+        cur_p = p;
+      }
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tmem + acc * NC;
+      const bool last_of_p = (it + 1 == hi_it) || ((it + 1) / P.n_blk != p);
+      for (int j = 0; j < n_kb; ++j) {
+        const uint32_t kc = kblock_width(P.Cpad, j);
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t st = smem_u32(abuf + stage * 2 * a_half);
+          const uint32_t vb = smem_u32(vbuf) + kblock_off(j, P.Cppad);
+          const uint32_t sbo = 16 * kc;
+          for (uint32_t s = 0; s < kc / 16; ++s) {
+            const uint64_t ahi = smem_desc(st + s * 256, 128, sbo);
+            const uint64_t alo = smem_desc(st + a_half + s * 256, 128, sbo);
+            const uint64_t bhi = smem_desc(vb + s * 256, 128, sbo);
+            const uint64_t blo = smem_desc(vb + v_half + s * 256, 128, sbo);
+            const uint32_t first = (j == 0 && s == 0) ? 0u : 1u;
+            if (P.passes > 1) {
+              mma_bf16_ss(dcol, alo, bhi, idesc, first);
+              mma_bf16_ss(dcol, ahi, blo, idesc, 1u);
+              mma_bf16_ss(dcol, ahi, bhi, idesc, 1u);
+            } else {
+              mma_bf16_ss(dcol, ahi, bhi, idesc, first);
+            }
+          }
+          mma_commit(&empty_bar[stage]);
+          if (j == n_kb - 1) {
+            mma_commit(&tfull[acc]);
+            if (last_of_p) mma_commit(&vempty);
+          }
+        }
+        __syncwarp();
+        if (++stage == kResStages) { stage = 0; phase ^= 1; }
+      }
+      if (++acc == kResAcc) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane_id();
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int it = lo_it; it < hi_it; ++it) {
+      const int p = it / P.n_blk, blk = it - p * P.n_blk;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int tile = blk * kBlockTiles + row;
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * NC;
+      float* mrow = P.M + static_cast<size_t>(p) * P.Cp * P.ldm + tile;
+      for (int c = 0; c < NC; c += 16) {
+        float v[16];
+        tmem_ld16(taddr + c, v);
+        tmem_ld_wait();
+        if (tile < P.n_valid) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c + i < P.Cp) mrow[static_cast<size_t>(c + i) * P.ldm] = v[i];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == kResAcc) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    if (tcols == 256) tmem_dealloc<256>(tmem);
+    else tmem_dealloc<512>(tmem);
+  }
+}
+
+size_t gemm_resident_smem(const Geo& g) {
+  const size_t v = static_cast<size_t>(g.Cppad) * g.Cpad * 2 * 2;
+  return round_up(static_cast<int>(v), 1024) + kResStages * 2 * kBlockTiles * kKBlock * 2;
+}
+
+bool gemm_resident_fits(const Geo& g) {
+  return g.Cppad <= 128 && gemm_resident_smem(g) <= 200 * 1024;
+}
+
+cudaError_t launch_gemm_resident(const uint8_t* U, const uint8_t* V, float* M, const Geo& g, int nblk,
+                                 int ldm, int n_valid, int passes, int sm_count, cudaStream_t st) {
+  ResParams P;
+  P.U = U; P.V = V; P.M = M;
+  P.n_pos = g.T * g.T; P.n_blk = nblk;
+  P.Cpad = g.Cpad; P.Cppad = g.Cppad; P.Cp = g.Cp;
+  P.ldm = ldm; P.n_valid = n_valid; P.passes = passes;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int n_items = P.n_pos * nblk;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_items < sm_count ? n_items : sm_count);
+  cfg.blockDim = dim3(kResThreads);
+  cfg.dynamicSmemBytes = gemm_resident_smem(g);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_resident_kernel, P);
+}
+
+// ------------------------------------------------------------ stage C, v2
+// Thread = (TPT consecutive tiles, c'): vector loads of M[p][c'][tile..]
+// (tiles are contiguous, ldm is a multiple of 128) so a warp moves
+// 32 * TPT * 4 bytes per position per instruction.
+template <int T, int TPT>
+__global__ void __launch_bounds__(128) inverse_vec_kernel(const float* __restrict__ M, float* __restrict__ y,
+                                                          Geo g, int tile0, int ntile_local, int ldm) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int tq = (blockIdx.x * blockDim.x + threadIdx.x) * TPT;
+  const int cp = blockIdx.y;
+  if (tq >= ntile_local) return;
+  constexpr int MO = T - 2;
+  float mm[TPT][T][T];
+  const float* src = M + static_cast<size_t>(cp) * ldm + tq;
+  const size_t pstride = static_cast<size_t>(g.Cp) * ldm;
+#pragma unroll
+  for (int r = 0; r < T; ++r)
+#pragma unroll
+    for (int s = 0; s < T; ++s) {
+      const float* ptr = src + (r * T + s) * pstride;
+      if constexpr (TPT == 4) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(ptr));
+        mm[0][r][s] = v.x; mm[1][r][s] = v.y; mm[2][r][s] = v.z; mm[3][r][s] = v.w;
+      } else {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(ptr));
+        mm[0][r][s] = v.x; mm[1][r][s] = v.y;
+      }
+    }
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int tl = tq + k;
+    if (tl >= ntile_local) break;
+    float out[MO][MO];
+    inverse_transform<T>(mm[k], out);
+    int b, ty, tx;
+    tile_coords(g, tile0 + tl, b, ty, tx);
+    const int oy = ty * g.m, ox = tx * g.m;
+    float* plane = y + (static_cast<size_t>(b) * g.Cp + cp) * g.Ho * g.Wo;
+#pragma unroll
+    for (int r = 0; r < MO; ++r) {
+      if (oy + r >= g.Ho) break;
+#pragma unroll
+      for (int s = 0; s < MO; ++s)
+        if (ox + s < g.Wo) plane[static_cast<size_t>(oy + r) * g.Wo + ox + s] = out[r][s];
+    }
+  }
+}
+
+template <int T>
+static cudaError_t launch_inv_vec_t(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
+                                    cudaStream_t st) {
+  constexpr int TPT = T <= 6 ? 4 : 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ceil_div(ceil_div(ntile, TPT), 128), g.Cp);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, inverse_vec_kernel<T, TPT>, M, y, g, tile0, ntile, ldm);
+}
+
+cudaError_t launch_inverse_vec(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
+                               cudaStream_t st) {
+  switch (g.T) {
+    case 4: return launch_inv_vec_t<4>(M, y, g, tile0, ntile, ldm, st);
+    case 5: return launch_inv_vec_t<5>(M, y, g, tile0, ntile, ldm, st);
+    case 6: return launch_inv_vec_t<6>(M, y, g, tile0, ntile, ldm, st);
+    case 7: return launch_inv_vec_t<7>(M, y, g, tile0, ntile, ldm, st);
+    case 8: return launch_inv_vec_t<8>(M, y, g, tile0, ntile, ldm, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace wf

@@ -281,6 +281,8 @@ static cudaError_t launch_forward_t(const float* x, uint8_t* u, const Geo& g, in
 
 cudaError_t launch_forward_slab(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk,
                                 cudaStream_t st) {
+  const int cpc = forward_staged_cpc(g);
+  if (cpc) return launch_forward_staged(x, u, g, blk0, nblk, cpc, st);
   switch (g.T) {
     case 4: return launch_forward_t<4>(x, u, g, blk0, nblk, st);
     case 5: return launch_forward_t<5>(x, u, g, blk0, nblk, st);
@@ -301,6 +303,8 @@ int gemm_nc(int Cppad) {
 cudaError_t launch_position_gemm(const uint8_t* U, const uint8_t* V, float* M, const Geo& g,
                                  int nblk, int ldm, int n_valid, int passes, int sm_count,
                                  cudaStream_t st) {
+  if (gemm_resident_fits(g))
+    return launch_gemm_resident(U, V, M, g, nblk, ldm, n_valid, passes, sm_count, st);
   GemmParams P;
   P.U = U; P.V = V; P.M = M;
   P.n_pos = g.T * g.T;
@@ -339,6 +343,7 @@ static cudaError_t launch_inverse_t(const float* M, float* y, const Geo& g, int 
 
 cudaError_t launch_inverse(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
                            cudaStream_t st) {
+  return launch_inverse_vec(M, y, g, tile0, ntile, ldm, st);
   switch (g.T) {
     case 4: return launch_inverse_t<4>(M, y, g, tile0, ntile, ldm, st);
     case 5: return launch_inverse_t<5>(M, y, g, tile0, ntile, ldm, st);

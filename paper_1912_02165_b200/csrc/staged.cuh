@@ -17,5 +17,19 @@ cudaError_t launch_position_gemm(const uint8_t* U, const uint8_t* V, float* M, c
 cudaError_t launch_inverse(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
                            cudaStream_t st);
 int gemm_nc(int Cppad);
+// Shared-memory-staged forward transform (forward.cu); 0 = geometry too wide.
+int forward_staged_cpc(const Geo& g);
+cudaError_t launch_forward_staged(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc,
+                                  cudaStream_t st);
 
+}  // namespace wf
+
+namespace wf {
+// Position-major GEMM with the transformed kernels of one position resident
+// in shared memory (gemm_resident.cu); used whenever C'pad <= 128 and V_p fits.
+bool gemm_resident_fits(const Geo& g);
+cudaError_t launch_gemm_resident(const uint8_t* U, const uint8_t* V, float* M, const Geo& g, int nblk,
+                                 int ldm, int n_valid, int passes, int sm_count, cudaStream_t st);
+cudaError_t launch_inverse_vec(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
+                               cudaStream_t st);
 }  // namespace wf
