@@ -175,3 +175,38 @@ def max_rel_error(got, ref) -> float:
 
 def threads() -> int:
     return int(load().oracle_max_threads())
+
+
+def fft_conv_f64(x: np.ndarray, pack: np.ndarray, spec) -> np.ndarray:
+    """FP64 numpy restatement of the FFT-16 overlap-save convolution.
+
+    No reference implementation exists (FFT parity is
+    "unpinned" against the reference and anchored on the FP64 direct
+    oracle).  Follows the definition of SURVEY.md 8(b): 16x16 windows at
+    stride 14 (tile grid of reference tiling.py:66-75 with m = 14), rfft2,
+    per-bin real-expanded GEMM with ``pack`` (144, 2C, 2C'), irfft2, keep the
+    valid 14x14 block.  Used to check the pack expansion and tiling on CPU.
+    """
+    b, c, h, w = x.shape
+    k = spec.kernel
+    m = 17 - k
+    _, _, ho, wo = _out_dims(spec)
+    ty, tx = -(-ho // m), -(-wo // m)
+    hp, wp = (ty - 1) * m + 16, (tx - 1) * m + 16
+    xp = np.zeros((b, c, max(hp, spec.pad_lo + h), max(wp, spec.pad_lo + w)), np.float64)
+    xp[:, :, spec.pad_lo:spec.pad_lo + h, spec.pad_lo:spec.pad_lo + w] = x
+    wins = np.empty((b, ty, tx, c, 16, 16), np.float64)
+    for i in range(ty):
+        for j in range(tx):
+            wins[:, i, j] = xp[:, :, i * m:i * m + 16, j * m:j * m + 16]
+    spec_x = np.fft.rfft2(wins).reshape(b * ty * tx, c, 144)           # (tiles, C, 144)
+    cp = pack.shape[2] // 2
+    out = np.empty((b * ty * tx, cp, 144), np.complex128)
+    p64 = pack.astype(np.float64)
+    for p in range(144):
+        a = np.concatenate([spec_x[:, :, p].real, spec_x[:, :, p].imag], axis=1)   # (tiles, 2C)
+        r = a @ p64[p]                                                              # (tiles, 2C')
+        out[:, :, p] = r[:, :cp] + 1j * r[:, cp:]
+    blocks = np.fft.irfft2(out.reshape(b * ty * tx, cp, 16, 9), s=(16, 16))[:, :, :m, :m]
+    y = blocks.reshape(b, ty, tx, cp, m, m).transpose(0, 3, 1, 4, 2, 5).reshape(b, cp, ty * m, tx * m)
+    return y[:, :, :ho, :wo]

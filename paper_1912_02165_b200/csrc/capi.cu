@@ -55,8 +55,11 @@ static int make_geo(const wf_layer* L, int tile, int transform, Geo& g) {
     if (tile < 4 || tile > 8) return fail(WF_ERR_PARAM, "tile side must be in [4, 8], got %d", tile);
     if (L->kernel != 3)
       return fail(WF_ERR_UNSUPPORTED, "sm_100a Winograd kernels implement K=3 only (got K=%d)", L->kernel);
+  } else if (transform == WF_FFT16) {
+    if (tile != 16) return fail(WF_ERR_PARAM, "the FFT transform uses tile 16, got %d", tile);
+    if (L->kernel != 3) return fail(WF_ERR_UNSUPPORTED, "FFT-16 kernels implement K=3 only (got K=%d)", L->kernel);
   } else {
-    return fail(WF_ERR_UNSUPPORTED, "transform %d not implemented in this build", transform);
+    return fail(WF_ERR_PARAM, "unknown transform %d", transform);
   }
   g.B = L->batch; g.C = L->in_channels; g.Cp = L->out_channels;
   g.H = L->height; g.W = L->width; g.pad_lo = L->pad_lo;
@@ -68,8 +71,11 @@ static int make_geo(const wf_layer* L, int tile, int transform, Geo& g) {
   const long long nt = 1LL * g.B * g.tiles_y * g.tiles_x;
   if (nt > (1LL << 30)) return fail(WF_ERR_UNSUPPORTED, "layer too large (%lld tiles)", nt);
   g.n_tile = static_cast<int>(nt);
-  g.Cpad = round_up(g.C, 16);
-  g.Cppad = round_up(g.Cp, 16);
+  g.fft = transform == WF_FFT16 ? 1 : 0;
+  g.Cpad = round_up(g.fft ? 2 * g.C : g.C, 16);
+  g.Cppad = round_up(g.fft ? 2 * g.Cp : g.Cp, 16);
+  g.P = g.fft ? 16 * 9 : g.T * g.T;
+  g.Nout = g.fft ? 2 * g.Cp : g.Cp;
   g.n_blk = ceil_div(g.n_tile, kBlockTiles);
   return WF_OK;
 }
@@ -260,17 +266,31 @@ int wf_filter_transform(const float* w, float* pack, int c_in, int c_out, int ti
 }
 
 size_t wf_mma_pack_bytes(int tile, int c_in, int c_out, int transform) {
-  if (transform != WF_WINOGRAD || tile < 4 || tile > 8 || c_in < 1 || c_out < 1) return 0;
+  if (c_in < 1 || c_out < 1) return 0;
+  if (transform == WF_FFT16 && tile == 16)   // 144 bins, real-expanded (2C x 2C') complex GEMM
+    return static_cast<size_t>(144) * 2 * round_up(2 * c_out, 16) * round_up(2 * c_in, 16) * 2;
+  if (transform != WF_WINOGRAD || tile < 4 || tile > 8) return 0;
   return static_cast<size_t>(tile) * tile * 2 * round_up(c_out, 16) * round_up(c_in, 16) * 2;
 }
 
 int wf_mma_pack(const float* pack, void* mma_pack, int tile, int c_in, int c_out, int transform,
                 void* stream) {
   if (!pack || !mma_pack) return fail(WF_ERR_PARAM, "null pointer");
-  if (transform != WF_WINOGRAD) return fail(WF_ERR_UNSUPPORTED, "transform %d", transform);
-  if (tile < 4 || tile > 8) return fail(WF_ERR_PARAM, "tile side must be in [4, 8], got %d", tile);
   if (c_in < 1 || c_out < 1) return fail(WF_ERR_SHAPE, "channels must be >= 1");
-  const int P = tile * tile, Cpad = round_up(c_in, 16), Cppad = round_up(c_out, 16);
+  int P;
+  if (transform == WF_FFT16) {
+    // pack holds the real expansion (144, 2C, 2C') of the complex bins
+    if (tile != 16) return fail(WF_ERR_PARAM, "the FFT transform uses tile 16, got %d", tile);
+    P = 144;
+    c_in *= 2;
+    c_out *= 2;
+  } else if (transform == WF_WINOGRAD) {
+    if (tile < 4 || tile > 8) return fail(WF_ERR_PARAM, "tile side must be in [4, 8], got %d", tile);
+    P = tile * tile;
+  } else {
+    return fail(WF_ERR_PARAM, "unknown transform %d", transform);
+  }
+  const int Cpad = round_up(c_in, 16), Cppad = round_up(c_out, 16);
   const long long total = 1LL * P * Cppad * (Cpad / 2);
   mma_pack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       pack, static_cast<uint8_t*>(mma_pack), P, c_in, c_out, Cpad, Cppad);
@@ -281,9 +301,9 @@ int wf_mma_pack(const float* pack, void* mma_pack, int tile, int c_in, int c_out
 size_t wf_three_stage_scratch_bytes(const wf_layer* layer, int tile, int transform) {
   Geo g;
   if (make_geo(layer, tile, transform, g) != WF_OK) return 0;
-  const size_t P = static_cast<size_t>(g.T) * g.T;
+  const size_t P = static_cast<size_t>(g.P);
   const size_t u = P * g.n_blk * 2 * kBlockTiles * g.Cpad * 2;
-  const size_t m = P * g.Cp * static_cast<size_t>(g.n_blk) * kBlockTiles * 4;
+  const size_t m = P * g.Nout * static_cast<size_t>(g.n_blk) * kBlockTiles * 4;
   return u + m;
 }
 
@@ -298,7 +318,7 @@ int wf_conv_three_stage(const float* x, const void* mma_pack, float* y, void* sc
   const size_t need = wf_three_stage_scratch_bytes(layer, tile, transform);
   if (scratch_bytes < need) return fail(WF_ERR_SCRATCH, "scratch %zu < %zu bytes", scratch_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t P = static_cast<size_t>(g.T) * g.T;
+  const size_t P = static_cast<size_t>(g.P);
   uint8_t* U = static_cast<uint8_t*>(scratch);
   float* M = reinterpret_cast<float*>(U + P * g.n_blk * 2 * kBlockTiles * g.Cpad * 2);
   const int ldm = g.n_blk * kBlockTiles;

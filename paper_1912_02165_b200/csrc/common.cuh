@@ -20,8 +20,11 @@ struct Geo {
   int T, m;          // window side, output block side
   int Ho, Wo;        // output extents
   int tiles_y, tiles_x, n_tile;
-  int Cpad, Cppad;   // channels rounded up to the MMA K / N granularity (16)
+  int Cpad, Cppad;   // GEMM K / N (channels, x2 for FFT re|im) rounded up to 16
   int n_blk;         // ceil(n_tile / 128)
+  int P;             // transform positions: T*T (Winograd) or 16*9 bins (FFT-16)
+  int Nout;          // product rows per position: C' (Winograd) or 2C' (FFT re|im)
+  int fft;           // 1 for the FFT-16 overlap-save transform
 };
 
 // ------------------------------------------------------------------------

@@ -1,0 +1,250 @@
+// fft16.cu -- stage kernels of the FFT-16 overlap-save transformed
+// convolution (BASELINE config c4).  The reference has no FFT path
+// (SURVEY.md 8(a) "FFT variant": SPEC.md:17 puts it out of scope); this
+// follows the definition SURVEY.md 8(b) gives for the new framework:
+//
+//   * 16x16 input windows at stride 14 (the same OLA tile grid as
+//     Winograd with m = 14), zero outside the padded input;
+//   * rfft2 of each window: 16 x 9 = 144 Hermitian-half bins;
+//   * per bin a complex GEMM  M[t][c'] = sum_c X[t][c] * conj(W[c'][c]),
+//     run as a real GEMM with K = 2C ([Re | Im] of X) and N = 2C'
+//     ([Re | Im] of M) on the same tcgen05 position GEMM as Winograd;
+//   * irfft2 of each product window, keep the valid 14 x 14 block.
+//
+// Forward: one CTA = 16 tiles x 8 input channels, 16 half-warp groups.  A
+// group computes one (tile, channel) 2-D FFT at a time: thread r does the
+// real 16-point DFT of window row r, the row spectra go through a per-group
+// shared scratch, then threads v = 0..8 run the complex 16-point FFT down
+// column v.  The CTA's 144 x 16 x 8 spectrum is staged in shared memory and
+// written as bf16 hi/lo operand slabs (coalesced 128-byte core matrices).
+// Inverse mirrors it: load M for 16 tiles x 8 output channels, column
+// inverse FFTs, then each row thread runs the inverse real DFT and keeps 14
+// outputs.
+#include "common.cuh"
+#include "fft16.cuh"
+#include "sm100.cuh"
+#include "staged.cuh"
+
+namespace wf {
+namespace {
+
+constexpr int kFftTiles = 16;            // tiles per CTA
+constexpr int kFftCh = 8;                // channels per CTA
+constexpr int kBins = 144;               // 16 x 9
+constexpr int kBinPitch = 129;           // floats per bin in the staging arrays (odd: conflict-free columns)
+constexpr int kGroupScratch = 2 * 144;   // per-group row spectra (re, im), pitch 9 per row
+constexpr size_t kFftSmem = (2ull * kBins * kBinPitch + 16ull * kGroupScratch) * sizeof(float);
+
+__device__ __forceinline__ int stage_idx(int p, int c, int t) { return p * kBinPitch + c * kFftTiles + t; }
+
+__global__ void __launch_bounds__(256, 1) fft_forward_kernel(const float* __restrict__ x, uint8_t* __restrict__ u,
+                                                             Geo g, int tile0, int nblk_local) {
+  extern __shared__ float smem[];
+  float* sre = smem;
+  float* sim = smem + kBins * kBinPitch;
+  const int grp = threadIdx.x >> 4, r = threadIdx.x & 15;
+  float* gre = smem + 2 * kBins * kBinPitch + grp * kGroupScratch;
+  float* gim = gre + 144;
+  const unsigned gmask = 0xFFFFu << (threadIdx.x & 16);
+  const int local_limit = nblk_local * kBlockTiles;
+  const int tl0 = blockIdx.x * kFftTiles;   // first local tile of this CTA
+  const int cg0 = blockIdx.y * kFftCh;      // first input channel
+
+  // ---- 2-D FFTs: group grp owns tile grp, channels 0..7 in turn.
+  {
+    const int tl = tl0 + grp, tile = tile0 + tl;
+    const bool tvalid = tl < local_limit && tile < g.n_tile;
+    int b = 0, ty = 0, tx = 0;
+    if (tvalid) tile_coords(g, tile, b, ty, tx);
+    const int iy = ty * g.m - g.pad_lo + r, ox = tx * g.m - g.pad_lo;
+    const bool rvalid = tvalid && iy >= 0 && iy < g.H;
+    for (int c = 0; c < kFftCh; ++c) {
+      const int ch = cg0 + c;
+      float row[16];
+      if (rvalid && ch < g.C) {
+        const float* src = x + ((static_cast<size_t>(b) * g.C + ch) * g.H + iy) * g.W;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          const int ix = ox + s;
+          row[s] = (ix >= 0 && ix < g.W) ? __ldg(src + ix) : 0.0f;
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) row[s] = 0.0f;
+      }
+      float fr[9], fi[9];
+      fft::rfft16(row, fr, fi);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        gre[r * 9 + k] = fr[k];
+        gim[r * 9 + k] = fi[k];
+      }
+      __syncwarp(gmask);
+      if (r < 9) {
+        float cr[16], ci[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          cr[q] = gre[q * 9 + r];
+          ci[q] = gim[q * 9 + r];
+        }
+        fft::fft16<-1>(cr, ci);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          sre[stage_idx(q * 9 + r, c, grp)] = cr[q];
+          sim[stage_idx(q * 9 + r, c, grp)] = ci[q];
+        }
+      }
+      __syncwarp(gmask);
+    }
+  }
+  __syncthreads();
+
+  // ---- write the bf16 hi/lo slabs: K index c (Re) and C + c (Im).
+  const size_t slab = static_cast<size_t>(kBlockTiles) * g.Cpad * 2;
+  const int tid = threadIdx.x;
+  if ((g.C & 7) == 0) {
+    // Re and Im 8-channel groups are both aligned core-matrix columns.
+    const int q = tid & 3, t = (tid >> 2) & 15, part = (tid >> 6) & 1, pp = tid >> 7;
+    const int tl = tl0 + t;
+    if (tl < local_limit) {
+      const int blk = tl / kBlockTiles, row = tl % kBlockTiles;
+      const uint32_t off = slab_off(row, (part ? g.C : 0) + cg0 + 2 * q, kBlockTiles, g.Cpad);
+      const float* sa = part ? sim : sre;
+      for (int p = pp; p < kBins; p += 2) {
+        uint32_t hi, lo;
+        split_bf16x2(sa[stage_idx(p, 2 * q, t)], sa[stage_idx(p, 2 * q + 1, t)], hi, lo);
+        uint8_t* base = u + ((static_cast<size_t>(p) * nblk_local + blk) * 2) * slab + off;
+        *reinterpret_cast<uint32_t*>(base) = hi;
+        *reinterpret_cast<uint32_t*>(base + slab) = lo;
+      }
+    }
+  } else {
+    // General channel counts: element-wise 16-bit stores.
+    const int c = tid & 7, t = (tid >> 3) & 15, part = (tid >> 7) & 1;
+    const int tl = tl0 + t;
+    if (tl < local_limit && cg0 + c < g.C) {
+      const int blk = tl / kBlockTiles, row = tl % kBlockTiles;
+      const uint32_t off = slab_off(row, (part ? g.C : 0) + cg0 + c, kBlockTiles, g.Cpad);
+      const float* sa = part ? sim : sre;
+      for (int p = 0; p < kBins; ++p) {
+        const float v = sa[stage_idx(p, c, t)];
+        const uint32_t hv = pack_bf16x2(v, 0.0f);
+        const float vh = __uint_as_float(hv << 16);
+        const uint32_t lv = pack_bf16x2(v - vh, 0.0f);
+        uint8_t* base = u + ((static_cast<size_t>(p) * nblk_local + blk) * 2) * slab + off;
+        *reinterpret_cast<uint16_t*>(base) = static_cast<uint16_t>(hv & 0xFFFFu);
+        *reinterpret_cast<uint16_t*>(base + slab) = static_cast<uint16_t>(lv & 0xFFFFu);
+      }
+    }
+    // K padding [2C, Cpad) must hold zeros: channel-group 0 writes it.
+    const int npad = g.Cpad - 2 * g.C;
+    if (blockIdx.y == 0 && npad > 0) {
+      for (int i = tid; i < kBins * kFftTiles * npad; i += blockDim.x) {
+        const int k = 2 * g.C + i % npad;
+        const int t = (i / npad) % kFftTiles;
+        const int p = i / (npad * kFftTiles);
+        const int tl2 = tl0 + t;
+        if (tl2 >= local_limit) continue;
+        const int blk = tl2 / kBlockTiles, row = tl2 % kBlockTiles;
+        uint8_t* base = u + ((static_cast<size_t>(p) * nblk_local + blk) * 2) * slab +
+                        slab_off(row, k, kBlockTiles, g.Cpad);
+        *reinterpret_cast<uint16_t*>(base) = 0;
+        *reinterpret_cast<uint16_t*>(base + slab) = 0;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) fft_inverse_kernel(const float* __restrict__ M, float* __restrict__ y,
+                                                             Geo g, int tile0, int ntile, int ldm) {
+  extern __shared__ float smem[];
+  float* sre = smem;
+  float* sim = smem + kBins * kBinPitch;
+  const int grp = threadIdx.x >> 4, r = threadIdx.x & 15;
+  float* gre = smem + 2 * kBins * kBinPitch + grp * kGroupScratch;
+  float* gim = gre + 144;
+  const unsigned gmask = 0xFFFFu << (threadIdx.x & 16);
+  const int tl0 = blockIdx.x * kFftTiles;
+  const int cg0 = blockIdx.y * kFftCh;
+
+  // ---- load M[p][part*C' + c'][tile] for 16 tiles x 8 channels x 144 bins.
+  for (int i = threadIdx.x; i < kBins * 2 * kFftCh * kFftTiles; i += blockDim.x) {
+    const int t = i & 15, c = (i >> 4) & 7, part = (i >> 7) & 1, p = i >> 8;
+    const int tl = tl0 + t, cp = cg0 + c;
+    float v = 0.0f;
+    if (tl < ntile && cp < g.Cp) v = __ldcg(M + (static_cast<size_t>(p) * g.Nout + part * g.Cp + cp) * ldm + tl);
+    (part ? sim : sre)[stage_idx(p, c, t)] = v;
+  }
+  __syncthreads();
+
+  const int tl = tl0 + grp, tile = tile0 + tl;
+  if (tl >= ntile) return;
+  int b = 0, ty = 0, tx = 0;
+  tile_coords(g, tile, b, ty, tx);
+  const int oy = ty * g.m + r, ox = tx * g.m;
+  for (int c = 0; c < kFftCh; ++c) {
+    const int cp = cg0 + c;
+    if (cp >= g.Cp) break;
+    if (r < 9) {
+      float cr[16], ci[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        cr[q] = sre[stage_idx(q * 9 + r, c, grp)];
+        ci[q] = sim[stage_idx(q * 9 + r, c, grp)];
+      }
+      fft::fft16<1>(cr, ci);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        gre[q * 9 + r] = cr[q];
+        gim[q * 9 + r] = ci[q];
+      }
+    }
+    __syncwarp(gmask);
+    if (r < 14 && oy < g.Ho) {
+      float zr[9], zi[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        zr[k] = gre[r * 9 + k];
+        zi[k] = gim[r * 9 + k];
+      }
+      float out[14];
+      fft::irfft16<14>(zr, zi, out);
+      float* dst = y + ((static_cast<size_t>(b) * g.Cp + cp) * g.Ho + oy) * g.Wo + ox;
+#pragma unroll
+      for (int s = 0; s < 14; ++s)
+        if (ox + s < g.Wo) dst[s] = out[s] * (1.0f / 256.0f);
+    }
+    __syncwarp(gmask);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_fft_forward(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fft_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kFftSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(ceil_div(nblk * kBlockTiles, kFftTiles), ceil_div(g.C, kFftCh));
+  fft_forward_kernel<<<grid, 256, kFftSmem, st>>>(x, u, g, blk0 * kBlockTiles, nblk);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fft_inverse(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
+                               cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fft_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kFftSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(ceil_div(ntile, kFftTiles), ceil_div(g.Cp, kFftCh));
+  fft_inverse_kernel<<<grid, 256, kFftSmem, st>>>(M, y, g, tile0, ntile, ldm);
+  return cudaGetLastError();
+}
+
+}  // namespace wf

@@ -25,8 +25,8 @@ static constexpr size_t kL2Budget = 56ull << 20;    // U + M of all in-flight wa
 
 // Bytes of U + M for one 128-tile block.
 static size_t block_bytes(const Geo& g) {
-  const size_t P = static_cast<size_t>(g.T) * g.T;
-  return P * 2 * kBlockTiles * g.Cpad * 2 + P * g.Cp * kBlockTiles * 4;
+  const size_t P = static_cast<size_t>(g.P);
+  return P * 2 * kBlockTiles * g.Cpad * 2 + P * g.Nout * kBlockTiles * 4;
 }
 
 static int wave_blocks(const Geo& g) {
@@ -65,7 +65,7 @@ cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* s
                       int passes, int /*r*/, int sm_count, cudaStream_t st) {
   if (persistent_fits(g)) return run_fused_persistent(x, vpack, y, scratch, g, passes, sm_count, st);
   const int wb = wave_blocks(g);
-  const size_t P = static_cast<size_t>(g.T) * g.T;
+  const size_t P = static_cast<size_t>(g.P);
   const size_t lane_bytes = static_cast<size_t>(wb) * block_bytes(g);
   const int n_waves = ceil_div(g.n_blk, wb);
   const int lanes = n_waves > 1 ? kLanes : 1;

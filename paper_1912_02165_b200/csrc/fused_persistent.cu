@@ -544,6 +544,7 @@ struct PersistPlan {
 
 static PersistPlan persist_plan(const Geo& g) {
   PersistPlan pl = {};
+  if (g.fft) return pl;                    // FFT-16 runs the staged L2 waves
   pl.nt = 256;
   pl.cps = g.T <= 6 ? 2 : 1;              // CTAs per SM (two overlap each other's latency)
   pl.stages = pl.cps == 2 ? 2 : 3;

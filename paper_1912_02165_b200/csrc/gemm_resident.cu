@@ -189,8 +189,8 @@ cudaError_t launch_gemm_resident(const uint8_t* U, const uint8_t* V, float* M, c
                                  int ldm, int n_valid, int passes, int sm_count, cudaStream_t st) {
   ResParams P;
   P.U = U; P.V = V; P.M = M;
-  P.n_pos = g.T * g.T; P.n_blk = nblk;
-  P.Cpad = g.Cpad; P.Cppad = g.Cppad; P.Cp = g.Cp;
+  P.n_pos = g.P; P.n_blk = nblk;
+  P.Cpad = g.Cpad; P.Cppad = g.Cppad; P.Cp = g.Nout;
   P.ldm = ldm; P.n_valid = n_valid; P.passes = passes;
   static bool attr = false;
   if (!attr) {

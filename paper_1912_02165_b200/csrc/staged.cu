@@ -281,6 +281,7 @@ static cudaError_t launch_forward_t(const float* x, uint8_t* u, const Geo& g, in
 
 cudaError_t launch_forward_slab(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk,
                                 cudaStream_t st) {
+  if (g.fft) return launch_fft_forward(x, u, g, blk0, nblk, st);
   const int cpc = forward_staged_cpc(g);
   if (cpc) return launch_forward_staged(x, u, g, blk0, nblk, cpc, st);
   switch (g.T) {
@@ -307,9 +308,9 @@ cudaError_t launch_position_gemm(const uint8_t* U, const uint8_t* V, float* M, c
     return launch_gemm_resident(U, V, M, g, nblk, ldm, n_valid, passes, sm_count, st);
   GemmParams P;
   P.U = U; P.V = V; P.M = M;
-  P.n_pos = g.T * g.T;
+  P.n_pos = g.P;
   P.n_blk = nblk;
-  P.Cpad = g.Cpad; P.Cppad = g.Cppad; P.Cp = g.Cp;
+  P.Cpad = g.Cpad; P.Cppad = g.Cppad; P.Cp = g.Nout;
   P.NC = gemm_nc(g.Cppad);
   P.n_nc = ceil_div(g.Cppad, P.NC);
   P.ldm = ldm;
@@ -343,6 +344,7 @@ static cudaError_t launch_inverse_t(const float* M, float* y, const Geo& g, int 
 
 cudaError_t launch_inverse(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
                            cudaStream_t st) {
+  if (g.fft) return launch_fft_inverse(M, y, g, tile0, ntile, ldm, st);
   return launch_inverse_vec(M, y, g, tile0, ntile, ldm, st);
   switch (g.T) {
     case 4: return launch_inverse_t<4>(M, y, g, tile0, ntile, ldm, st);

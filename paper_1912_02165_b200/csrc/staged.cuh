@@ -32,4 +32,8 @@ cudaError_t launch_gemm_resident(const uint8_t* U, const uint8_t* V, float* M, c
                                  int ldm, int n_valid, int passes, int sm_count, cudaStream_t st);
 cudaError_t launch_inverse_vec(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
                                cudaStream_t st);
+// FFT-16 overlap-save stage kernels (fft16.cu)
+cudaError_t launch_fft_forward(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, cudaStream_t st);
+cudaError_t launch_fft_inverse(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
+                               cudaStream_t st);
 }  // namespace wf

@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _lib
 from . import device as _dev
-from .basis import make_basis
+from .basis import FftBasis, make_basis, make_fft_basis
 from .errors import (IntermediateAllocationError, InvalidParameterError, ShapeMismatchError,
                      WinofuseError)
 from .tensor import LayerSpec, Tensor4D, aligned_empty
@@ -188,8 +188,9 @@ def _check_input(inp, spec: LayerSpec) -> None:
 
 def _resolve_pack(kers, spec: LayerSpec, basis) -> KernelPack:
     if isinstance(kers, KernelPack):
+        want = "fft" if isinstance(basis, FftBasis) else "winograd"
         if (kers.tile != basis.tile or kers.kernel_side != spec.kernel or kers.c_in != spec.in_channels
-                or kers.c_out != spec.out_channels):
+                or kers.c_out != spec.out_channels or kers.transform != want):
             raise ShapeMismatchError(
                 f"kernel pack (T={kers.tile}, K={kers.kernel_side}, C={kers.c_in}, C'={kers.c_out}) "
                 f"does not match layer/config")
@@ -202,14 +203,24 @@ def _resolve_pack(kers, spec: LayerSpec, basis) -> KernelPack:
 
 
 def _basis_for(cfg: EngineConfig, spec: LayerSpec):
-    if cfg.transform != "winograd":
-        from .errors import UnsupportedConfigError
-        raise UnsupportedConfigError("FFT-16 engine is not available in this build")
+    if cfg.transform == "fft":
+        return make_fft_basis(spec.kernel)
     if cfg.points is not None and tuple(str(p) for p in cfg.points) != \
             tuple(str(p) for p in make_basis(cfg.tile, spec.kernel).points):
         from .errors import UnsupportedConfigError
         raise UnsupportedConfigError("the sm_100a kernels bake in the default interpolation nodes")
     return make_basis(cfg.tile, spec.kernel, cfg.points)
+
+
+def _intermediate_bytes(n_tile: int, spec: LayerSpec, cfg: EngineConfig) -> int:
+    """Full-size transformed intermediates of the three-stage engine.
+
+    Winograd: 4 * T^2 * n_tile * (C + C'); FFT-16: complex64 bins,
+    8 * 144 * n_tile * (C + C') (SURVEY.md 8(d) Q_3stage).
+    """
+    if cfg.transform == "fft":
+        return 8 * 144 * n_tile * (spec.in_channels + spec.out_channels)
+    return _FP32 * cfg.tile * cfg.tile * n_tile * (spec.in_channels + spec.out_channels)
 
 
 def _finish(y, host_result: bool):
@@ -277,13 +288,12 @@ def conv_three_stage(inp, kers, spec: LayerSpec, config: EngineConfig | None = N
     basis = _basis_for(cfg, spec)
     _check_input(inp, spec)
     pack = _resolve_pack(kers, spec, basis)
-    pl = tile_plan(spec, cfg.tile)
-    t2 = cfg.tile * cfg.tile
+    pl = tile_plan(spec, cfg.tile, out=basis.out)
     dev = _dev.require_cuda(cfg.device if not _dev.is_torch(inp) else inp.device)
     lib = _lib.load()
     layer = _lib.layer_struct(spec)
     tf = _lib.TRANSFORMS[cfg.transform]
-    inter_bytes = _FP32 * t2 * pl.n_tile * (spec.in_channels + spec.out_channels)
+    inter_bytes = _intermediate_bytes(pl.n_tile, spec, cfg)
     need = lib.wf_three_stage_scratch_bytes(layer, cfg.tile, tf)
     if need == 0:
         _lib.check(lib.wf_conv_three_stage(None, None, None, None, 0, layer, cfg.tile, tf, 0, None),
@@ -301,7 +311,8 @@ def conv_three_stage(inp, kers, spec: LayerSpec, config: EngineConfig | None = N
                                            _dev.stream_ptr(dev)), "wf_conv_three_stage")
     wall = tm.seconds()
     stats = ConvStats(engine="three_stage", wall_s=wall,
-                      flops=multiply_flops(pl.n_tile, spec.in_channels, spec.out_channels, cfg.tile),
+                      flops=multiply_flops(pl.n_tile, spec.in_channels, spec.out_channels, cfg.tile,
+                                           cfg.transform),
                       n_tile=pl.n_tile, workers=cfg.resolved_workers(), intermediate_bytes=inter_bytes,
                       scratch_bytes=int(need), phase_s={"total": wall}, device=str(dev),
                       precision=cfg.precision, transform=cfg.transform)
@@ -323,7 +334,7 @@ def conv_fused(inp, pack: KernelPack, spec: LayerSpec, config: EngineConfig | No
     basis = _basis_for(cfg, spec)
     _check_input(inp, spec)
     pack = _resolve_pack(pack, spec, basis)
-    pl = tile_plan(spec, cfg.tile)
+    pl = tile_plan(spec, cfg.tile, out=basis.out)
     n_task = -(-pl.n_tile // cfg.r)
     if task_order is None:
         order = list(range(n_task))
@@ -351,12 +362,12 @@ def conv_fused(inp, pack: KernelPack, spec: LayerSpec, config: EngineConfig | No
                                      _dev.stream_ptr(dev)), "wf_conv_fused")
     wall = tm.seconds()
     workers = cfg.resolved_workers(n_task)
-    flops = multiply_flops(pl.n_tile, spec.in_channels, spec.out_channels, cfg.tile)
+    flops = multiply_flops(pl.n_tile, spec.in_channels, spec.out_channels, cfg.tile, cfg.transform)
     task_flops = trace = None
     violations = None
     if cfg.instrumented:
         task_flops = [multiply_flops(min(cfg.r, pl.n_tile - i * cfg.r), spec.in_channels, spec.out_channels,
-                                     cfg.tile) for i in range(n_task)]
+                                     cfg.tile, cfg.transform) for i in range(n_task)]
         trace = [(order[pos], pos % workers) for pos in range(n_task)]
         violations = 0
     stats = ConvStats(engine="fused", wall_s=wall, flops=flops, n_tile=pl.n_tile, n_task=n_task, r=cfg.r,

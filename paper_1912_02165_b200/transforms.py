@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from . import device as _dev
-from .basis import WinogradBasis
+from .basis import FftBasis, WinogradBasis
 from .errors import ShapeMismatchError
 from .tensor import LayerSpec, Tensor4D, aligned_empty
 from .tiling import TilePlan
@@ -86,11 +86,35 @@ class LeftHandBlock:
         return cls(data=aligned_empty((tile * tile, rows, c_in)), r_eff=rows)
 
 
-def transform_kernels(kers, basis: WinogradBasis) -> KernelPack:
+def fft_pack_host(w64: np.ndarray) -> np.ndarray:
+    """Real expansion of the conjugate kernel spectra, (144, 2C, 2C') float32.
+
+    V[p][c][c'] = conj(rfft2(w[c'][c] zero-padded to 16x16))[p] (cross-
+    correlation), computed in float64.  The complex product M = X V over c is
+    a real GEMM [Re X | Im X] @ [[Re V, Im V], [-Im V, Re V]]: rows 0..C-1 of
+    the pack multiply Re X, rows C..2C-1 Im X; columns 0..C'-1 give Re M,
+    C'..2C'-1 Im M.
+    """
+    c_out, c_in = w64.shape[:2]
+    padded = np.zeros((c_out, c_in, 16, 16), np.float64)
+    padded[:, :, :w64.shape[2], :w64.shape[3]] = w64
+    spec = np.conj(np.fft.rfft2(padded))                       # (C', C, 16, 9)
+    v = spec.reshape(c_out, c_in, 144).transpose(2, 1, 0)      # (144, C, C')
+    host = aligned_empty((144, 2 * c_in, 2 * c_out))
+    host[:, :c_in, :c_out] = v.real
+    host[:, :c_in, c_out:] = v.imag
+    host[:, c_in:, :c_out] = -v.imag
+    host[:, c_in:, c_out:] = v.real
+    return host
+
+
+def transform_kernels(kers, basis) -> KernelPack:
     """G w G^T for every (c', c), packed position-major (T*T, C, C').
 
     Host weights: float64 numpy, one f32 rounding (reference
     transforms.py:73-77).  CUDA weights: the same arithmetic on the device.
+    With an :class:`FftBasis` the pack is the real-expanded conjugate kernel
+    spectrum (144, 2C, 2C') of :func:`fft_pack_host` (one-time, host f64).
     """
     dims = _dev.dims_of(kers)
     if len(dims) != 4:
@@ -98,6 +122,15 @@ def transform_kernels(kers, basis: WinogradBasis) -> KernelPack:
     c_out, c_in, kh, kw = dims
     if kh != basis.kernel or kw != basis.kernel:
         raise ShapeMismatchError(f"kernel dims {dims} do not match basis K={basis.kernel}")
+    if isinstance(basis, FftBasis):
+        if _dev.is_torch(kers):
+            w64 = kers.detach().cpu().double().numpy()
+        else:
+            w64 = (kers.data if isinstance(kers, Tensor4D) else np.asarray(kers)).astype(np.float64)
+        host = fft_pack_host(w64)
+        host.setflags(write=False)
+        return KernelPack(data=host, tile=basis.tile, kernel_side=basis.kernel, c_in=c_in, c_out=c_out,
+                          transform="fft")
     t = basis.tile
     if _dev.is_torch(kers) and kers.is_cuda:
         dev = kers.device
@@ -121,8 +154,14 @@ def transform_kernels(kers, basis: WinogradBasis) -> KernelPack:
     return KernelPack(data=host, tile=t, kernel_side=basis.kernel, c_in=c_in, c_out=c_out)
 
 
-def multiply_flops(rows: int, c_in: int, c_out: int, tile: int) -> int:
-    """Useful multiply-stage flops for ``rows`` tiles (2 * rows * C * C' * T^2)."""
+def multiply_flops(rows: int, c_in: int, c_out: int, tile: int, transform: str = "winograd") -> int:
+    """Useful multiply-stage flops for ``rows`` tiles.
+
+    Winograd: 2 * rows * C * C' * T^2.  FFT-16: 8 * rows * C * C' * 144
+    (a complex multiply-add is 8 real flops).
+    """
+    if transform == "fft":
+        return 8 * rows * c_in * c_out * 144
     return 2 * rows * c_in * c_out * tile * tile
 
 
