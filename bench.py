@@ -44,7 +44,7 @@ CONFIGS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
@@ -87,29 +87,61 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / clock-event (throttle) reasons sampled during the timed region.
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    Uses NVML directly (the same counters nvidia-smi reads) so that a timed
+    region of a few milliseconds still gets many samples; falls back to one
+    nvidia-smi query per sample when NVML is unavailable.
+    """
 
-    def __init__(self, index):
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index, period_s=0.0005):
         self.index = index
-        self.samples = []
+        self.period = period_s
+        self.samples = []            # (wall time, sm_mhz, reasons bitmask)
+        self.window = None           # (t0, t1) of the timed region
+        self.max_mhz = None
+        self.source = "nvml"
         self._stop = threading.Event()
         self._thread = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+            self.source = "nvidia-smi"
+
+    def _sample(self):
+        if self._nvml is not None:
+            n = self._nvml
+            sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+            try:
+                mask = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except AttributeError:
+                mask = n.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            return time.perf_counter(), float(sm), int(mask)
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                              "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        self.max_mhz = float(out[1])
+        return time.perf_counter(), float(out[0]), int(out[2].strip(), 16)
 
     def _run(self):
-        while not self._stop.is_set():
+        while True:
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            if self._stop.is_set():
+                break
+            time.sleep(self.period)
 
     def __enter__(self):
         self._thread = threading.Thread(target=self._run, daemon=True)
@@ -120,16 +152,27 @@ class ClockSampler:
         self._stop.set()
         self._thread.join(timeout=10)
 
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 5 + i and s[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        """Samples taken inside the timed region (wall-clock window from the
+        first launch to the final synchronize); if the region was shorter
+        than one sample period, the samples adjacent to it."""
+        samples = self.samples
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [s for s in samples if t0 <= s[0] <= t1]
+            if not inside and samples:
+                inside = sorted(samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:2]
+            samples = inside
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["clock query unavailable"],
+                    "samples": 0, "source": self.source}
+        sm = [s[1] for s in samples]
+        reasons = sorted({name for _, _, m in samples for bit, name in self.REASONS.items() if m & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(samples), "source": self.source}
 
 
 def cpu_baseline(cfg_name, t, spec_full, threads=None):
@@ -239,13 +282,18 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    launches0 = _lib.load().wf_kernel_launches()
     with ClockSampler(local) as clocks:
+        time.sleep(0.05)                                            # sampler running before the region
+        w0 = time.perf_counter()
         for i in range(args.steps):
             flush.zero_()                                           # evict input/output from L2
             starts[i].record(stream)
             plan(x_dev)
             ends[i].record(stream)
         torch.cuda.synchronize(dev)
+        clocks.mark(w0, time.perf_counter())
+    launches = _lib.load().wf_kernel_launches() - launches0
     if world > 1:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -280,16 +328,7 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
 
-    lib = _lib.load()
-    launches_per_step = 0
     n_tile, q_fused, q_three, f_gemm = roofline_terms(spec, t, args.precision)
-    if args.engine == "fused":
-        nbytes = lib.wf_fused_scratch_bytes(_lib.layer_struct(spec), t, 0, 0)
-        per_block = (t * t * 2 * 128 * (-(-spec.in_channels // 16) * 16) * 2 + t * t * spec.out_channels * 128 * 4)
-        waves = -(-(-(-n_tile // 128)) // max(1, nbytes // per_block))
-        launches_per_step = 3 * waves
-    else:
-        launches_per_step = 3
 
     if rank == 0:
         hbm_peak, bf16_peak, peak_kind = measured_peaks()
@@ -325,7 +364,7 @@ def run_ours(args):
                          "unit_of_launch": "one fused layer call (all its kernels)"},
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": int(x_np.nbytes),
                     "d2h_bytes_per_step": int(np.prod(spec.output_dims()) * 4), "ms_per_step": e2e_ms},
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }

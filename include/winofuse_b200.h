@@ -55,6 +55,9 @@ typedef struct wf_layer {
 int wf_version(void);
 const char* wf_last_error(void);
 int wf_device_sm_count(void);
+/* Number of kernels this library has launched in the process so far
+ * (diagnostic; benchmarks difference it around a timed region). */
+unsigned long long wf_kernel_launches(void);
 
 /* ---------------------------------------------------------------- packs --
  * Replaces transforms.transform_kernels (winofuse/transforms.py:63-80):

@@ -42,6 +42,7 @@ SIGNATURES = {
     "wf_version": (_i, []),
     "wf_last_error": (ctypes.c_char_p, []),
     "wf_device_sm_count": (_i, []),
+    "wf_kernel_launches": (ctypes.c_ulonglong, []),
     "wf_filter_transform": (_i, [_fp, _fp, _i, _i, _i, _vp]),
     "wf_mma_pack_bytes": (_sz, [_i, _i, _i, _i]),
     "wf_mma_pack": (_i, [_fp, _vp, _i, _i, _i, _i, _vp]),

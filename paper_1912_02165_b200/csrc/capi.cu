@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/winofuse_b200.h) plus the small
 // utility kernels: device filter transform, MMA pack, FP64 direct
 // convolution and the reference-layout stage kernels.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -15,6 +16,9 @@
 namespace wf {
 
 static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -254,12 +258,15 @@ const char* wf_last_error(void) { return g_last_error.c_str(); }
 
 int wf_device_sm_count(void) { return sm_count(); }
 
+unsigned long long wf_kernel_launches(void) { return wf::g_launches.load(); }
+
 int wf_filter_transform(const float* w, float* pack, int c_in, int c_out, int tile, void* stream) {
   if (!w || !pack) return fail(WF_ERR_PARAM, "null pointer");
   if (c_in < 1 || c_out < 1) return fail(WF_ERR_SHAPE, "channels must be >= 1");
   if (tile < 4 || tile > 8) return fail(WF_ERR_PARAM, "tile side must be in [4, 8], got %d", tile);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int n = c_in * c_out;
+  note_launch();
   WF_TDISPATCH(tile, (filter_transform_kernel<TT><<<ceil_div(n, 128), 128, 0, st>>>(w, pack, c_in, c_out)));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? WF_OK : cuda_fail(e, "filter_transform");
@@ -292,6 +299,7 @@ int wf_mma_pack(const float* pack, void* mma_pack, int tile, int c_in, int c_out
   }
   const int Cpad = round_up(c_in, 16), Cppad = round_up(c_out, 16);
   const long long total = 1LL * P * Cppad * (Cpad / 2);
+  note_launch();
   mma_pack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       pack, static_cast<uint8_t*>(mma_pack), P, c_in, c_out, Cpad, Cppad);
   cudaError_t e = cudaGetLastError();
@@ -364,6 +372,7 @@ int wf_conv_direct(const float* x, const float* w, float* y, const wf_layer* lay
   const int Wo = L.width + L.pad_lo + L.pad_hi - L.kernel + 1;
   if (Ho < 1 || Wo < 1) return fail(WF_ERR_SHAPE, "padded input smaller than kernel");
   const long long total = 1LL * L.batch * L.out_channels * Ho * Wo;
+  note_launch();
   direct_conv_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       x, w, y, L, Ho, Wo);
   cudaError_t e = cudaGetLastError();
@@ -380,6 +389,7 @@ int wf_forward_tiles(const float* x, float* dst, const wf_layer* layer, int tile
   if (row0 < 0 || row0 + (t1 - t0) > dst_rows) return fail(WF_ERR_SHAPE, "destination rows too small");
   dim3 blk(32, 4), grid(ceil_div(t1 - t0, 4), ceil_div(g.C, 32));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  note_launch();
   WF_TDISPATCH(tile, (forward_tiles_kernel<TT><<<grid, blk, 0, st>>>(x, dst, g, t0, t1, row0, dst_rows)));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? WF_OK : cuda_fail(e, "forward_tiles");
@@ -392,6 +402,7 @@ int wf_multiply_positions(const float* left, const float* pack, float* res, int 
     return fail(WF_ERR_SHAPE, "bad multiply shape");
   if (r_eff == 0) return WF_OK;
   dim3 grid(ceil_div(c_out, 128), r_eff, positions);
+  note_launch();
   multiply_positions_kernel<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(left, pack, res, rows, r_eff,
                                                                                  c_in, c_out);
   cudaError_t e = cudaGetLastError();
@@ -408,6 +419,7 @@ int wf_inverse_tiles(const float* res, float* y, const wf_layer* layer, int tile
   if (row0 < 0 || row0 + (t1 - t0) > res_rows) return fail(WF_ERR_SHAPE, "result rows too small");
   dim3 blk(32, 4), grid(ceil_div(t1 - t0, 4), ceil_div(g.Cp, 32));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  note_launch();
   WF_TDISPATCH(tile, (inverse_tiles_kernel<TT><<<grid, blk, 0, st>>>(res, y, g, t0, t1, row0, res_rows)));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? WF_OK : cuda_fail(e, "inverse_tiles");

@@ -13,6 +13,10 @@ constexpr int kKBlock = 64;       // channels per K block of an operand slab
 __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
 __host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
+// Host-side count of kernel launches issued by the library (capi.cu);
+// exported as wf_kernel_launches() so benchmarks can report their launches.
+void note_launch();
+
 // Layer geometry for one (layer, tile) pair; tile order is batch-major, then
 // tile row, then tile column (reference tiling.py:8-11, 66-75).
 struct Geo {

@@ -229,6 +229,7 @@ cudaError_t launch_fft_forward(const float* x, uint8_t* u, const Geo& g, int blk
     attr = true;
   }
   dim3 grid(ceil_div(nblk * kBlockTiles, kFftTiles), ceil_div(g.C, kFftCh));
+  note_launch();
   fft_forward_kernel<<<grid, 256, kFftSmem, st>>>(x, u, g, blk0 * kBlockTiles, nblk);
   return cudaGetLastError();
 }
@@ -243,6 +244,7 @@ cudaError_t launch_fft_inverse(const float* M, float* y, const Geo& g, int tile0
     attr = true;
   }
   dim3 grid(ceil_div(ntile, kFftTiles), ceil_div(g.Cp, kFftCh));
+  note_launch();
   fft_inverse_kernel<<<grid, 256, kFftSmem, st>>>(M, y, g, tile0, ntile, ldm);
   return cudaGetLastError();
 }

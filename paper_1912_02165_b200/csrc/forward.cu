@@ -159,6 +159,7 @@ static cudaError_t launch_staged(const float* x, uint8_t* u, const Geo& g, int b
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  note_launch();
   return cudaLaunchKernelEx(&cfg, kern, x, u, g, blk0, nblk, S);
 }
 

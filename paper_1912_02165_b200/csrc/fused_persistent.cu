@@ -630,6 +630,7 @@ static cudaError_t launch_persist_t(const PersistParams& P, size_t smem, int gri
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  note_launch();
   kern<<<grid, NT, smem, st>>>(P);
   return cudaGetLastError();
 }

@@ -210,6 +210,7 @@ cudaError_t launch_gemm_resident(const uint8_t* U, const uint8_t* V, float* M, c
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  note_launch();
   return cudaLaunchKernelEx(&cfg, gemm_resident_kernel, P);
 }
 
@@ -274,6 +275,7 @@ static cudaError_t launch_inv_vec_t(const float* M, float* y, const Geo& g, int 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  note_launch();
   return cudaLaunchKernelEx(&cfg, inverse_vec_kernel<T, TPT>, M, y, g, tile0, ntile, ldm);
 }
 

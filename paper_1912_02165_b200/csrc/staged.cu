@@ -275,6 +275,7 @@ template <int T>
 static cudaError_t launch_forward_t(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk,
                                     cudaStream_t st) {
   dim3 grid(ceil_div(nblk * kBlockTiles, 32), g.Cpad / 16);
+  note_launch();
   forward_slab_kernel<T><<<grid, 256, 0, st>>>(x, u, g, blk0 * kBlockTiles, nblk);
   return cudaGetLastError();
 }
@@ -330,6 +331,7 @@ cudaError_t launch_position_gemm(const uint8_t* U, const uint8_t* V, float* M, c
   }
   const int n_items = P.n_pos * P.n_blk * P.n_nc;
   const int grid = n_items < sm_count ? n_items : sm_count;
+  note_launch();
   position_gemm_kernel<<<grid, kGemmThreads, smem, st>>>(P);
   return cudaGetLastError();
 }
@@ -338,6 +340,7 @@ template <int T>
 static cudaError_t launch_inverse_t(const float* M, float* y, const Geo& g, int tile0, int ntile,
                                     int ldm, cudaStream_t st) {
   dim3 grid(ceil_div(ntile, 128), g.Cp);
+  note_launch();
   inverse_kernel<T><<<grid, 128, 0, st>>>(M, y, g, tile0, ntile, ldm);
   return cudaGetLastError();
 }
