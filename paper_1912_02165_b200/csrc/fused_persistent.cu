@@ -41,7 +41,6 @@ struct PersistParams {
   int passes;
   int n_steps, n_items;
   int wreg, trows, plane; // F staging geometry
-  int wo_pad;             // I staging row pitch (floats)
   int f_desc_off, f_max_rows;  // F row-descriptor table (bytes into smem, capacity)
   int stages;                  // G smem pipeline depth
   int f_bulk, f_shift;         // F staging by bulk copies; staged column of x = 0
@@ -90,7 +89,7 @@ struct GemmSync {
 };
 
 // ------------------------------------------------------------------ F item
-template <int T, int NT>
+template <int T, int NT, int KC>
 __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t* smem, GemmSync& sy,
                                  int fparity) {
   const Geo& g = P.g;
@@ -226,9 +225,10 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
       for (int s = 0; s < T; ++s) ua[r][s] = ub[r][s] = 0.0f;
   }
   if (warp < 4 * pairs) {
-    const size_t slab = static_cast<size_t>(kBlockTiles) * g.Cpad * 2;
+    const int cpad = KC ? KC : g.Cpad;
+    const size_t slab = static_cast<size_t>(kBlockTiles) * cpad * 2;
     uint8_t* slot = P.uring + static_cast<size_t>(b % P.NU) * T * T * 2 * slab;
-    uint8_t* dst = slot + slab_off(tl, c0, kBlockTiles, g.Cpad);
+    uint8_t* dst = slot + slab_off(tl, c0, kBlockTiles, cpad);
 #pragma unroll
     for (int r = 0; r < T; ++r)
 #pragma unroll
@@ -253,7 +253,7 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
 // identical copies): pipeline step K (over all G items of this CTA) uses
 // stage K % 3 with parity (K / 3) & 1; accumulator pl has been completed
 // tuse[pl] times before this item.
-template <int NT>
+template <int NT, int KC>
 __device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* smem, GemmSync& sy,
                               uint32_t tmem, int gbase, const int (&tuse)[8]) {
   const Geo& g = P.g;
@@ -326,20 +326,35 @@ __device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* sm
     const int qd = warp & 3;
     const int row = qd * 32 + lane_id();
     const int tile = b * kBlockTiles + row;
-    float* mslot = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * g.Cp * kBlockTiles;
+    const int cpo = KC ? KC : g.Cp;
+    float* mslot = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * cpo * kBlockTiles;
+    const bool live = tile < g.n_tile;
     for (int pl = 0; pl < np; ++pl) {
       mbar_wait(&sy.tfull[pl], tuse[pl] & 1);
       tc_fence_after();
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) + pl * g.Cppad;
-      float* mrow = mslot + static_cast<size_t>(p0 + pl) * g.Cp * kBlockTiles + row;
-      for (int c = 0; c < g.Cppad; c += 16) {
-        float v[16];
-        tmem_ld16(taddr + c, v);
-        tmem_ld_wait();
-        if (tile < g.n_tile) {
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) + pl * (KC ? KC : g.Cppad);
+      float* mrow = mslot + static_cast<size_t>(p0 + pl) * cpo * kBlockTiles + row;
+      if constexpr (KC != 0) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c + i < g.Cp) __stcg(mrow + static_cast<size_t>(c + i) * kBlockTiles, v[i]);
+        for (int c = 0; c < KC; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + c, v);
+          tmem_ld_wait();
+          if (live) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) __stcg(mrow + (c + i) * kBlockTiles, v[i]);
+          }
+        }
+      } else {
+        for (int c = 0; c < g.Cppad; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + c, v);
+          tmem_ld_wait();
+          if (live) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c + i < g.Cp) __stcg(mrow + static_cast<size_t>(c + i) * kBlockTiles, v[i]);
+          }
         }
       }
     }
@@ -348,96 +363,68 @@ __device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* sm
 }
 
 // ------------------------------------------------------------------ I item
-// Thread = (TPT consecutive tiles, c'): vector loads of the products, inverse
-// transform, then the m x m blocks are staged in shared memory in output-row
-// order and written back by whole warps along output rows (coalesced), only
-// for the columns this block's tiles own in each tile row.
-template <int T, int NT>
-__device__ void run_inverse_item(const PersistParams& P, int b, int ig, uint8_t* smem) {
+// Thread = (tile, c' sub-lane): the T*T products of one (tile, c') are read
+// with one coalesced load per position (lanes = consecutive tiles), inverse
+// transformed, and the m x m block is stored row by row -- vector stores
+// when the rows are 16-byte (8-byte) aligned, so a warp writes contiguous
+// output-row segments with no shared-memory staging.
+template <int T, int NT, int KC>
+__device__ void run_inverse_item(const PersistParams& P, int b, int ig) {
   const Geo& g = P.g;
-  constexpr int TPT = T <= 5 ? 4 : 2;        // tiles per thread (register budget)
-  constexpr int QUADS = kBlockTiles / TPT;
   constexpr int MO = T - 2;
-  float* ys = reinterpret_cast<float*>(smem);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int t0 = b * kBlockTiles;
-  const int gr0 = t0 / g.tiles_x;
-  const int tend = min(t0 + kBlockTiles, g.n_tile);
-  const int nrows = (tend - 1) / g.tiles_x - gr0 + 1;
-  const int wo_pad = P.wo_pad;
-  const int cpl = tid / QUADS;              // c' within the group
-  const int quad = tid % QUADS;
-  const int cp = ig * P.igc + cpl;
-  const int tl0 = quad * TPT;
-  const int tile0 = t0 + tl0;
-  long long tprof = 0;
-  if (g_prof_on && tid == 0) tprof = clock64();
-  if (cpl < P.igc && cp < g.Cp && tile0 < g.n_tile) {
-    const float* mslot = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * g.Cp * kBlockTiles;
-    const float* src = mslot + static_cast<size_t>(cp) * kBlockTiles + tl0;
-    const size_t pstride = static_cast<size_t>(g.Cp) * kBlockTiles;
-    float mm[TPT][T][T];
+  constexpr int SUB = NT / kBlockTiles;      // c' handled concurrently
+  const int cpo = KC ? KC : g.Cp;            // M ring rows per position
+  const int tid = threadIdx.x;
+  const int tl = tid % kBlockTiles, cs = tid / kBlockTiles;
+  const int tile = b * kBlockTiles + tl;
+  if (tile >= g.n_tile) return;
+  const int per_img = g.tiles_y * g.tiles_x;
+  const int bi = tile / per_img;
+  const int rem = tile - bi * per_img;
+  const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+  const int oy = ty * MO, ox = tx * MO;
+  const bool full = oy + MO <= g.Ho && ox + MO <= g.Wo;
+  const bool vec = full && ((MO == 4 && (g.Wo & 3) == 0) || (MO == 2 && (g.Wo & 1) == 0));
+  const float* mbase = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * cpo * kBlockTiles + tl;
+  const size_t plane = static_cast<size_t>(g.Ho) * g.Wo;
+  float* ybase = P.y + static_cast<size_t>(bi) * g.Cp * plane + static_cast<size_t>(oy) * g.Wo + ox;
+  const int c_end = min(g.Cp, (ig + 1) * P.igc);
+  for (int cp = ig * P.igc + cs; cp < c_end; cp += SUB) {
+    const float* src = mbase + static_cast<size_t>(cp) * kBlockTiles;
+    float mm[T][T];
 #pragma unroll
     for (int r = 0; r < T; ++r)
 #pragma unroll
-      for (int s = 0; s < T; ++s) {
-        if constexpr (TPT == 4) {
-          const float4 v = __ldcg(reinterpret_cast<const float4*>(src + (r * T + s) * pstride));
-          mm[0][r][s] = v.x; mm[1][r][s] = v.y; mm[2][r][s] = v.z; mm[3][r][s] = v.w;
-        } else {
-          const float2 v = __ldcg(reinterpret_cast<const float2*>(src + (r * T + s) * pstride));
-          mm[0][r][s] = v.x; mm[1][r][s] = v.y;
+      for (int s = 0; s < T; ++s) mm[r][s] = __ldcg(src + static_cast<size_t>(r * T + s) * cpo * kBlockTiles);
+    float out[MO][MO];
+    inverse_transform<T>(mm, out);
+    float* dst = ybase + static_cast<size_t>(cp) * plane;
+    if (vec) {
+#pragma unroll
+      for (int r = 0; r < MO; ++r) {
+        if constexpr (MO == 4) {
+          *reinterpret_cast<float4*>(dst + r * g.Wo) = make_float4(out[r][0], out[r][1], out[r][2], out[r][3]);
+        } else if constexpr (MO == 2) {
+          *reinterpret_cast<float2*>(dst + r * g.Wo) = make_float2(out[r][0], out[r][1]);
         }
       }
-#pragma unroll
-    for (int k = 0; k < TPT; ++k) {
-      const int tile = tile0 + k;
-      if (tile >= g.n_tile) break;
-      float out[MO][MO];
-      inverse_transform<T>(mm[k], out);
-      const int gr = tile / g.tiles_x;
-      const int tx = tile - gr * g.tiles_x;
-      float* dst = ys + ((cpl * nrows + (gr - gr0)) * MO) * wo_pad + tx * MO;
+    } else {
 #pragma unroll
       for (int r = 0; r < MO; ++r)
 #pragma unroll
-        for (int s = 0; s < MO; ++s) dst[r * wo_pad + s] = out[r][s];
+        for (int s = 0; s < MO; ++s)
+          if (oy + r < g.Ho && ox + s < g.Wo) dst[r * g.Wo + s] = out[r][s];
     }
   }
-  prof_mark(11, tprof);
-  __syncthreads();
-  prof_mark(12, tprof);
-  // coalesced write-back: one warp per (c', tile row), all MO output rows,
-  // lanes along x; only the columns this block's tiles own
-  const int total = P.igc * nrows;
-  for (int q = warp; q < total; q += NT / 32) {
-    const int j = q % nrows;
-    const int c = q / nrows;
-    const int cpo = ig * P.igc + c;
-    if (cpo >= g.Cp) continue;
-    const int gr = gr0 + j;
-    const int bi = gr / g.tiles_y, ty = gr - bi * g.tiles_y;
-    const int tlo = max(t0, gr * g.tiles_x), thi = min(tend, (gr + 1) * g.tiles_x);
-    const int xlo = (tlo - gr * g.tiles_x) * MO;
-    const int xhi = min((thi - gr * g.tiles_x) * MO, g.Wo);
-    const float* sbase = ys + (c * nrows + j) * MO * wo_pad;
-    float* dbase = P.y + ((static_cast<size_t>(bi) * g.Cp + cpo) * g.Ho + ty * MO) * g.Wo;
-#pragma unroll
-    for (int r = 0; r < MO; ++r) {
-      if (ty * MO + r >= g.Ho) break;
-      for (int xx = xlo + lane; xx < xhi; xx += 32) dbase[r * g.Wo + xx] = sbase[r * wo_pad + xx];
-    }
-  }
-  prof_mark(13, tprof);
 }
 
 // ------------------------------------------------------------------ kernel
-template <int T, int NT, int CPS>
+template <int T, int NT, int CPS, int KC>
 __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ GemmSync sy;
   __shared__ uint32_t tmem_slot;
-  __shared__ int item_s;
+  __shared__ int item_s[3];          // kind, block, sub-index (or -1: done)
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nb = P.g.n_blk;
   int* head = P.counters;
@@ -460,42 +447,51 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
   int tuse[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int n_kb = ceil_div(P.g.Cpad, kKBlock);
 
+  // item decode state, kept by thread 0 only (items are handed out in
+  // increasing order, so the step walk is amortised)
   int step = 0, step_base = 0, nf = 0, ng = 0;
   int next_item = 0;
-  if (tid == 0) next_item = atomicAdd(head, 1);
-  int step_items = items_in_step(P, 0, nf, ng);
+  int step_items = 0;
+  if (tid == 0) {
+    next_item = atomicAdd(head, 1);
+    step_items = items_in_step(P, 0, nf, ng);
+  }
   for (;;) {
     // the next item index is fetched while this one runs (hides the atomic's
     // round trip); dependencies only point backwards, so holding one
     // prefetched item cannot deadlock the queue
     if (tid == 0) {
-      item_s = next_item;
+      const int item = next_item;
       next_item = atomicAdd(head, 1);
+      if (item >= P.n_items) {
+        item_s[0] = -1;
+      } else {
+        while (item >= step_base + step_items) {
+          step_base += step_items;
+          ++step;
+          step_items = items_in_step(P, step, nf, ng);
+        }
+        const int k = item - step_base;
+        if (k < nf) { item_s[0] = 0; item_s[1] = step; item_s[2] = k; }
+        else if (k < nf + ng) { item_s[0] = 1; item_s[1] = step - P.L1; item_s[2] = k - nf; }
+        else { item_s[0] = 2; item_s[1] = step - P.L2; item_s[2] = k - nf - ng; }
+      }
     }
     __syncthreads();
-    const int item = item_s;
+    const int kind = item_s[0], b = item_s[1], sub = item_s[2];
     __syncthreads();
-    if (item >= P.n_items) break;
-    while (item >= step_base + step_items) {   // items are handed out in increasing order
-      step_base += step_items;
-      ++step;
-      step_items = items_in_step(P, step, nf, ng);
-    }
-    const int k = item - step_base;
+    if (kind < 0) break;
     long long t_a = 0, t_b = 0;
-    const int kind = k < nf ? 0 : (k < nf + ng ? 1 : 2);
     if (g_prof_on && tid == 0) t_a = clock64();
-    if (k < nf) {                                          // ---- F(step, k)
-      const int b = step;
+    if (kind == 0) {                                       // ---- F(b, sub)
       if (tid == 0 && b >= P.NU) spin_until(doneG + (b - P.NU), P.n_gg);
       if (g_prof_on && tid == 0) t_b = clock64();
       __syncthreads();
-      run_forward_item<T, NT>(P, b, k, smem, sy, fcount & 1);
+      run_forward_item<T, NT, KC>(P, b, sub, smem, sy, fcount & 1);
       ++fcount;
       __syncthreads();
       if (tid == 0) { __threadfence(); atomicAdd(doneF + b, 1); }
-    } else if (k < nf + ng) {                              // ---- G(step - L1, k - nf)
-      const int b = step - P.L1;
+    } else if (kind == 1) {                                // ---- G(b, sub)
       if (tid == 0) {
         spin_until(doneF + b, P.n_cg);
         if (b >= P.NM) spin_until(doneI + (b - P.NM), P.n_ig);
@@ -504,8 +500,8 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
       }
       __syncthreads();
       tc_fence_after();
-      const int gg = k - nf;
-      run_gemm_item<NT>(P, b, gg, smem, sy, tmem, gsteps, tuse);
+      const int gg = sub;
+      run_gemm_item<NT, KC>(P, b, gg, smem, sy, tmem, gsteps, tuse);
       const int np = min(P.gp, P.g.T * P.g.T - gg * P.gp);
       gsteps += np * n_kb;
 #pragma unroll
@@ -513,12 +509,11 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
       tc_fence_before();
       __syncthreads();
       if (tid == 0) { __threadfence(); atomicAdd(doneG + b, 1); }
-    } else {                                               // ---- I(step - L2, k - nf - ng)
-      const int b = step - P.L2;
+    } else {                                               // ---- I(b, sub)
       if (tid == 0) spin_until(doneG + b, P.n_gg);
       if (g_prof_on && tid == 0) t_b = clock64();
       __syncthreads();
-      run_inverse_item<T, NT>(P, b, k - nf - ng, smem);
+      run_inverse_item<T, NT, KC>(P, b, sub);
       __syncthreads();
       if (tid == 0) { __threadfence(); atomicAdd(doneI + b, 1); }
     }
@@ -537,7 +532,7 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
 // ------------------------------------------------------------------ host
 struct PersistPlan {
   bool ok;
-  int cpc, gp, igc, n_cg, n_gg, n_ig, NU, NM, L1, L2, wreg, trows, plane, nt, wo_pad, f_desc_off, f_max_rows, cps, stages;
+  int cpc, gp, igc, n_cg, n_gg, n_ig, NU, NM, L1, L2, wreg, trows, plane, nt, f_desc_off, f_max_rows, cps, stages;
   int f_bulk, f_shift;
   size_t u_slot, m_slot, counters_bytes, smem;
 };
@@ -553,7 +548,7 @@ static PersistPlan persist_plan(const Geo& g) {
   pl.gp = (512 / pl.cps) / g.Cppad;
   if (pl.gp > 8) pl.gp = 8;
   if (pl.gp > g.T * g.T) pl.gp = g.T * g.T;
-  pl.igc = pl.nt * (g.T <= 5 ? 4 : 2) / kBlockTiles;   // threads = 128/TPT tile groups x igc c'
+  pl.igc = 8;                              // c' per I item (thread = tile x c' sub-lane)
   pl.n_cg = g.Cpad / pl.cpc;
   pl.n_gg = ceil_div(g.T * g.T, pl.gp);
   pl.n_ig = ceil_div(g.Cp, pl.igc);
@@ -574,11 +569,8 @@ static PersistPlan persist_plan(const Geo& g) {
   pl.f_max_rows = pl.cpc * pl.trows * g.T;
   pl.f_desc_off = round_up(pl.cpc * pl.plane * 4, 16);
   const size_t f_smem = pl.f_desc_off + static_cast<size_t>(pl.f_max_rows) * 12;
-  pl.wo_pad = round_up(pl.wreg, 4) + 1;     // >= tiles_x * m >= W'
-  const size_t i_smem = static_cast<size_t>(pl.igc) * pl.trows * g.m * pl.wo_pad * 4;
   const size_t g_smem = pl.stages * (2 * kBlockTiles * kKBlock * 2 + 2 * static_cast<size_t>(g.Cppad) * kKBlock * 2);
   pl.smem = f_smem > g_smem ? f_smem : g_smem;
-  if (i_smem > pl.smem) pl.smem = i_smem;
   if (pl.smem > (pl.cps == 2 ? 108u : 200u) * 1024) return pl;
   pl.u_slot = static_cast<size_t>(g.T) * g.T * 2 * kBlockTiles * g.Cpad * 2;
   pl.m_slot = static_cast<size_t>(g.T) * g.T * g.Cp * kBlockTiles * 4;
@@ -621,9 +613,9 @@ size_t persistent_scratch_bytes(const Geo& g) {
   return round_up(static_cast<int>(pl.counters_bytes), 1024) + pl.NU * pl.u_slot + pl.NM * pl.m_slot;
 }
 
-template <int T, int NT, int CPS>
+template <int T, int NT, int CPS, int KC>
 static cudaError_t launch_persist_t(const PersistParams& P, size_t smem, int grid, cudaStream_t st) {
-  auto kern = fused_persistent_kernel<T, NT, CPS>;
+  auto kern = fused_persistent_kernel<T, NT, CPS, KC>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -651,7 +643,7 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   P.passes = passes;
   P.n_steps = g.n_blk + pl.L2;
   P.n_items = g.n_blk * (pl.n_cg + pl.n_gg + pl.n_ig);
-  P.wreg = pl.wreg; P.trows = pl.trows; P.plane = pl.plane; P.wo_pad = pl.wo_pad;
+  P.wreg = pl.wreg; P.trows = pl.trows; P.plane = pl.plane;
   P.f_desc_off = pl.f_desc_off; P.f_max_rows = pl.f_max_rows;
   P.f_bulk = pl.f_bulk; P.f_shift = pl.f_shift;
   cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
@@ -665,12 +657,19 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   }
   const int grid = sm_count * pl.cps;
   P.stages = pl.stages;
+  // square channel counts that are multiples of 16 get compile-time strides
+  const int kc = (g.Cpad == g.Cppad && g.Cppad == g.Cp && g.C == g.Cp) ? g.Cp : 0;
   switch (g.T) {
-    case 4: return launch_persist_t<4, 256, 2>(P, pl.smem, grid, st);
-    case 5: return launch_persist_t<5, 256, 2>(P, pl.smem, grid, st);
-    case 6: return launch_persist_t<6, 256, 2>(P, pl.smem, grid, st);
-    case 7: return launch_persist_t<7, 256, 1>(P, pl.smem, grid, st);
-    case 8: return launch_persist_t<8, 256, 1>(P, pl.smem, grid, st);
+    case 4: return launch_persist_t<4, 256, 2, 0>(P, pl.smem, grid, st);
+    case 5: return launch_persist_t<5, 256, 2, 0>(P, pl.smem, grid, st);
+    case 6:
+      if (kc == 64) return launch_persist_t<6, 256, 2, 64>(P, pl.smem, grid, st);
+      if (kc == 32) return launch_persist_t<6, 256, 2, 32>(P, pl.smem, grid, st);
+      return launch_persist_t<6, 256, 2, 0>(P, pl.smem, grid, st);
+    case 7: return launch_persist_t<7, 256, 1, 0>(P, pl.smem, grid, st);
+    case 8:
+      if (kc == 64) return launch_persist_t<8, 256, 1, 64>(P, pl.smem, grid, st);
+      return launch_persist_t<8, 256, 1, 0>(P, pl.smem, grid, st);
   }
   return cudaErrorInvalidValue;
 }
