@@ -109,6 +109,62 @@ __device__ __forceinline__ void inverse_transform(const float (&mm)[T][T], float
     }
 }
 
+// Two independent transforms at once on packed f32x2 (FFMA2/FADD2 on
+// sm_100): per element exactly the operations, order and rounding of the
+// scalar versions above, so the results are bitwise identical to them.
+__device__ __forceinline__ float2 f2_fma(float c, float2 x, float2 acc) {
+  return __ffma2_rn(make_float2(c, c), x, acc);
+}
+template <int T>
+__device__ __forceinline__ void forward_transform2(const float2 (&x)[T][T], float2 (&u)[T][T]) {
+  float2 t[T][T];
+#pragma unroll
+  for (int r = 0; r < T; ++r)
+#pragma unroll
+    for (int s = 0; s < T; ++s) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < T; ++q)
+        if (bt<T>(r, q) != 0.0f) acc = f2_fma(bt<T>(r, q), x[q][s], acc);
+      t[r][s] = acc;
+    }
+#pragma unroll
+  for (int r = 0; r < T; ++r)
+#pragma unroll
+    for (int s = 0; s < T; ++s) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < T; ++q)
+        if (bt<T>(s, q) != 0.0f) acc = f2_fma(bt<T>(s, q), t[r][q], acc);
+      u[r][s] = acc;
+    }
+}
+template <int T>
+__device__ __forceinline__ void inverse_transform2(const float2 (&mm)[T][T], float2 (&y)[T - 2][T - 2]) {
+  constexpr int M = T - 2;
+  float2 t[M][T];
+#pragma unroll
+  for (int r = 0; r < M; ++r)
+#pragma unroll
+    for (int s = 0; s < T; ++s) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < T; ++q)
+        if (at<T>(r, q) != 0.0f) acc = f2_fma(at<T>(r, q), mm[q][s], acc);
+      t[r][s] = acc;
+    }
+#pragma unroll
+  for (int r = 0; r < M; ++r)
+#pragma unroll
+    for (int s = 0; s < M; ++s) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < T; ++q)
+        if (at<T>(s, q) != 0.0f) acc = f2_fma(at<T>(s, q), t[r][q], acc);
+      y[r][s] = acc;
+    }
+}
+
 // Zero-filled T x T input window for one (tile, channel) (reference
 // kernels.py:73-86: origin (ty*m - pad_lo, tx*m - pad_lo), implicit padding).
 template <int T>

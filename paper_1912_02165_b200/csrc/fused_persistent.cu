@@ -199,30 +199,26 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
   const int q = lane / tpw;
   const int tile = t0 + tl;
   const int c0 = cbase + 2 * q;
-  float ua[T][T], ub[T][T];
+  float2 u2[T][T];
   if (tile < g.n_tile && warp < 4 * pairs) {
     const int per_img = g.tiles_y * g.tiles_x;
     const int bi = tile / per_img;
     const int rem = tile - bi * per_img;
     const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
     const int j = bi * g.tiles_y + ty - gr0;
-    const float* base = xs + j * row_elems + tx * g.m - g.pad_lo + P.f_shift;
-    float w[T][T];
+    const float* pa = xs + j * row_elems + tx * g.m - g.pad_lo + P.f_shift + (2 * q) * P.plane;
+    const float* pb = pa + P.plane;
+    float2 w[T][T];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float* pl = base + (2 * q + h) * P.plane;
+    for (int r = 0; r < T; ++r)
 #pragma unroll
-      for (int r = 0; r < T; ++r)
-#pragma unroll
-        for (int s = 0; s < T; ++s) w[r][s] = pl[r * P.wreg + s];
-      if (h == 0) forward_transform<T>(w, ua);
-      else forward_transform<T>(w, ub);
-    }
+      for (int s = 0; s < T; ++s) w[r][s] = make_float2(pa[r * P.wreg + s], pb[r * P.wreg + s]);
+    forward_transform2<T>(w, u2);     // channels 2q, 2q+1 of the pair (packed f32x2)
   } else {
 #pragma unroll
     for (int r = 0; r < T; ++r)
 #pragma unroll
-      for (int s = 0; s < T; ++s) ua[r][s] = ub[r][s] = 0.0f;
+      for (int s = 0; s < T; ++s) u2[r][s] = make_float2(0.0f, 0.0f);
   }
   if (warp < 4 * pairs) {
     const int cpad = KC ? KC : g.Cpad;
@@ -234,7 +230,7 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
 #pragma unroll
       for (int s = 0; s < T; ++s) {
         uint32_t hi, lo;
-        split_bf16x2(ua[r][s], ub[r][s], hi, lo);
+        split_bf16x2(u2[r][s], hi, lo);
         uint8_t* p = dst + static_cast<size_t>(r * T + s) * 2 * slab;
         *reinterpret_cast<uint32_t*>(p) = hi;
         *reinterpret_cast<uint32_t*>(p + slab) = lo;
@@ -389,31 +385,44 @@ __device__ void run_inverse_item(const PersistParams& P, int b, int ig) {
   const size_t plane = static_cast<size_t>(g.Ho) * g.Wo;
   float* ybase = P.y + static_cast<size_t>(bi) * g.Cp * plane + static_cast<size_t>(oy) * g.Wo + ox;
   const int c_end = min(g.Cp, (ig + 1) * P.igc);
-  for (int cp = ig * P.igc + cs; cp < c_end; cp += SUB) {
-    const float* src = mbase + static_cast<size_t>(cp) * kBlockTiles;
-    float mm[T][T];
+  // two c' per pass (packed f32x2 inverse); the second may be past the end
+  for (int cp = ig * P.igc + cs; cp < c_end; cp += 2 * SUB) {
+    const bool two = cp + SUB < c_end;
+    const float* src0 = mbase + static_cast<size_t>(cp) * kBlockTiles;
+    const float* src1 = two ? src0 + SUB * kBlockTiles : src0;
+    float2 mm[T][T];
 #pragma unroll
     for (int r = 0; r < T; ++r)
 #pragma unroll
-      for (int s = 0; s < T; ++s) mm[r][s] = __ldcg(src + static_cast<size_t>(r * T + s) * cpo * kBlockTiles);
-    float out[MO][MO];
-    inverse_transform<T>(mm, out);
-    float* dst = ybase + static_cast<size_t>(cp) * plane;
-    if (vec) {
-#pragma unroll
-      for (int r = 0; r < MO; ++r) {
-        if constexpr (MO == 4) {
-          *reinterpret_cast<float4*>(dst + r * g.Wo) = make_float4(out[r][0], out[r][1], out[r][2], out[r][3]);
-        } else if constexpr (MO == 2) {
-          *reinterpret_cast<float2*>(dst + r * g.Wo) = make_float2(out[r][0], out[r][1]);
-        }
+      for (int s = 0; s < T; ++s) {
+        const size_t off = static_cast<size_t>(r * T + s) * cpo * kBlockTiles;
+        mm[r][s] = make_float2(__ldcg(src0 + off), __ldcg(src1 + off));
       }
-    } else {
+    float2 out[MO][MO];
+    inverse_transform2<T>(mm, out);
 #pragma unroll
-      for (int r = 0; r < MO; ++r)
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !two) break;
+      float* dst = ybase + static_cast<size_t>(cp + h * SUB) * plane;
+      if (vec) {
 #pragma unroll
-        for (int s = 0; s < MO; ++s)
-          if (oy + r < g.Ho && ox + s < g.Wo) dst[r * g.Wo + s] = out[r][s];
+        for (int r = 0; r < MO; ++r) {
+          if constexpr (MO == 4) {
+            *reinterpret_cast<float4*>(dst + r * g.Wo) =
+                h ? make_float4(out[r][0].y, out[r][1].y, out[r][2].y, out[r][3].y)
+                  : make_float4(out[r][0].x, out[r][1].x, out[r][2].x, out[r][3].x);
+          } else if constexpr (MO == 2) {
+            *reinterpret_cast<float2*>(dst + r * g.Wo) =
+                h ? make_float2(out[r][0].y, out[r][1].y) : make_float2(out[r][0].x, out[r][1].x);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < MO; ++r)
+#pragma unroll
+          for (int s = 0; s < MO; ++s)
+            if (oy + r < g.Ho && ox + s < g.Wo) dst[r * g.Wo + s] = h ? out[r][s].y : out[r][s].x;
+      }
     }
   }
 }
@@ -579,13 +588,15 @@ static PersistPlan persist_plan(const Geo& g) {
   // A "window" = the blocks whose items occupy all CTAs at once.  Producers
   // run `lag` steps ahead of consumers; a ring slot is reused only after
   // lag + window more steps, so neither side normally waits.
-  // measured on B200 (c2): rings below ~64 MB starve the pipeline; 100 MB of
-  // the 126 MB L2 with lag 8 was the best point (tools/item_profile.py sweep)
-  size_t budget = 100ull << 20;
+  // measured on B200 (c2, tools/lag_sweep.py): rings below ~64 MB starve the
+  // pipeline and larger rings keep helping -- up to ~160 MB, i.e. somewhat
+  // beyond the 126 MB L2 (the spill costs little HBM time here) -- with a
+  // lag of 16 steps: 100 MB / lag 8: 178 us, 124 / 12: 150 us, 160 / 16: 141 us
+  size_t budget = 160ull << 20;
   if (const char* env = getenv("WF_L2_BUDGET_MB")) budget = static_cast<size_t>(atoi(env)) << 20;
   const int items_per_block = pl.n_cg + pl.n_gg + pl.n_ig;
   const int window = ceil_div(148 * pl.cps, items_per_block) + 1;
-  int lag = window < 8 ? window : 8;
+  int lag = window < 16 ? window : 16;
   if (const char* env = getenv("WF_LAG")) lag = atoi(env);
   const int slots = static_cast<int>(budget / (pl.u_slot + pl.m_slot));
   if (slots < 4) return pl;

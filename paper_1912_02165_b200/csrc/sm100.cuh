@@ -207,5 +207,10 @@ __device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uin
   const float bh = __uint_as_float(hi & 0xFFFF0000u);
   lo = pack_bf16x2(a - ah, b - bh);
 }
+__device__ __forceinline__ void split_bf16x2(float2 v, uint32_t& hi, uint32_t& lo) {
+  hi = pack_bf16x2(v.x, v.y);
+  const float2 r = __fadd2_rn(v, make_float2(-__uint_as_float(hi << 16), -__uint_as_float(hi & 0xFFFF0000u)));
+  lo = pack_bf16x2(r.x, r.y);
+}
 
 }  // namespace wf
