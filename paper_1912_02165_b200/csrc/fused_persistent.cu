@@ -64,6 +64,15 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 constexpr int kProfCtas = 512, kProfSlots = 16;
 __device__ unsigned long long g_prof[kProfCtas * kProfSlots];
 __constant__ int g_prof_on;
+// Optional item trace (WF_PROFILE=2): per item {cta, kind<<24 | block, start ns, end ns}.
+constexpr int kTraceMax = 16384;
+__device__ unsigned long long g_trace[kTraceMax * 2];
+__device__ int g_trace_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 // sub-phase marks (thread 0): slot 9 F staging, 10 F transform+store,
 // 11 I loads, 12 I transform+smem, 13 I write-back
 __device__ __forceinline__ void prof_mark(int slot, long long& t) {
@@ -106,32 +115,35 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
   long long tprof = 0;
   if (g_prof_on && tid == 0) tprof = clock64();
   if (P.f_bulk) {
-    // Rows are 16-byte aligned in global memory (W % 4 == 0): every staged
-    // row is one bulk async copy of its W interior floats (column 4 of the
-    // staged row = x 0), completing on an mbarrier; pad columns and rows
-    // outside the image are zeroed with plain stores.  All copies are in
-    // flight at once -- one memory latency per item.
+    // Rows are 16-byte aligned in global memory (W % 4 == 0) and the T
+    // window rows of a tile row are consecutive image rows, i.e. one
+    // contiguous global range: ONE bulk async copy per (channel, tile row),
+    // landing unpadded (pitch W) in shared memory; rows outside the image
+    // are zeroed with plain stores and the left/right padding columns are
+    // masked when the windows are read.  All copies complete on one mbarrier.
     fence_proxy_async_smem();
-    for (int row = tid; row < total_rows; row += NT) {
-      const int r = row % T;
-      const int rest = row / T;
-      const int j = rest % nrows;
-      const int cl = rest / nrows;
+    const int units = CPC * nrows;
+    for (int u = tid; u < units; u += NT) {
+      const int j = u % nrows;
+      const int cl = u / nrows;
       const int gr = gr0 + j;
       const int bi = gr / g.tiles_y, ty = gr - bi * g.tiles_y;
-      const int yy = ty * g.m - g.pad_lo + r;
+      const int y0 = ty * g.m - g.pad_lo;
+      const int ya = max(y0, 0), yb = min(y0 + T, g.H);
       const int c = cbase + cl;
-      float* dst = xs + cl * P.plane + j * row_elems + r * P.wreg;
-      if (c < g.C && yy >= 0 && yy < g.H && bi < g.B) {
+      float* dst = xs + cl * P.plane + j * row_elems;
+      const bool ok = c < g.C && bi < g.B && yb > ya;
+      if (ok) {
+        const uint32_t bytes = static_cast<uint32_t>((yb - ya) * g.W * 4);
         asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sy.fbar)),
-                     "r"(g.W * 4) : "memory");
-        bulk_g2s(dst + 4, P.x + ((static_cast<size_t>(bi) * g.C + c) * g.H + yy) * g.W, g.W * 4, &sy.fbar);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) dst[s] = 0.0f;
-        for (int s = 4 + g.W; s < P.wreg; ++s) dst[s] = 0.0f;
-      } else {
-        for (int s = 0; s < P.wreg; ++s) dst[s] = 0.0f;
+                     "r"(bytes) : "memory");
+        bulk_g2s(dst + (ya - y0) * g.W, P.x + ((static_cast<size_t>(bi) * g.C + c) * g.H + ya) * g.W, bytes,
+                 &sy.fbar);
       }
+      const int z0 = ok ? ya - y0 : 0, z1 = ok ? yb - y0 : 0;   // rows [z0, z1) come from the copy
+      for (int r = 0; r < T; ++r)
+        if (r < z0 || r >= z1)
+          for (int s2 = 0; s2 < g.W; ++s2) dst[r * g.W + s2] = 0.0f;
     }
     __syncthreads();
     if (tid == 0) mbar_arrive(&sy.fbar);
@@ -206,13 +218,24 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
     const int rem = tile - bi * per_img;
     const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
     const int j = bi * g.tiles_y + ty - gr0;
-    const float* pa = xs + j * row_elems + tx * g.m - g.pad_lo + P.f_shift + (2 * q) * P.plane;
+    const int x0 = tx * g.m - g.pad_lo;          // image column of window column 0
+    const float* pa = xs + j * row_elems + x0 + P.f_shift + (2 * q) * P.plane;
     const float* pb = pa + P.plane;
     float2 w[T][T];
+    if (!P.f_bulk || (x0 >= 0 && x0 + T <= g.W)) {
 #pragma unroll
-    for (int r = 0; r < T; ++r)
+      for (int r = 0; r < T; ++r)
 #pragma unroll
-      for (int s = 0; s < T; ++s) w[r][s] = make_float2(pa[r * P.wreg + s], pb[r * P.wreg + s]);
+        for (int s = 0; s < T; ++s) w[r][s] = make_float2(pa[r * P.wreg + s], pb[r * P.wreg + s]);
+    } else {                                      // unpadded staging: mask the border columns
+#pragma unroll
+      for (int r = 0; r < T; ++r)
+#pragma unroll
+        for (int s = 0; s < T; ++s) {
+          const bool in = x0 + s >= 0 && x0 + s < g.W;
+          w[r][s] = in ? make_float2(pa[r * P.wreg + s], pb[r * P.wreg + s]) : make_float2(0.0f, 0.0f);
+        }
+    }
     forward_transform2<T>(w, u2);     // channels 2q, 2q+1 of the pair (packed f32x2)
   } else {
 #pragma unroll
@@ -491,7 +514,8 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
     __syncthreads();
     if (kind < 0) break;
     long long t_a = 0, t_b = 0;
-    if (g_prof_on && tid == 0) t_a = clock64();
+    unsigned long long g_a = 0;
+    if (g_prof_on && tid == 0) { t_a = clock64(); g_a = gtimer(); }
     if (kind == 0) {                                       // ---- F(b, sub)
       if (tid == 0 && b >= P.NU) spin_until(doneG + (b - P.NU), P.n_gg);
       if (g_prof_on && tid == 0) t_b = clock64();
@@ -525,6 +549,13 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
       run_inverse_item<T, NT, KC>(P, b, sub);
       __syncthreads();
       if (tid == 0) { __threadfence(); atomicAdd(doneI + b, 1); }
+    }
+    if (g_prof_on > 1 && tid == 0) {
+      const int kk = atomicAdd(&g_trace_n, 1);
+      if (kk < kTraceMax) {
+        g_trace[2 * kk] = (static_cast<unsigned long long>(blockIdx.x) << 32) | (static_cast<unsigned>(kind) << 24) | b;
+        g_trace[2 * kk + 1] = ((gtimer() - g_a) << 40) | (g_a & ((1ull << 40) - 1));
+      }
     }
     if (g_prof_on && tid == 0) {
       unsigned long long* pr = g_prof + (blockIdx.x % kProfCtas) * kProfSlots + kind * 3;
@@ -564,17 +595,14 @@ static PersistPlan persist_plan(const Geo& g) {
   pl.wreg = (g.tiles_x - 1) * g.m + g.T;
   // bulk-copy staging needs 16-byte aligned input rows; staged column 4 = x 0
   pl.f_bulk = (g.W % 4 == 0) ? 1 : 0;
-  pl.f_shift = pl.f_bulk ? 4 : g.pad_lo;
-  if (pl.f_bulk) {
-    const int need = (g.W > pl.wreg - g.pad_lo ? g.W : pl.wreg - g.pad_lo) + 4;
-    pl.wreg = round_up(need, 4);
-  }
+  pl.f_shift = pl.f_bulk ? 0 : g.pad_lo;
+  if (pl.f_bulk) pl.wreg = g.W;             // unpadded rows, one bulk copy per (channel, tile row)
   pl.trows = ceil_div(kBlockTiles - 1, g.tiles_x) + 1;
   if (pl.trows > g.B * g.tiles_y) pl.trows = g.B * g.tiles_y;
   // plane pitch = 1 (mod 32) words: the 4 channel pairs of a warp land on
   // different banks (2-way instead of 4-way conflicts on the window reads)
   // (bulk-copy staging needs 16-byte aligned rows: pitch = 4 mod 32 instead)
-  pl.plane = round_up(pl.trows * g.T * pl.wreg, 32) + (pl.f_bulk ? 4 : 1);
+  pl.plane = round_up(pl.trows * g.T * pl.wreg, 32) + (pl.f_bulk ? 16 : 1);
   pl.f_max_rows = pl.cpc * pl.trows * g.T;
   pl.f_desc_off = round_up(pl.cpc * pl.plane * 4, 16);
   const size_t f_smem = pl.f_desc_off + static_cast<size_t>(pl.f_max_rows) * 12;
@@ -596,7 +624,7 @@ static PersistPlan persist_plan(const Geo& g) {
   if (const char* env = getenv("WF_L2_BUDGET_MB")) budget = static_cast<size_t>(atoi(env)) << 20;
   const int items_per_block = pl.n_cg + pl.n_gg + pl.n_ig;
   const int window = ceil_div(148 * pl.cps, items_per_block) + 1;
-  int lag = window < 16 ? window : 16;
+  int lag = 16;
   if (const char* env = getenv("WF_LAG")) lag = atoi(env);
   const int slots = static_cast<int>(budget / (pl.u_slot + pl.m_slot));
   if (slots < 4) return pl;
@@ -662,7 +690,7 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   {
     static int prof_state = -1;
     if (prof_state < 0) {
-      prof_state = getenv("WF_PROFILE") ? 1 : 0;
+      prof_state = getenv("WF_PROFILE") ? atoi(getenv("WF_PROFILE")) : 0;
       cudaMemcpyToSymbol(g_prof_on, &prof_state, sizeof(int));
     }
   }
@@ -696,4 +724,18 @@ extern "C" int wf_debug_fused_profile(unsigned long long* host, int n) {
   static unsigned long long zeros[kProfCtas * kProfSlots] = {0};
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(wf::g_prof, zeros, sizeof(zeros));
   return e == cudaSuccess ? 0 : 4;
+}
+
+// Debug/tuning hook: copy the item trace (2 words per item) and reset it;
+// returns the number of items recorded.
+extern "C" int wf_debug_fused_trace(unsigned long long* host, int max_items) {
+  using namespace wf;
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, wf::g_trace_n, sizeof(int));
+  if (n > kTraceMax) n = kTraceMax;
+  if (n > max_items) n = max_items;
+  cudaMemcpyFromSymbol(host, wf::g_trace, static_cast<size_t>(n) * 2 * sizeof(unsigned long long));
+  const int zero = 0;
+  cudaMemcpyToSymbol(wf::g_trace_n, &zero, sizeof(int));
+  return n;
 }
