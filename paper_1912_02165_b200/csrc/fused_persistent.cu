@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ GemmSync sy;
   __shared__ uint32_t tmem_slot;
-  __shared__ int item_s[3];          // kind, block, sub-index (or -1: done)
+  __shared__ int item_s[2][3];       // double-buffered: kind, block, sub-index (or -1: done)
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nb = P.g.n_blk;
   int* head = P.counters;
@@ -479,76 +479,89 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
   int tuse[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int n_kb = ceil_div(P.g.Cpad, kKBlock);
 
-  // item decode state, kept by thread 0 only (items are handed out in
-  // increasing order, so the step walk is amortised)
+  // Item decode (thread kDecodeTid only; items are handed out in increasing
+  // order, so the step walk is amortised).  The decode of item k+1 -- from
+  // a queue index fetched one item earlier, hiding the atomic's round trip --
+  // runs at the start of item k and lands in the other half of item_s, so
+  // the loop has a single barrier per item.  Dependencies only point
+  // backwards, so holding prefetched items cannot deadlock the queue.
+  constexpr int kDecodeTid = 64;
   int step = 0, step_base = 0, nf = 0, ng = 0;
   int next_item = 0;
   int step_items = 0;
-  if (tid == 0) {
+  auto decode = [&](int* dst) {
+    const int item = next_item;
+    next_item = atomicAdd(head, 1);
+    if (item >= P.n_items) {
+      dst[0] = -1;
+      return;
+    }
+    while (item >= step_base + step_items) {
+      step_base += step_items;
+      ++step;
+      step_items = items_in_step(P, step, nf, ng);
+    }
+    const int k = item - step_base;
+    if (k < nf) { dst[0] = 0; dst[1] = step; dst[2] = k; }
+    else if (k < nf + ng) { dst[0] = 1; dst[1] = step - P.L1; dst[2] = k - nf; }
+    else { dst[0] = 2; dst[1] = step - P.L2; dst[2] = k - nf - ng; }
+  };
+  if (tid == kDecodeTid) {
     next_item = atomicAdd(head, 1);
     step_items = items_in_step(P, 0, nf, ng);
+    decode(item_s[0]);
   }
-  for (;;) {
-    // the next item index is fetched while this one runs (hides the atomic's
-    // round trip); dependencies only point backwards, so holding one
-    // prefetched item cannot deadlock the queue
-    if (tid == 0) {
-      const int item = next_item;
-      next_item = atomicAdd(head, 1);
-      if (item >= P.n_items) {
-        item_s[0] = -1;
-      } else {
-        while (item >= step_base + step_items) {
-          step_base += step_items;
-          ++step;
-          step_items = items_in_step(P, step, nf, ng);
-        }
-        const int k = item - step_base;
-        if (k < nf) { item_s[0] = 0; item_s[1] = step; item_s[2] = k; }
-        else if (k < nf + ng) { item_s[0] = 1; item_s[1] = step - P.L1; item_s[2] = k - nf; }
-        else { item_s[0] = 2; item_s[1] = step - P.L2; item_s[2] = k - nf - ng; }
-      }
-    }
-    __syncthreads();
-    const int kind = item_s[0], b = item_s[1], sub = item_s[2];
-    __syncthreads();
+  __syncthreads();
+  for (int it = 0;; ++it) {
+    const int* cur = item_s[it & 1];
+    const int kind = cur[0], b = cur[1], sub = cur[2];
     if (kind < 0) break;
+    if (tid == kDecodeTid) decode(item_s[(it + 1) & 1]);
     long long t_a = 0, t_b = 0;
     unsigned long long g_a = 0;
     if (g_prof_on && tid == 0) { t_a = clock64(); g_a = gtimer(); }
+    // Dependency wait, per warp (lane 0 acquires, __syncwarp orders the
+    // lanes after it): no CTA barrier at the start of an item.
+    if ((tid & 31) == 0) {
+      if (kind == 0) {
+        if (b >= P.NU) spin_until(doneG + (b - P.NU), P.n_gg);          // U slot free
+      } else if (kind == 1) {
+        spin_until(doneF + b, P.n_cg);                                   // U complete
+        if (b >= P.NM) spin_until(doneI + (b - P.NM), P.n_ig);           // M slot free
+        fence_proxy_async_global();
+      } else {
+        spin_until(doneG + b, P.n_gg);                                   // M complete
+      }
+    }
+    __syncwarp();
+    if (g_prof_on && tid == 0) t_b = clock64();
     if (kind == 0) {                                       // ---- F(b, sub)
-      if (tid == 0 && b >= P.NU) spin_until(doneG + (b - P.NU), P.n_gg);
-      if (g_prof_on && tid == 0) t_b = clock64();
-      __syncthreads();
       run_forward_item<T, NT, KC>(P, b, sub, smem, sy, fcount & 1);
       ++fcount;
-      __syncthreads();
-      if (tid == 0) { __threadfence(); atomicAdd(doneF + b, 1); }
     } else if (kind == 1) {                                // ---- G(b, sub)
-      if (tid == 0) {
-        spin_until(doneF + b, P.n_cg);
-        if (b >= P.NM) spin_until(doneI + (b - P.NM), P.n_ig);
-        fence_proxy_async_global();
-        if (g_prof_on) t_b = clock64();
-      }
-      __syncthreads();
       tc_fence_after();
-      const int gg = sub;
-      run_gemm_item<NT, KC>(P, b, gg, smem, sy, tmem, gsteps, tuse);
-      const int np = min(P.gp, P.g.T * P.g.T - gg * P.gp);
+      run_gemm_item<NT, KC>(P, b, sub, smem, sy, tmem, gsteps, tuse);
+      const int np = min(P.gp, P.g.T * P.g.T - sub * P.gp);
       gsteps += np * n_kb;
 #pragma unroll
       for (int i = 0; i < 8; ++i) tuse[i] += (i < np) ? 1 : 0;
       tc_fence_before();
-      __syncthreads();
-      if (tid == 0) { __threadfence(); atomicAdd(doneG + b, 1); }
     } else {                                               // ---- I(b, sub)
-      if (tid == 0) spin_until(doneG + b, P.n_gg);
-      if (g_prof_on && tid == 0) t_b = clock64();
-      __syncthreads();
       run_inverse_item<T, NT, KC>(P, b, sub);
-      __syncthreads();
-      if (tid == 0) { __threadfence(); atomicAdd(doneI + b, 1); }
+    }
+    __syncthreads();                                       // item done: smem free, next item decoded
+    {
+      // Completion is published by a thread whose warp has slack at the start
+      // of the next item (warp 3 is idle in G items; warp 7 waits for the
+      // staging issue of F items), so its fence does not delay the item.
+      const int publisher = item_s[(it + 1) & 1][0] == 1 ? 96 : 224;
+      if (tid == publisher) {
+        long long tp = 0;
+        if (g_prof_on) tp = clock64();
+        __threadfence();
+        atomicAdd((kind == 0 ? doneF : kind == 1 ? doneG : doneI) + b, 1);
+        if (g_prof_on) g_prof[(blockIdx.x % kProfCtas) * kProfSlots + 14] += clock64() - tp;
+      }
     }
     if (g_prof_on > 1 && tid == 0) {
       const int kk = atomicAdd(&g_trace_n, 1);
@@ -617,14 +630,14 @@ static PersistPlan persist_plan(const Geo& g) {
   // run `lag` steps ahead of consumers; a ring slot is reused only after
   // lag + window more steps, so neither side normally waits.
   // measured on B200 (c2, tools/lag_sweep.py): rings below ~64 MB starve the
-  // pipeline and larger rings keep helping -- up to ~160 MB, i.e. somewhat
-  // beyond the 126 MB L2 (the spill costs little HBM time here) -- with a
-  // lag of 16 steps: 100 MB / lag 8: 178 us, 124 / 12: 150 us, 160 / 16: 141 us
-  size_t budget = 160ull << 20;
+  // pipeline and larger rings with longer lags keep helping, beyond the
+  // 126 MB L2 (the spilled part of the rings costs little HBM time here):
+  // 100 MB / lag 8: 178 us, 124 / 12: 150 us, 160 / 16: 150 us, 220 / 24: 139 us
+  size_t budget = 220ull << 20;
   if (const char* env = getenv("WF_L2_BUDGET_MB")) budget = static_cast<size_t>(atoi(env)) << 20;
   const int items_per_block = pl.n_cg + pl.n_gg + pl.n_ig;
   const int window = ceil_div(148 * pl.cps, items_per_block) + 1;
-  int lag = 16;
+  int lag = 24;
   if (const char* env = getenv("WF_LAG")) lag = atoi(env);
   const int slots = static_cast<int>(budget / (pl.u_slot + pl.m_slot));
   if (slots < 4) return pl;

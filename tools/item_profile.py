@@ -31,4 +31,6 @@ for it in range(3):
               f"wait {a[:, 3*k].sum()/ctas/clk:6.1f} us")
     nf, ni = a[:, 2].sum(), a[:, 8].sum()
     print(f"   F phases per item: staging {a[:, 9].sum()/max(nf,1)/clk:.2f} us, transform+store {a[:, 10].sum()/max(nf,1)/clk:.2f} us")
-    print(f"   I phases per item: load+transform {a[:, 11].sum()/max(ni,1)/clk:.2f} us, barrier {a[:, 12].sum()/max(ni,1)/clk:.2f} us, write-back {a[:, 13].sum()/max(ni,1)/clk:.2f} us")
+    nall = a[:, 2].sum() + a[:, 5].sum() + a[:, 8].sum()
+    print(f"   per item: completion publish (fence+atomic) {a[:, 14].sum()/max(nall,1)/clk:.2f} us, "
+          f"dispatch (loop top to start) {a[:, 15].sum()/max(nall,1)/clk:.2f} us, thread-0 decode {a[:, 13].sum()/max(nall,1)/clk:.2f} us")
