@@ -37,6 +37,7 @@ struct PersistParams {
   Geo g;
   int n_cg, n_gg, n_ig;   // items per block of each kind
   int cpc, gp, igc;       // channels per F item, positions per G item, c' per I item
+  int ftiles;             // tiles per F item (a 128-tile block is split into 128 / ftiles parts)
   int NU, NM, L1, L2;
   int passes;
   int n_steps, n_items;
@@ -105,11 +106,16 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
   float* xs = reinterpret_cast<float*>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int CPC = P.cpc;
-  const int t0 = b * kBlockTiles;
+  // item cg = (part of the block) x (channel group)
+  const int n_cgrp = g.Cpad / CPC;
+  const int part = cg / n_cgrp;
+  cg -= part * n_cgrp;
+  const int tb0 = part * P.ftiles;                 // first tile of this part inside the block
+  const int t0 = b * kBlockTiles + tb0;
   const int cbase = cg * CPC;
   const int gr0 = t0 / g.tiles_x;
-  const int tlast = min(t0 + kBlockTiles, g.n_tile) - 1;
-  const int nrows = tlast / g.tiles_x - gr0 + 1;
+  const int tlast = min(t0 + P.ftiles, g.n_tile) - 1;
+  const int nrows = tlast >= t0 ? tlast / g.tiles_x - gr0 + 1 : 0;
   const int row_elems = T * P.wreg;
   const int total_rows = CPC * nrows * T;
   long long tprof = 0;
@@ -205,14 +211,17 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
   __syncthreads();
   prof_mark(9, tprof);
 
+  // thread = (tile, channel pair); a warp = 32 / pairs tiles x all pairs, so
+  // each store instruction writes whole 16-byte core-matrix rows (CPC = 8)
   const int pairs = CPC / 2;
   const int tpw = 32 / pairs;
-  const int tl = (warp % (kBlockTiles / tpw)) * tpw + lane % tpw;
+  const int nwarps_used = P.ftiles / tpw;
+  const int tl = (warp % nwarps_used) * tpw + lane % tpw;   // tile inside the part
   const int q = lane / tpw;
   const int tile = t0 + tl;
   const int c0 = cbase + 2 * q;
   float2 u2[T][T];
-  if (tile < g.n_tile && warp < 4 * pairs) {
+  if (tile < g.n_tile && warp < nwarps_used) {
     const int per_img = g.tiles_y * g.tiles_x;
     const int bi = tile / per_img;
     const int rem = tile - bi * per_img;
@@ -243,11 +252,11 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
 #pragma unroll
       for (int s = 0; s < T; ++s) u2[r][s] = make_float2(0.0f, 0.0f);
   }
-  if (warp < 4 * pairs) {
+  if (warp < nwarps_used) {
     const int cpad = KC ? KC : g.Cpad;
     const size_t slab = static_cast<size_t>(kBlockTiles) * cpad * 2;
     uint8_t* slot = P.uring + static_cast<size_t>(b % P.NU) * T * T * 2 * slab;
-    uint8_t* dst = slot + slab_off(tl, c0, kBlockTiles, cpad);
+    uint8_t* dst = slot + slab_off(tb0 + tl, c0, kBlockTiles, cpad);
 #pragma unroll
     for (int r = 0; r < T; ++r)
 #pragma unroll
@@ -585,7 +594,7 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
 // ------------------------------------------------------------------ host
 struct PersistPlan {
   bool ok;
-  int cpc, gp, igc, n_cg, n_gg, n_ig, NU, NM, L1, L2, wreg, trows, plane, nt, f_desc_off, f_max_rows, cps, stages;
+  int cpc, ftiles, gp, igc, n_cg, n_gg, n_ig, NU, NM, L1, L2, wreg, trows, plane, nt, f_desc_off, f_max_rows, cps, stages;
   int f_bulk, f_shift;
   size_t u_slot, m_slot, counters_bytes, smem;
 };
@@ -596,13 +605,14 @@ static PersistPlan persist_plan(const Geo& g) {
   pl.nt = 256;
   pl.cps = g.T <= 6 ? 2 : 1;              // CTAs per SM (two overlap each other's latency)
   pl.stages = pl.cps == 2 ? 2 : 3;
-  pl.cpc = pl.nt / 64;                     // 128 tiles x cpc/2 pairs = nt threads
+  pl.cpc = 8;                              // one full 8-channel core-matrix column per F item
+  pl.ftiles = pl.nt / (pl.cpc / 2);        // ftiles x cpc/2 pairs = nt threads (64 tiles)
   if (g.Cpad % pl.cpc != 0 || g.Cppad > 128) return pl;
   pl.gp = (512 / pl.cps) / g.Cppad;
   if (pl.gp > 8) pl.gp = 8;
   if (pl.gp > g.T * g.T) pl.gp = g.T * g.T;
   pl.igc = 8;                              // c' per I item (thread = tile x c' sub-lane)
-  pl.n_cg = g.Cpad / pl.cpc;
+  pl.n_cg = (kBlockTiles / pl.ftiles) * (g.Cpad / pl.cpc);
   pl.n_gg = ceil_div(g.T * g.T, pl.gp);
   pl.n_ig = ceil_div(g.Cp, pl.igc);
   pl.wreg = (g.tiles_x - 1) * g.m + g.T;
@@ -610,7 +620,7 @@ static PersistPlan persist_plan(const Geo& g) {
   pl.f_bulk = (g.W % 4 == 0) ? 1 : 0;
   pl.f_shift = pl.f_bulk ? 0 : g.pad_lo;
   if (pl.f_bulk) pl.wreg = g.W;             // unpadded rows, one bulk copy per (channel, tile row)
-  pl.trows = ceil_div(kBlockTiles - 1, g.tiles_x) + 1;
+  pl.trows = ceil_div(pl.ftiles - 1, g.tiles_x) + 1;
   if (pl.trows > g.B * g.tiles_y) pl.trows = g.B * g.tiles_y;
   // plane pitch = 1 (mod 32) words: the 4 channel pairs of a warp land on
   // different banks (2-way instead of 4-way conflicts on the window reads)
@@ -690,7 +700,7 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   P.mring = reinterpret_cast<float*>(P.uring + pl.NU * pl.u_slot);
   P.g = g;
   P.n_cg = pl.n_cg; P.n_gg = pl.n_gg; P.n_ig = pl.n_ig;
-  P.cpc = pl.cpc; P.gp = pl.gp; P.igc = pl.igc;
+  P.cpc = pl.cpc; P.gp = pl.gp; P.igc = pl.igc; P.ftiles = pl.ftiles;
   P.NU = pl.NU; P.NM = pl.NM; P.L1 = pl.L1; P.L2 = pl.L2;
   P.passes = passes;
   P.n_steps = g.n_blk + pl.L2;
