@@ -354,14 +354,16 @@ __device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* sm
     const int qd = warp & 3;
     const int row = qd * 32 + lane_id();
     const int tile = b * kBlockTiles + row;
-    const int cpo = KC ? KC : g.Cp;
-    float* mslot = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * cpo * kBlockTiles;
+    // M ring layout: [p][c' pair][tile][2] -- a lane stores 8 bytes (two c'),
+    // a warp 256 contiguous bytes; the I items load the same pairs
+    const int cpo2 = KC ? KC : round_up(g.Cp, 2);
+    float* mslot = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * cpo2 * kBlockTiles;
     const bool live = tile < g.n_tile;
     for (int pl = 0; pl < np; ++pl) {
       mbar_wait(&sy.tfull[pl], tuse[pl] & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) + pl * (KC ? KC : g.Cppad);
-      float* mrow = mslot + static_cast<size_t>(p0 + pl) * cpo * kBlockTiles + row;
+      float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(p0 + pl) * cpo2 * kBlockTiles) + row;
       if constexpr (KC != 0) {
 #pragma unroll
         for (int c = 0; c < KC; c += 16) {
@@ -370,7 +372,7 @@ __device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* sm
           tmem_ld_wait();
           if (live) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) __stcg(mrow + (c + i) * kBlockTiles, v[i]);
+            for (int i = 0; i < 8; ++i) __stcg(mrow + (c / 2 + i) * kBlockTiles, make_float2(v[2 * i], v[2 * i + 1]));
           }
         }
       } else {
@@ -380,8 +382,9 @@ __device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* sm
           tmem_ld_wait();
           if (live) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c + i < g.Cp) __stcg(mrow + static_cast<size_t>(c + i) * kBlockTiles, v[i]);
+            for (int i = 0; i < 8; ++i)
+              if (c + 2 * i < g.Cp)
+                __stcg(mrow + static_cast<size_t>(c / 2 + i) * kBlockTiles, make_float2(v[2 * i], v[2 * i + 1]));
           }
         }
       }
@@ -401,7 +404,7 @@ __device__ void run_inverse_item(const PersistParams& P, int b, int ig) {
   const Geo& g = P.g;
   constexpr int MO = T - 2;
   constexpr int SUB = NT / kBlockTiles;      // c' handled concurrently
-  const int cpo = KC ? KC : g.Cp;            // M ring rows per position
+  const int cpo2 = KC ? KC : round_up(g.Cp, 2);   // M ring rows per position
   const int tid = threadIdx.x;
   const int tl = tid % kBlockTiles, cs = tid / kBlockTiles;
   const int tile = b * kBlockTiles + tl;
@@ -413,29 +416,27 @@ __device__ void run_inverse_item(const PersistParams& P, int b, int ig) {
   const int oy = ty * MO, ox = tx * MO;
   const bool full = oy + MO <= g.Ho && ox + MO <= g.Wo;
   const bool vec = full && ((MO == 4 && (g.Wo & 3) == 0) || (MO == 2 && (g.Wo & 1) == 0));
-  const float* mbase = P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * cpo * kBlockTiles + tl;
+  const float2* mbase =
+      reinterpret_cast<const float2*>(P.mring + static_cast<size_t>(b % P.NM) * g.T * g.T * cpo2 * kBlockTiles) + tl;
   const size_t plane = static_cast<size_t>(g.Ho) * g.Wo;
   float* ybase = P.y + static_cast<size_t>(bi) * g.Cp * plane + static_cast<size_t>(oy) * g.Wo + ox;
   const int c_end = min(g.Cp, (ig + 1) * P.igc);
-  // two c' per pass (packed f32x2 inverse); the second may be past the end
-  for (int cp = ig * P.igc + cs; cp < c_end; cp += 2 * SUB) {
-    const bool two = cp + SUB < c_end;
-    const float* src0 = mbase + static_cast<size_t>(cp) * kBlockTiles;
-    const float* src1 = two ? src0 + SUB * kBlockTiles : src0;
+  // one c' pair (2k, 2k+1) per pass: one 8-byte load per position, packed
+  // f32x2 inverse; the odd member may be past the end
+  for (int cp = ig * P.igc + 2 * cs; cp < c_end; cp += 2 * SUB) {
+    const bool two = cp + 1 < c_end;
+    const float2* src = mbase + static_cast<size_t>(cp / 2) * kBlockTiles;
     float2 mm[T][T];
 #pragma unroll
     for (int r = 0; r < T; ++r)
 #pragma unroll
-      for (int s = 0; s < T; ++s) {
-        const size_t off = static_cast<size_t>(r * T + s) * cpo * kBlockTiles;
-        mm[r][s] = make_float2(__ldcg(src0 + off), __ldcg(src1 + off));
-      }
+      for (int s = 0; s < T; ++s) mm[r][s] = __ldcg(src + static_cast<size_t>(r * T + s) * (cpo2 / 2) * kBlockTiles);
     float2 out[MO][MO];
     inverse_transform2<T>(mm, out);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (h == 1 && !two) break;
-      float* dst = ybase + static_cast<size_t>(cp + h * SUB) * plane;
+      float* dst = ybase + static_cast<size_t>(cp + h) * plane;
       if (vec) {
 #pragma unroll
         for (int r = 0; r < MO; ++r) {
@@ -633,7 +634,7 @@ static PersistPlan persist_plan(const Geo& g) {
   pl.smem = f_smem > g_smem ? f_smem : g_smem;
   if (pl.smem > (pl.cps == 2 ? 108u : 200u) * 1024) return pl;
   pl.u_slot = static_cast<size_t>(g.T) * g.T * 2 * kBlockTiles * g.Cpad * 2;
-  pl.m_slot = static_cast<size_t>(g.T) * g.T * g.Cp * kBlockTiles * 4;
+  pl.m_slot = static_cast<size_t>(g.T) * g.T * round_up(g.Cp, 2) * kBlockTiles * 4;
   // lags and ring sizes: ~a machine-full of items in flight between stages,
   // rings within an L2 budget
   // A "window" = the blocks whose items occupy all CTAs at once.  Producers
