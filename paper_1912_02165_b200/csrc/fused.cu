@@ -29,8 +29,16 @@ static size_t block_bytes(const Geo& g) {
   return P * 2 * kBlockTiles * g.Cpad * 2 + P * g.Nout * kBlockTiles * 4;
 }
 
+// Blocks per wave: as many as keep a wave's U and M in its share of L2, but
+// at least enough that the wave's GEMM has work for every SM twice over
+// (position x block x N-chunk items) -- for wide layers (C' >= 256) one
+// L2-sized block would leave most SMs idle and the wave loop would be
+// launch-bound.
 static int wave_blocks(const Geo& g) {
   size_t nb = kL2Budget / kLanes / block_bytes(g);
+  const int n_nc = ceil_div(g.Cppad, gemm_nc(g.Cppad));
+  const size_t nb_par = static_cast<size_t>(ceil_div(2 * 148, g.P * n_nc));
+  if (nb < nb_par) nb = nb_par;
   if (nb < 1) nb = 1;
   if (nb > static_cast<size_t>(g.n_blk)) nb = g.n_blk;
   return static_cast<int>(nb);

@@ -600,14 +600,28 @@ struct PersistPlan {
   size_t u_slot, m_slot, counters_bytes, smem;
 };
 
+static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc);
+
+// Two CTAs per SM (they overlap each other's latency) when T <= 6 and the
+// shared memory fits, else one; forward items of 64 tiles x 8 channels
+// (whole 16-byte core-matrix rows per store) when their input staging fits,
+// else 128 tiles x 4 channels (fewer staged rows per channel, for wide images).
 static PersistPlan persist_plan(const Geo& g) {
+  PersistPlan pl = {};
+  for (int cps = (g.T <= 6 ? 2 : 1); cps >= 1 && !pl.ok; --cps)
+    for (int cpc = 8; cpc >= 4 && !pl.ok; cpc /= 2) pl = persist_plan_cpc(g, cps, cpc);
+  return pl;
+}
+
+static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   PersistPlan pl = {};
   if (g.fft) return pl;                    // FFT-16 runs the staged L2 waves
   pl.nt = 256;
-  pl.cps = g.T <= 6 ? 2 : 1;              // CTAs per SM (two overlap each other's latency)
+  pl.cps = cps;
   pl.stages = pl.cps == 2 ? 2 : 3;
-  pl.cpc = 8;                              // one full 8-channel core-matrix column per F item
-  pl.ftiles = pl.nt / (pl.cpc / 2);        // ftiles x cpc/2 pairs = nt threads (64 tiles)
+  pl.cpc = cpc;
+  pl.ftiles = pl.nt / (pl.cpc / 2);        // ftiles x cpc/2 pairs = nt threads
+  if (pl.ftiles > kBlockTiles) return pl;
   if (g.Cpad % pl.cpc != 0 || g.Cppad > 128) return pl;
   pl.gp = (512 / pl.cps) / g.Cppad;
   if (pl.gp > 8) pl.gp = 8;
@@ -723,9 +737,14 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   // square channel counts that are multiples of 16 get compile-time strides
   const int kc = (g.Cpad == g.Cppad && g.Cppad == g.Cp && g.C == g.Cp) ? g.Cp : 0;
   switch (g.T) {
-    case 4: return launch_persist_t<4, 256, 2, 0>(P, pl.smem, grid, st);
-    case 5: return launch_persist_t<5, 256, 2, 0>(P, pl.smem, grid, st);
+    case 4:
+      if (pl.cps == 1) return launch_persist_t<4, 256, 1, 0>(P, pl.smem, grid, st);
+      return launch_persist_t<4, 256, 2, 0>(P, pl.smem, grid, st);
+    case 5:
+      if (pl.cps == 1) return launch_persist_t<5, 256, 1, 0>(P, pl.smem, grid, st);
+      return launch_persist_t<5, 256, 2, 0>(P, pl.smem, grid, st);
     case 6:
+      if (pl.cps == 1) return launch_persist_t<6, 256, 1, 0>(P, pl.smem, grid, st);
       if (kc == 64) return launch_persist_t<6, 256, 2, 64>(P, pl.smem, grid, st);
       if (kc == 32) return launch_persist_t<6, 256, 2, 32>(P, pl.smem, grid, st);
       return launch_persist_t<6, 256, 2, 0>(P, pl.smem, grid, st);
