@@ -155,66 +155,68 @@ __global__ void __launch_bounds__(256, 1) fft_forward_kernel(const float* __rest
   }
 }
 
-__global__ void __launch_bounds__(256, 1) fft_inverse_kernel(const float* __restrict__ M, float* __restrict__ y,
-                                                             Geo g, int tile0, int ntile, int ldm) {
-  extern __shared__ float smem[];
-  float* sre = smem;
-  float* sim = smem + kBins * kBinPitch;
-  const int grp = threadIdx.x >> 4, r = threadIdx.x & 15;
-  float* gre = smem + 2 * kBins * kBinPitch + grp * kGroupScratch;
-  float* gim = gre + 144;
-  const unsigned gmask = 0xFFFFu << (threadIdx.x & 16);
-  const int tl0 = blockIdx.x * kFftTiles;
-  const int cg0 = blockIdx.y * kFftCh;
+// Inverse: CTA = 32 tiles x 4 output channels, 9 warps.  Pass 1: warp v
+// runs the complex 16-point inverse FFT down spectrum column v for its 32
+// tiles (lane = tile: every load of M is one coalesced 128-byte row) and
+// keeps rows 0..13 in shared memory.  Pass 2: thread = (tile, c', output
+// row r) runs the inverse real DFT over the 9 columns and stores its 14
+// outputs (a warp covers whole output-row segments of adjacent tiles).
+constexpr int kInvTiles = 32;
+constexpr int kInvCh = 4;
+constexpr int kInvThreads = 9 * 32;
+constexpr size_t kInvSmem = static_cast<size_t>(kInvCh) * 14 * 9 * kInvTiles * sizeof(float2);
 
-  // ---- load M[p][part*C' + c'][tile] for 16 tiles x 8 channels x 144 bins.
-  for (int i = threadIdx.x; i < kBins * 2 * kFftCh * kFftTiles; i += blockDim.x) {
-    const int t = i & 15, c = (i >> 4) & 7, part = (i >> 7) & 1, p = i >> 8;
-    const int tl = tl0 + t, cp = cg0 + c;
-    float v = 0.0f;
-    if (tl < ntile && cp < g.Cp) v = __ldcg(M + (static_cast<size_t>(p) * g.Nout + part * g.Cp + cp) * ldm + tl);
-    (part ? sim : sre)[stage_idx(p, c, t)] = v;
+__global__ void __launch_bounds__(kInvThreads) fft_inverse_kernel(const float* __restrict__ M, float* __restrict__ y,
+                                                                   Geo g, int tile0, int ntile, int ldm) {
+  extern __shared__ float2 zs[];                 // [c][r][v][tile]
+  const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
+  const int tl0 = blockIdx.x * kInvTiles;
+  const int cg0 = blockIdx.y * kInvCh;
+  const int tl = tl0 + lane;
+  const bool tvalid = tl < ntile;
+  for (int c = 0; c < kInvCh; ++c) {
+    const int cp = cg0 + c;
+    float re[16], im[16];
+    if (tvalid && cp < g.Cp) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const size_t row = static_cast<size_t>(u * 9 + v) * g.Nout;
+        re[u] = __ldcg(M + (row + cp) * ldm + tl);
+        im[u] = __ldcg(M + (row + g.Cp + cp) * ldm + tl);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) re[u] = im[u] = 0.0f;
+    }
+    fft::fft16<1>(re, im);
+#pragma unroll
+    for (int r = 0; r < 14; ++r) zs[((c * 14 + r) * 9 + v) * kInvTiles + lane] = make_float2(re[r], im[r]);
   }
   __syncthreads();
-
-  const int tl = tl0 + grp, tile = tile0 + tl;
-  if (tl >= ntile) return;
-  int b = 0, ty = 0, tx = 0;
-  tile_coords(g, tile, b, ty, tx);
-  const int oy = ty * g.m + r, ox = tx * g.m;
-  for (int c = 0; c < kFftCh; ++c) {
+  for (int u = threadIdx.x; u < kInvCh * 14 * kInvTiles; u += kInvThreads) {
+    const int t = u % kInvTiles;
+    const int r = (u / kInvTiles) % 14;
+    const int c = u / (kInvTiles * 14);
     const int cp = cg0 + c;
-    if (cp >= g.Cp) break;
-    if (r < 9) {
-      float cr[16], ci[16];
+    const int tli = tl0 + t;
+    if (tli >= ntile || cp >= g.Cp) continue;
+    int b = 0, ty = 0, tx = 0;
+    tile_coords(g, tile0 + tli, b, ty, tx);
+    const int oy = ty * g.m + r, ox = tx * g.m;
+    if (oy >= g.Ho) continue;
+    float zr[9], zi[9];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        cr[q] = sre[stage_idx(q * 9 + r, c, grp)];
-        ci[q] = sim[stage_idx(q * 9 + r, c, grp)];
-      }
-      fft::fft16<1>(cr, ci);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        gre[q * 9 + r] = cr[q];
-        gim[q * 9 + r] = ci[q];
-      }
+    for (int k = 0; k < 9; ++k) {
+      const float2 z = zs[((c * 14 + r) * 9 + k) * kInvTiles + t];
+      zr[k] = z.x;
+      zi[k] = z.y;
     }
-    __syncwarp(gmask);
-    if (r < 14 && oy < g.Ho) {
-      float zr[9], zi[9];
+    float out[14];
+    fft::irfft16<14>(zr, zi, out);
+    float* dst = y + ((static_cast<size_t>(b) * g.Cp + cp) * g.Ho + oy) * g.Wo + ox;
 #pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        zr[k] = gre[r * 9 + k];
-        zi[k] = gim[r * 9 + k];
-      }
-      float out[14];
-      fft::irfft16<14>(zr, zi, out);
-      float* dst = y + ((static_cast<size_t>(b) * g.Cp + cp) * g.Ho + oy) * g.Wo + ox;
-#pragma unroll
-      for (int s = 0; s < 14; ++s)
-        if (ox + s < g.Wo) dst[s] = out[s] * (1.0f / 256.0f);
-    }
-    __syncwarp(gmask);
+    for (int s2 = 0; s2 < 14; ++s2)
+      if (ox + s2 < g.Wo) dst[s2] = out[s2] * (1.0f / 256.0f);
   }
 }
 
@@ -239,13 +241,13 @@ cudaError_t launch_fft_inverse(const float* M, float* y, const Geo& g, int tile0
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(fft_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kFftSmem));
+                                         static_cast<int>(kInvSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(ceil_div(ntile, kFftTiles), ceil_div(g.Cp, kFftCh));
+  dim3 grid(ceil_div(ntile, kInvTiles), ceil_div(g.Cp, kInvCh));
   note_launch();
-  fft_inverse_kernel<<<grid, 256, kFftSmem, st>>>(M, y, g, tile0, ntile, ldm);
+  fft_inverse_kernel<<<grid, kInvThreads, kInvSmem, st>>>(M, y, g, tile0, ntile, ldm);
   return cudaGetLastError();
 }
 
