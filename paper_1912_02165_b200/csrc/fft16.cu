@@ -11,7 +11,7 @@
 //     ([Re | Im] of M) on the same tcgen05 position GEMM as Winograd;
 //   * irfft2 of each product window, keep the valid 14 x 14 block.
 //
-// Forward: one CTA = 16 tiles x 8 input channels, 16 half-warp groups.  A
+// Forward: one CTA = 8 tiles x 8 input channels, 16 half-warp groups.  A
 // group computes one (tile, channel) 2-D FFT at a time: thread r does the
 // real 16-point DFT of window row r, the row spectra go through a per-group
 // shared scratch, then threads v = 0..8 run the complex 16-point FFT down
@@ -28,16 +28,16 @@
 namespace wf {
 namespace {
 
-constexpr int kFftTiles = 16;            // tiles per CTA
+constexpr int kFftTiles = 8;             // tiles per CTA (one 8-row core-matrix group of the slab)
 constexpr int kFftCh = 8;                // channels per CTA
 constexpr int kBins = 144;               // 16 x 9
-constexpr int kBinPitch = 129;           // floats per bin in the staging arrays (odd: conflict-free columns)
+constexpr int kBinPitch = 65;            // floats per bin in the staging arrays (odd: conflict-free columns)
 constexpr int kGroupScratch = 2 * 144;   // per-group row spectra (re, im), pitch 9 per row
 constexpr size_t kFftSmem = (2ull * kBins * kBinPitch + 16ull * kGroupScratch) * sizeof(float);
 
 __device__ __forceinline__ int stage_idx(int p, int c, int t) { return p * kBinPitch + c * kFftTiles + t; }
 
-__global__ void __launch_bounds__(256, 1) fft_forward_kernel(const float* __restrict__ x, uint8_t* __restrict__ u,
+__global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __restrict__ x, uint8_t* __restrict__ u,
                                                              Geo g, int tile0, int nblk_local) {
   extern __shared__ float smem[];
   float* sre = smem;
@@ -50,15 +50,17 @@ __global__ void __launch_bounds__(256, 1) fft_forward_kernel(const float* __rest
   const int tl0 = blockIdx.x * kFftTiles;   // first local tile of this CTA
   const int cg0 = blockIdx.y * kFftCh;      // first input channel
 
-  // ---- 2-D FFTs: group grp owns tile grp, channels 0..7 in turn.
+  // ---- 2-D FFTs: group grp owns tile grp & 7, channels 4 * (grp >> 3) + 0..3.
   {
-    const int tl = tl0 + grp, tile = tile0 + tl;
+    const int tg = grp & (kFftTiles - 1);
+    const int tl = tl0 + tg, tile = tile0 + tl;
     const bool tvalid = tl < local_limit && tile < g.n_tile;
     int b = 0, ty = 0, tx = 0;
     if (tvalid) tile_coords(g, tile, b, ty, tx);
     const int iy = ty * g.m - g.pad_lo + r, ox = tx * g.m - g.pad_lo;
     const bool rvalid = tvalid && iy >= 0 && iy < g.H;
-    for (int c = 0; c < kFftCh; ++c) {
+    for (int ci4 = 0; ci4 < kFftCh / 2; ++ci4) {
+      const int c = (grp >> 3) * (kFftCh / 2) + ci4;
       const int ch = cg0 + c;
       float row[16];
       if (rvalid && ch < g.C) {
@@ -90,8 +92,8 @@ __global__ void __launch_bounds__(256, 1) fft_forward_kernel(const float* __rest
         fft::fft16<-1>(cr, ci);
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          sre[stage_idx(q * 9 + r, c, grp)] = cr[q];
-          sim[stage_idx(q * 9 + r, c, grp)] = ci[q];
+          sre[stage_idx(q * 9 + r, c, tg)] = cr[q];
+          sim[stage_idx(q * 9 + r, c, tg)] = ci[q];
         }
       }
       __syncwarp(gmask);
@@ -104,13 +106,13 @@ __global__ void __launch_bounds__(256, 1) fft_forward_kernel(const float* __rest
   const int tid = threadIdx.x;
   if ((g.C & 7) == 0) {
     // Re and Im 8-channel groups are both aligned core-matrix columns.
-    const int q = tid & 3, t = (tid >> 2) & 15, part = (tid >> 6) & 1, pp = tid >> 7;
+    const int q = tid & 3, t = (tid >> 2) & 7, part = (tid >> 5) & 1, pp = tid >> 6;
     const int tl = tl0 + t;
     if (tl < local_limit) {
       const int blk = tl / kBlockTiles, row = tl % kBlockTiles;
       const uint32_t off = slab_off(row, (part ? g.C : 0) + cg0 + 2 * q, kBlockTiles, g.Cpad);
       const float* sa = part ? sim : sre;
-      for (int p = pp; p < kBins; p += 2) {
+      for (int p = pp; p < kBins; p += 4) {
         uint32_t hi, lo;
         split_bf16x2(sa[stage_idx(p, 2 * q, t)], sa[stage_idx(p, 2 * q + 1, t)], hi, lo);
         uint8_t* base = u + ((static_cast<size_t>(p) * nblk_local + blk) * 2) * slab + off;
@@ -120,13 +122,13 @@ __global__ void __launch_bounds__(256, 1) fft_forward_kernel(const float* __rest
     }
   } else {
     // General channel counts: element-wise 16-bit stores.
-    const int c = tid & 7, t = (tid >> 3) & 15, part = (tid >> 7) & 1;
+    const int c = tid & 7, t = (tid >> 3) & 7, part = (tid >> 6) & 1, pp = tid >> 7;
     const int tl = tl0 + t;
     if (tl < local_limit && cg0 + c < g.C) {
       const int blk = tl / kBlockTiles, row = tl % kBlockTiles;
       const uint32_t off = slab_off(row, (part ? g.C : 0) + cg0 + c, kBlockTiles, g.Cpad);
       const float* sa = part ? sim : sre;
-      for (int p = 0; p < kBins; ++p) {
+      for (int p = pp; p < kBins; p += 2) {
         const float v = sa[stage_idx(p, c, t)];
         const uint32_t hv = pack_bf16x2(v, 0.0f);
         const float vh = __uint_as_float(hv << 16);
@@ -155,14 +157,14 @@ __global__ void __launch_bounds__(256, 1) fft_forward_kernel(const float* __rest
   }
 }
 
-// Inverse: CTA = 32 tiles x 4 output channels, 9 warps.  Pass 1: warp v
+// Inverse: CTA = 32 tiles x 2 output channels, 9 warps.  Pass 1: warp v
 // runs the complex 16-point inverse FFT down spectrum column v for its 32
 // tiles (lane = tile: every load of M is one coalesced 128-byte row) and
 // keeps rows 0..13 in shared memory.  Pass 2: thread = (tile, c', output
 // row r) runs the inverse real DFT over the 9 columns and stores its 14
 // outputs (a warp covers whole output-row segments of adjacent tiles).
 constexpr int kInvTiles = 32;
-constexpr int kInvCh = 4;
+constexpr int kInvCh = 2;
 constexpr int kInvThreads = 9 * 32;
 constexpr size_t kInvSmem = static_cast<size_t>(kInvCh) * 14 * 9 * kInvTiles * sizeof(float2);
 
