@@ -398,7 +398,7 @@ class LayerPlan:
     with CUDA events or captured into a CUDA graph.  Used by bench.py.
     """
 
-    def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None):
+    def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None, scratch=None):
         cfg = config or EngineConfig(kind="fused")
         if cfg.kind == "direct":
             raise InvalidParameterError("LayerPlan covers the transformed engines")
@@ -416,7 +416,10 @@ class LayerPlan:
             self.nbytes = int(self.lib.wf_fused_scratch_bytes(self.layer, cfg.tile, self.tf, 0))
         else:
             self.nbytes = int(self.lib.wf_three_stage_scratch_bytes(self.layer, cfg.tile, self.tf))
-        self.scratch = _dev.torch.empty(max(self.nbytes, 16), dtype=_dev.torch.uint8, device=self.dev)
+        if scratch is not None and scratch.numel() >= self.nbytes:
+            self.scratch = scratch                    # shared with other plans on the same stream
+        else:
+            self.scratch = _dev.torch.empty(max(self.nbytes, 16), dtype=_dev.torch.uint8, device=self.dev)
         self.vpack = self.pack.device_mma(self.dev)
         self.out = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=self.dev)
 
@@ -433,3 +436,47 @@ class LayerPlan:
                                               self.tf, self.prec, stream)
         _lib.check(rc, "LayerPlan")
         return y
+
+
+class LayerStack:
+    """Back-to-back layers on one stream (layer chaining).
+
+    ``LayerStack(specs, packs, configs)`` plans every layer once; calling it
+    runs them in order on the current stream -- layer i's output buffer is
+    layer i+1's input, with no host synchronisation, re-layout or copy in
+    between (activations stay NCHW f32 in HBM).  The layers share one
+    scratch buffer (the size of the largest), which is safe because they are
+    stream-ordered.  As in the reference there is no bias, activation or
+    pooling between layers, so consecutive specs must match:
+    ``specs[i].output_dims() == specs[i + 1].input_dims()``.
+    """
+
+    def __init__(self, specs, packs, configs):
+        specs, packs = list(specs), list(packs)
+        configs = list(configs) if isinstance(configs, (list, tuple)) else [configs] * len(specs)
+        if not specs or not (len(specs) == len(packs) == len(configs)):
+            raise InvalidParameterError("LayerStack needs matching, non-empty specs / packs / configs")
+        for i in range(len(specs) - 1):
+            if specs[i].output_dims() != specs[i + 1].input_dims():
+                raise ShapeMismatchError(f"layer {i} output {specs[i].output_dims()} does not feed layer {i + 1} "
+                                         f"input {specs[i + 1].input_dims()}")
+        self.plans = []
+        shared = None
+        for spec, pack, cfg in zip(specs, packs, configs):
+            plan = LayerPlan(spec, pack, cfg, scratch=shared)
+            if shared is None or plan.scratch.numel() > shared.numel():
+                shared = plan.scratch
+            self.plans.append(plan)
+        # give every plan the largest scratch so none keeps a private copy
+        for plan in self.plans:
+            plan.scratch = shared
+
+    def __call__(self, x):
+        """Launch every layer on the current stream; returns the last output."""
+        for plan in self.plans:
+            x = plan(x)
+        return x
+
+    @property
+    def direct_flops(self) -> int:
+        return sum(p.spec.direct_flops() for p in self.plans)

@@ -1,0 +1,92 @@
+"""Suite / report / CLI re-target and layer chaining."""
+import json
+
+import numpy as np
+import pytest
+
+import paper_1912_02165_b200 as wf
+from paper_1912_02165_b200 import cli, suite
+from oracle import oracle as O
+
+
+def _fake_results():
+    a = suite.BenchResult(label="l1", engine="fused", tile=6, r=24, workers=148, times_ms=[1.0, 2.0],
+                          median_ms=1.5, min_ms=1.0, flops=10, tasks=3, verify="pass", max_rel_err=1e-4,
+                          direct_flops=int(3e9), batch=4, t_roof_s=1e-4)
+    b = suite.BenchResult(label="l1", engine="three_stage", tile=6, r=24, workers=148, median_ms=3.0,
+                          min_ms=2.9, flops=10, direct_flops=int(3e9), batch=4, t_roof_s=1e-4)
+    c = suite.BenchResult(label="l2", engine="fused", tile=6, r=24, workers=0, error="boom", verify="error")
+    return [a, b, c]
+
+
+def test_report_formats_share_values():
+    res = _fake_results()
+    rows = json.loads(suite.emit_report(res, "json"))
+    assert [r["engine"] for r in rows] == ["fused", "three_stage", "fused"]
+    assert rows[0]["tflops"] == 2.0 and rows[0]["roofline_frac"] == pytest.approx(0.0667, abs=1e-4)
+    assert rows[2]["error"] == "boom" and rows[2]["verify"] == "error"
+    csv_text = suite.emit_report(res, "csv")
+    assert csv_text.splitlines()[0].split(",") == suite.CSV_COLUMNS
+    table = suite.emit_report(res, "table")
+    assert "2.00x" in table and "error: boom" in table
+    with pytest.raises(wf.InvalidParameterError):
+        suite.emit_report(res, "xml")
+    with pytest.raises(wf.InvalidParameterError):
+        suite.emit_report([], "csv")
+
+
+def test_builtin_suites_and_roofline():
+    assert [l for l, _ in suite.builtin_suite("resnet")][0] == "resnet_64ch_56"
+    assert len(suite.builtin_suite("vgg16")) == 13 and len(suite.builtin_suite("sweep")) == 12
+    with pytest.raises(wf.InvalidParameterError):
+        suite.builtin_suite("nope")
+    spec = wf.LayerSpec(64, 64, 64, 56, 56, 3, 1, 1)
+    t = suite.roofline_seconds(spec, 6, peaks={"hbm_gbs": 6545.3, "bf16_tflops": 1657.2})
+    assert t == pytest.approx(103350272 / 6545.3e9, rel=1e-9)      # c2 is HBM-bound
+
+
+def test_cli_parser_and_dump_basis(capsys):
+    assert cli.main(["dump-basis", "--tile", "4"]) == 0
+    out = capsys.readouterr().out
+    assert "tile T=4" in out and "[1, 1, 1, 0]" in out
+    args = cli.build_parser().parse_args(["bench", "--suite", "resnet", "--engines", "fused", "--transform", "fft"])
+    assert args.suite == "resnet" and args.transform == "fft"
+
+
+def test_layer_stack_rejects_mismatched_layers():
+    a = wf.LayerSpec(1, 8, 16, 10, 10, 3, 1, 1)
+    b = wf.LayerSpec(1, 8, 8, 10, 10, 3, 1, 1)          # expects 8 channels, gets 16
+    with pytest.raises(wf.ShapeMismatchError):
+        wf.LayerStack([a, b], [None, None], wf.EngineConfig())
+
+
+@pytest.mark.gpu
+def test_layer_stack_matches_layer_by_layer(cuda_dev):
+    import torch
+    specs = [wf.LayerSpec(2, 8, 32, 30, 30, 3, 1, 1), wf.LayerSpec(2, 32, 32, 30, 30, 3, 1, 1),
+             wf.LayerSpec(2, 32, 16, 30, 30, 3, 1, 1)]
+    cfgs = [wf.EngineConfig(kind="fused", tile=6, device=cuda_dev),
+            wf.EngineConfig(kind="three_stage", tile=4, device=cuda_dev),
+            wf.EngineConfig(kind="fused", transform="fft", tile=16, device=cuda_dev)]
+    packs = []
+    for i, (s, c) in enumerate(zip(specs, cfgs)):
+        w = wf.new_tensor(s.kernel_dims(), seed=10 + i)
+        basis = wf.make_fft_basis() if c.transform == "fft" else wf.make_basis(c.tile)
+        packs.append(wf.transform_kernels(w, basis))
+    x = wf.new_tensor(specs[0].input_dims(), seed=3)
+    stack = wf.LayerStack(specs, packs, cfgs)
+    y = stack(torch.from_numpy(x.data).to(cuda_dev)).cpu().numpy()
+    ref = x
+    for s, p, c in zip(specs, packs, cfgs):
+        ref, _ = wf.run_engine(c.kind, ref, p, s, c)
+    assert np.array_equal(y, ref.data)
+
+
+@pytest.mark.gpu
+def test_run_suite_small_layer_verifies(cuda_dev):
+    entries = [("small", wf.LayerSpec(2, 16, 16, 20, 20, 3, 1, 1))]
+    res = suite.run_suite(entries, ["fused", "three_stage", "direct"], tile=6, reps=2, warmup=1, verify=True,
+                          device=cuda_dev)
+    assert all(r.error is None and r.verify == "pass" for r in res), [(r.error, r.verify) for r in res]
+    rows = json.loads(suite.emit_report(res, "json"))
+    assert all(r["tflops"] > 0 for r in rows)
