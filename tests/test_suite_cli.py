@@ -90,3 +90,31 @@ def test_run_suite_small_layer_verifies(cuda_dev):
     assert all(r.error is None and r.verify == "pass" for r in res), [(r.error, r.verify) for r in res]
     rows = json.loads(suite.emit_report(res, "json"))
     assert all(r["tflops"] > 0 for r in rows)
+
+
+def test_reference_planner_restatement_matches_published_example():
+    # The reference README's planner example (skylakex-like model, C = C' = 64,
+    # T = 7): r_lower 20, r_upper 40, predicted utilization 0.457.
+    from paper_1912_02165_b200 import roofline
+    m = roofline.MachineModel.from_dict({"name": "skylakex-like", "peak_flops": 3.5e12,
+                                         "mem_bandwidth_bytes_per_s": 100e9, "l3_bandwidth_bytes_per_s": 350e9,
+                                         "l2_bytes_per_core": 1048576, "l3_bytes": 33554432, "cores": 28})
+    rep = roofline.plan(wf.LayerSpec(64, 64, 64, 56, 56, 3, 1, 1), 7, m)
+    assert (rep.r_lower, rep.r_upper, rep.chosen_r, rep.feasible) == (20, 40, 40, True)
+    assert round(rep.utilization_overall, 3) == 0.457 and rep.l3_fits
+    with pytest.raises(wf.MachineModelError):
+        roofline.MachineModel.from_dict({"name": "x"})
+
+
+def test_b200_planner_levels():
+    from paper_1912_02165_b200 import roofline
+    mach = roofline.B200Model.from_file(roofline.sample_model_path("b200"))
+    c2 = roofline.plan_b200(wf.LayerSpec(64, 64, 64, 56, 56, 3, 1, 1), 6, mach)
+    assert c2.n_tile == 12544 and c2.blocks == 98
+    assert c2.bytes["hbm_fused"] == 103350272                     # Q_fused of SURVEY.md 8(d)
+    assert c2.bytes["hbm_three"] == 103350272 + 8 * 36 * 12544 * 128
+    assert c2.predicted_winner == "fused" and "persistent" in c2.fused_variant
+    assert c2.r_upper < 128 <= c2.r_lower + 64                     # a 128-tile block does not fit one SM
+    fft = roofline.plan_b200(wf.LayerSpec(128, 64, 64, 56, 56, 3, 1, 1), 16, mach, transform="fft")
+    assert fft.n_tile == 2048 and "waves" in fft.fused_variant
+    assert "predicted winner" in c2.format()
