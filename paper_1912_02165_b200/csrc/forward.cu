@@ -23,9 +23,10 @@ __device__ __forceinline__ void grid_dependents_launch() {
 }
 
 struct FwdStage {
-  int wreg;      // staged row width  = (tiles_x - 1) * m + T
+  int wreg;      // staged row width: (tiles_x - 1) * m + T (padded rows) or W (bulk path)
   int trows;     // max tile rows touched by one block
   int plane;     // floats per staged channel (padded)
+  int bulk;      // 1: rows staged by bulk async copies, unpadded (W % 4 == 0)
 };
 
 template <int T, int CPC>
@@ -33,6 +34,7 @@ __global__ void __launch_bounds__(64 * CPC, (T <= 6 && CPC <= 4) ? 2 : 1)
 forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo g, int blk0,
                       int nblk_local, FwdStage S) {
   extern __shared__ float xs[];
+  __shared__ uint64_t stage_bar;
   constexpr int PAIRS = CPC / 2;
   constexpr int TPW = 32 / PAIRS;  // tiles per warp
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -46,9 +48,44 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
 
   grid_dependency_wait();
 
+  const int row_elems = T * S.wreg;
+  if (S.bulk) {
+    // ---- the T window rows of a tile row are consecutive image rows: ONE
+    // bulk async copy per (channel, tile row), all in flight at once,
+    // unpadded (pitch W); rows outside the image are zeroed, border columns
+    // are masked when the windows are read
+    if (tid == 0) {
+      mbar_init(&stage_bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    fence_proxy_async_smem();
+    for (int u = tid; u < CPC * nrows; u += blockDim.x) {
+      const int j = u % nrows, cl = u / nrows;
+      const int gr = gr0 + j;
+      const int b = gr / g.tiles_y, ty = gr - b * g.tiles_y;
+      const int y0 = ty * g.m - g.pad_lo;
+      const int ya = max(y0, 0), yb = min(y0 + T, g.H);
+      const int c = cbase + cl;
+      float* dst = xs + cl * S.plane + j * row_elems;
+      const bool ok = c < g.C && b < g.B && yb > ya;
+      if (ok) {
+        const uint32_t bytes = static_cast<uint32_t>((yb - ya) * g.W * 4);
+        mbar_add_tx(&stage_bar, bytes);
+        bulk_g2s(dst + (ya - y0) * g.W, x + ((static_cast<size_t>(b) * g.C + c) * g.H + ya) * g.W, bytes,
+                 &stage_bar);
+      }
+      const int z0 = ok ? ya - y0 : 0, z1 = ok ? yb - y0 : 0;
+      for (int r = 0; r < T; ++r)
+        if (r < z0 || r >= z1)
+          for (int s2 = 0; s2 < g.W; ++s2) dst[r * g.W + s2] = 0.0f;
+    }
+    __syncthreads();
+    if (tid == 0) mbar_arrive(&stage_bar);
+    mbar_wait(&stage_bar, 0);
+  } else {
   // ---- stage the input rows of this block's tile rows, zero padded; one
   // warp per staged row, lanes along the row (coalesced 128-byte loads)
-  const int row_elems = T * S.wreg;
   const int total_rows = CPC * nrows * T;
   for (int row = warp; row < total_rows; row += blockDim.x / 32) {
     const int r = row % T;
@@ -67,35 +104,45 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
     }
   }
   __syncthreads();
+  }
 
   // ---- transform: thread = (tile tl, channel pair q)
   const int tl = (warp % (kBlockTiles / TPW)) * TPW + lane % TPW;
   const int q = (warp / (kBlockTiles / TPW)) * PAIRS + lane / TPW;  // always 0..PAIRS-1 here
   const int tile = t0 + tl;
   const int c0 = cbase + 2 * q;
-  float ua[T][T], ub[T][T];
+  float2 u2[T][T];
   if (tile < g.n_tile) {
     const int b = tile / per_img;
     const int rem = tile - b * per_img;
     const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
     const int j = b * g.tiles_y + ty - gr0;
-    const float* base = xs + j * row_elems + tx * g.m;
-    float w[T][T];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float* pl = base + (2 * q + h) * S.plane;
+    // window column 0 = staged column tx*m (padded rows) or image column
+    // tx*m - pad_lo (bulk rows, masked at the borders)
+    const int x0 = tx * g.m - (S.bulk ? g.pad_lo : 0);
+    const float* pa = xs + j * row_elems + x0 + (2 * q) * S.plane;
+    const float* pb = pa + S.plane;
+    float2 w[T][T];
+    if (!S.bulk || (x0 >= 0 && x0 + T <= g.W)) {
 #pragma unroll
       for (int r = 0; r < T; ++r)
 #pragma unroll
-        for (int s = 0; s < T; ++s) w[r][s] = pl[r * S.wreg + s];
-      if (h == 0) forward_transform<T>(w, ua);
-      else forward_transform<T>(w, ub);
+        for (int s = 0; s < T; ++s) w[r][s] = make_float2(pa[r * S.wreg + s], pb[r * S.wreg + s]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < T; ++r)
+#pragma unroll
+        for (int s = 0; s < T; ++s) {
+          const bool in = x0 + s >= 0 && x0 + s < g.W;
+          w[r][s] = in ? make_float2(pa[r * S.wreg + s], pb[r * S.wreg + s]) : make_float2(0.0f, 0.0f);
+        }
     }
+    forward_transform2<T>(w, u2);          // channels 2q, 2q+1 (packed f32x2)
   } else {
 #pragma unroll
     for (int r = 0; r < T; ++r)
 #pragma unroll
-      for (int s = 0; s < T; ++s) ua[r][s] = ub[r][s] = 0.0f;
+      for (int s = 0; s < T; ++s) u2[r][s] = make_float2(0.0f, 0.0f);
   }
   const size_t slab = static_cast<size_t>(kBlockTiles) * g.Cpad * 2;
   const uint32_t off = slab_off(tl, c0, kBlockTiles, g.Cpad);
@@ -106,7 +153,7 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
 #pragma unroll
     for (int s = 0; s < T; ++s) {
       uint32_t hi, lo;
-      split_bf16x2(ua[r][s], ub[r][s], hi, lo);
+      split_bf16x2(u2[r][s], hi, lo);
       uint8_t* p = dst + (r * T + s) * pstride;
       *reinterpret_cast<uint32_t*>(p) = hi;
       *reinterpret_cast<uint32_t*>(p + slab) = lo;
@@ -115,7 +162,8 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
 
 static FwdStage stage_geometry(const Geo& g) {
   FwdStage S;
-  S.wreg = (g.tiles_x - 1) * g.m + g.T;
+  S.bulk = (g.W % 4 == 0) ? 1 : 0;
+  S.wreg = S.bulk ? g.W : (g.tiles_x - 1) * g.m + g.T;
   S.trows = ceil_div(kBlockTiles - 1, g.tiles_x) + 1;
   if (S.trows > g.B * g.tiles_y) S.trows = g.B * g.tiles_y;
   S.plane = round_up(S.trows * g.T * S.wreg, 32) + 4;
