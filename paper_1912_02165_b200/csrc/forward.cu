@@ -84,10 +84,16 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
     if (tid == 0) mbar_arrive(&stage_bar);
     mbar_wait(&stage_bar, 0);
   } else {
-  // ---- stage the input rows of this block's tile rows, zero padded; one
-  // warp per staged row, lanes along the row (coalesced 128-byte loads)
+  // ---- stage the input rows of this block's tile rows, zero padded.
+  // (1) one descriptor per staged row -- global row offset (or -1 for a
+  // zero row) and smem offset -- so the index divisions happen once per row;
+  // (2) one warp per staged row, lanes along the row, ROWS rows per
+  // iteration so every thread has ROWS independent loads in flight.
+  constexpr int ROWS = 8;
   const int total_rows = CPC * nrows * T;
-  for (int row = warp; row < total_rows; row += blockDim.x / 32) {
+  long long* rsrc = reinterpret_cast<long long*>(xs + CPC * S.plane);
+  int* rdst = reinterpret_cast<int*>(rsrc + total_rows);
+  for (int row = tid; row < total_rows; row += blockDim.x) {
     const int r = row % T;
     const int j = (row / T) % nrows;
     const int cl = row / (T * nrows);
@@ -96,11 +102,28 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
     const int yy = ty * g.m - g.pad_lo + r;
     const int c = cbase + cl;
     const bool rok = c < g.C && yy >= 0 && yy < g.H && b < g.B;
-    const float* src = x + ((static_cast<size_t>(b) * g.C + c) * g.H + yy) * g.W - g.pad_lo;
-    float* dst = xs + cl * S.plane + j * row_elems + r * S.wreg;
-    for (int s = lane; s < S.wreg; s += 32) {
+    rsrc[row] = rok ? ((static_cast<long long>(b) * g.C + c) * g.H + yy) * g.W : -1;
+    rdst[row] = cl * S.plane + j * row_elems + r * S.wreg;
+  }
+  __syncthreads();
+  const int nw = blockDim.x / 32;
+  for (int row0 = warp * ROWS; row0 < total_rows; row0 += nw * ROWS) {
+    for (int s0 = 0; s0 < S.wreg; s0 += 32) {
+      const int s = s0 + lane;
       const int xx = s - g.pad_lo;
-      dst[s] = (rok && xx >= 0 && xx < g.W) ? __ldg(src + s) : 0.0f;
+      const bool col_ok = s < S.wreg && xx >= 0 && xx < g.W;
+      float v[ROWS];
+#pragma unroll
+      for (int k = 0; k < ROWS; ++k) {
+        const int row = row0 + k;
+        const long long src = row < total_rows ? rsrc[row] : -1;
+        v[k] = (src >= 0 && col_ok) ? __ldg(x + src + xx) : 0.0f;
+      }
+#pragma unroll
+      for (int k = 0; k < ROWS; ++k) {
+        const int row = row0 + k;
+        if (row < total_rows && s < S.wreg) xs[rdst[row] + s] = v[k];
+      }
     }
   }
   __syncthreads();
@@ -177,11 +200,13 @@ int forward_staged_cpc(const Geo& g) {
   // transforms of a thread fit; larger tiles use 256-thread CTAs.
   // 4 channels per CTA first: 256-thread CTAs, two per SM, finer work items
   // (better wave balance than 512-thread CTAs).
+  const size_t desc = S.bulk ? 0 : static_cast<size_t>(S.trows) * g.T * 12;   // per channel
   for (int cpc : {4, 8, 2})
-    if ((cpc < 8 || g.T <= 6) && static_cast<size_t>(cpc) * S.plane * 4 <= 100 * 1024 && g.Cpad % cpc == 0)
+    if ((cpc < 8 || g.T <= 6) && static_cast<size_t>(cpc) * (S.plane * 4 + desc) <= 100 * 1024 &&
+        g.Cpad % cpc == 0)
       return cpc;
   for (int cpc : {2})
-    if (static_cast<size_t>(cpc) * S.plane * 4 <= 200 * 1024) return cpc;
+    if (static_cast<size_t>(cpc) * (S.plane * 4 + desc) <= 200 * 1024) return cpc;
   return 0;
 }
 
@@ -189,7 +214,8 @@ template <int T, int CPC>
 static cudaError_t launch_staged(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk,
                                  cudaStream_t st) {
   const FwdStage S = stage_geometry(g);
-  const int smem = CPC * S.plane * 4;
+  // staging planes + (non-bulk path) one 12-byte descriptor per staged row
+  const int smem = CPC * S.plane * 4 + (S.bulk ? 0 : CPC * S.trows * g.T * 12);
   auto kern = forward_staged_kernel<T, CPC>;
   static bool attr = false;
   if (!attr) {

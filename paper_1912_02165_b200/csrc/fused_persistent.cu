@@ -682,7 +682,16 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   return pl;
 }
 
-bool persistent_fits(const Geo& g) { return persist_plan(g).ok; }
+// Small layers (a few 128-tile blocks) have no stage overlap to exploit and
+// pay the persistent pipeline's fill and drain: they run as a single L2 wave
+// (three back-to-back kernels on L2-resident intermediates) instead.
+// (WF_PERSIST_MIN_BLOCKS overrides the threshold; tests use it to run the
+// persistent kernel on small layers.)
+static int persist_min_blocks() {
+  const char* env = getenv("WF_PERSIST_MIN_BLOCKS");
+  return env ? atoi(env) : 16;
+}
+bool persistent_fits(const Geo& g) { return g.n_blk >= persist_min_blocks() && persist_plan(g).ok; }
 
 size_t persistent_scratch_bytes(const Geo& g) {
   const PersistPlan pl = persist_plan(g);

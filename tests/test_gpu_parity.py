@@ -256,3 +256,21 @@ def test_fused_task_order_and_instrumented_accounting(golden_cases):
     assert sorted(tk for tk, _ in st.task_trace) == list(range(n_task))
     with pytest.raises(wf.InvalidParameterError):
         wf.conv_fused(wf.Tensor4D(c["x"]), pack, spec, cfg, task_order=[0] * n_task)
+
+
+@pytest.mark.parametrize("t", [4, 5, 6, 7, 8])
+def test_persistent_kernel_forced_on_small_layers(t, monkeypatch):
+    """Small layers normally run as one L2 wave; force the persistent
+    dataflow kernel (WF_PERSIST_MIN_BLOCKS=1) and check it on ragged shapes:
+    bitwise equal to three-stage, within tolerance of FP64."""
+    monkeypatch.setenv("WF_PERSIST_MIN_BLOCKS", "1")
+    for dims in [(2, 20, 24, 13, 11, 3, 1, 0), (3, 64, 64, 30, 28, 3, 1, 1), (1, 130, 40, 17, 20, 3, 0, 1)]:
+        spec = wf.LayerSpec(*dims)
+        rng = np.random.default_rng(t)
+        x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+        w = _he(rng, spec)
+        pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
+        f, _ = _run("fused", x, pack, spec, t)
+        s, _ = _run("three_stage", x, pack, spec, t)
+        assert np.array_equal(f, s), (t, dims)
+        assert O.max_rel_error(f, O.direct_conv_f64(x, w, spec)) <= TOL[t], (t, dims)
