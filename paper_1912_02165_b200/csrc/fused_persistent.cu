@@ -668,8 +668,11 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   if (slots < 4) return pl;
   if (2 * (lag + window) > slots) lag = slots / 2 - window;
   if (lag < 1) lag = 1;
+  int lag2 = lag;                          // inverse items trail the GEMM items by lag2 steps
+  if (const char* env = getenv("WF_LAG2")) lag2 = atoi(env);
+  if (lag2 < 1) lag2 = 1;
   pl.L1 = lag;
-  pl.L2 = 2 * lag;
+  pl.L2 = lag + lag2;
   pl.NU = slots / 2;
   pl.NM = slots - pl.NU;
   if (pl.NU < pl.L1 + 1) pl.NU = pl.L1 + 1;

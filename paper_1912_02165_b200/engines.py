@@ -480,3 +480,72 @@ class LayerStack:
     @property
     def direct_flops(self) -> int:
         return sum(p.spec.direct_flops() for p in self.plans)
+
+
+class HostPipeline:
+    """One layer over host (pinned) buffers, batch-chunked so the PCIe copies
+    overlap the compute.
+
+    ``HostPipeline(spec, pack, config, chunks=8)(x_host, y_host)`` splits the
+    batch into ``chunks`` contiguous slices (images are independent: the tile
+    order is batch-major, reference tiling.py:8-11) and runs, per slice, the
+    host->device copy on one stream, the layer on a second and the
+    device->host copy on a third, chained by events -- so slice i+1 is
+    uploading while slice i computes and slice i-1 downloads.  The result
+    is bitwise the one of a single call on the whole batch (every engine
+    path shares the same arithmetic).  Returns after the last download.
+    """
+
+    def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None, chunks: int = 8):
+        cfg = config or EngineConfig(kind="fused")
+        if chunks < 1:
+            raise InvalidParameterError("chunks must be >= 1")
+        self.spec, self.cfg = spec, cfg
+        chunks = min(chunks, spec.batch)
+        base, extra = divmod(spec.batch, chunks)
+        self.bounds = []
+        b0 = 0
+        for i in range(chunks):
+            nb = base + (1 if i < extra else 0)
+            self.bounds.append((b0, b0 + nb))
+            b0 += nb
+        torch = _dev.torch
+        self.dev = _dev.require_cuda(cfg.device)
+        self.plans = {}
+        shared = None
+        for nb in sorted({hi - lo for lo, hi in self.bounds}, reverse=True):
+            sub = LayerSpec(nb, spec.in_channels, spec.out_channels, spec.height, spec.width, spec.kernel,
+                            spec.pad_lo, spec.pad_hi)
+            plan = LayerPlan(sub, pack, cfg, scratch=shared)
+            shared = plan.scratch if shared is None or plan.scratch.numel() > shared.numel() else shared
+            self.plans[nb] = plan
+        for plan in self.plans.values():
+            plan.scratch = shared
+        self.x_dev = torch.empty(spec.input_dims(), dtype=torch.float32, device=self.dev)
+        self.y_dev = torch.empty(spec.output_dims(), dtype=torch.float32, device=self.dev)
+        self.streams = [torch.cuda.Stream(self.dev) for _ in range(3)]
+        n = len(self.bounds)
+        self.ev_in = [torch.cuda.Event() for _ in range(n)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(n)]
+
+    def __call__(self, x_host, y_host):
+        """x_host (B, C, H, W) and y_host (B, C', H', W'): CPU f32 tensors, ideally pinned."""
+        torch = _dev.torch
+        s_in, s_comp, s_out = self.streams
+        cur = torch.cuda.current_stream(self.dev)
+        for s in self.streams:
+            s.wait_stream(cur)
+        for i, (lo, hi) in enumerate(self.bounds):
+            with torch.cuda.stream(s_in):
+                self.x_dev[lo:hi].copy_(x_host[lo:hi], non_blocking=True)
+                self.ev_in[i].record(s_in)
+            with torch.cuda.stream(s_comp):
+                s_comp.wait_event(self.ev_in[i])
+                self.plans[hi - lo](self.x_dev[lo:hi], out=self.y_dev[lo:hi])
+                self.ev_comp[i].record(s_comp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(self.ev_comp[i])
+                y_host[lo:hi].copy_(self.y_dev[lo:hi], non_blocking=True)
+        cur.wait_stream(s_out)
+        s_out.synchronize()
+        return y_host

@@ -118,3 +118,20 @@ def test_b200_planner_levels():
     fft = roofline.plan_b200(wf.LayerSpec(128, 64, 64, 56, 56, 3, 1, 1), 16, mach, transform="fft")
     assert fft.n_tile == 2048 and "waves" in fft.fused_variant
     assert "predicted winner" in c2.format()
+
+
+@pytest.mark.gpu
+def test_host_pipeline_matches_single_call(cuda_dev):
+    import torch
+    spec = wf.LayerSpec(10, 32, 48, 28, 28, 3, 1, 1)
+    w = wf.new_tensor(spec.kernel_dims(), seed=2)
+    pack = wf.transform_kernels(w, wf.make_basis(6))
+    x = wf.new_tensor(spec.input_dims(), seed=1)
+    cfg = wf.EngineConfig(kind="fused", tile=6, device=cuda_dev)
+    ref = wf.LayerPlan(spec, pack, cfg)(torch.from_numpy(x.data).to(cuda_dev)).cpu().numpy()
+    x_host = torch.from_numpy(x.data).pin_memory()
+    y_host = torch.empty(spec.output_dims(), dtype=torch.float32).pin_memory()
+    for chunks in (1, 3, 4):
+        y_host.zero_()
+        wf.HostPipeline(spec, pack, cfg, chunks=chunks)(x_host, y_host)
+        assert np.array_equal(y_host.numpy(), ref), chunks
