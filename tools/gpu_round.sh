@@ -1,8 +1,9 @@
-# full measurement pass: GPU tests, bench (ours + reference arm), ncu launch list + full capture
+# full measurement pass: GPU tests, bench (ours + reference arm), all configs, ncu launch list + full capture
 set -x
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log
+timeout 1200 python tools/bench_all.py --reps 10 > gpurun_out/all_configs.md 2> gpurun_out/all_configs.err; echo all $?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu1 $?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_persistent -s 3 -c 1 -o gpurun_out/persist_full -f python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo ncu2 $?
