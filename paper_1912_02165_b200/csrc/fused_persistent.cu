@@ -52,9 +52,17 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Poll with relaxed loads (an acquire load also invalidates the SM's L1 on
+// every iteration), then one acquire load once the target is reached.
 __device__ __forceinline__ void spin_until(const int* p, int target) {
   if (ld_acquire(p) >= target) return;
-  while (ld_acquire(p) < target) __nanosleep(64);
+  while (ld_relaxed_gpu(p) < target) __nanosleep(128);
+  (void)ld_acquire(p);
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
