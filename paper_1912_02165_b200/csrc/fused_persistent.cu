@@ -41,6 +41,7 @@ struct PersistParams {
   int NU, NM, L1, L2;
   int passes;
   int n_steps, n_items;
+  int discard;                 // drop consumed ring lines from L2 (WF_DISCARD=0 disables)
   int wreg, trows, plane; // F staging geometry
   int f_desc_off, f_max_rows;  // F row-descriptor table (bytes into smem, capacity)
   int stages;                  // G smem pipeline depth
@@ -63,6 +64,10 @@ __device__ __forceinline__ void spin_until(const int* p, int target) {
   if (ld_acquire(p) >= target) return;
   while (ld_relaxed_gpu(p) < target) __nanosleep(128);
   (void)ld_acquire(p);
+}
+// Invalidate one 128-byte L2 line without writing it back (its data is dead).
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -568,6 +573,30 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
       run_inverse_item<T, NT, KC>(P, b, sub);
     }
     __syncthreads();                                       // item done: smem free, next item decoded
+    if (P.discard) {
+      // Ring data this item consumed is dead (each region has exactly one
+      // reader): drop its L2 lines without write-back, so dead U / M never
+      // costs DRAM write bandwidth and live ring data keeps the L2.
+      if (kind == 1) {
+        const int np = min(P.gp, P.g.T * P.g.T - sub * P.gp);
+        const size_t a2 = 2ull * kBlockTiles * P.g.Cpad * 2;           // hi + lo slab of one position
+        const uint8_t* base = P.uring + (static_cast<size_t>(b % P.NU) * P.g.T * P.g.T + sub * P.gp) * a2;
+        const int lines = static_cast<int>(np * a2 / 128);
+        for (int i = tid; i < lines; i += NT) discard_l2(base + static_cast<size_t>(i) * 128);
+      } else if (kind == 2) {
+        const int cpo2 = KC ? KC : round_up(P.g.Cp, 2);
+        const int pair0 = sub * P.igc / 2;
+        const int npair = (min(P.g.Cp, (sub + 1) * P.igc) - sub * P.igc + 1) / 2;
+        const size_t pstride = static_cast<size_t>(cpo2 / 2) * kBlockTiles * 8;    // bytes per position
+        const uint8_t* base = reinterpret_cast<const uint8_t*>(P.mring) +
+                              static_cast<size_t>(b % P.NM) * P.g.T * P.g.T * cpo2 * kBlockTiles * 4 +
+                              static_cast<size_t>(pair0) * kBlockTiles * 8;
+        const int per_pos = npair * kBlockTiles * 8 / 128;               // lines per position
+        const int lines = P.g.T * P.g.T * per_pos;
+        for (int i = tid; i < lines; i += NT)
+          discard_l2(base + static_cast<size_t>(i / per_pos) * pstride + static_cast<size_t>(i % per_pos) * 128);
+      }
+    }
     {
       // Completion is published by a thread whose warp has slack at the start
       // of the next item (warp 3 is idle in G items; warp 7 waits for the
@@ -665,12 +694,12 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   // measured on B200 (c2, tools/lag_sweep.py): rings below ~64 MB starve the
   // pipeline and larger rings with longer lags keep helping, beyond the
   // 126 MB L2 (the spilled part of the rings costs little HBM time here):
-  // 100 MB / lag 8: 178 us, 124 / 12: 150 us, 160 / 16: 150 us, 220 / 24: 139 us
-  size_t budget = 220ull << 20;
+  // 100 MB / lag 8: 178 us, 124 / 12: 150 us, 220 / 24: 121 us, 300 / 32: 117 us
+  size_t budget = 300ull << 20;
   if (const char* env = getenv("WF_L2_BUDGET_MB")) budget = static_cast<size_t>(atoi(env)) << 20;
   const int items_per_block = pl.n_cg + pl.n_gg + pl.n_ig;
   const int window = ceil_div(148 * pl.cps, items_per_block) + 1;
-  int lag = 24;
+  int lag = 32;
   if (const char* env = getenv("WF_LAG")) lag = atoi(env);
   const int slots = static_cast<int>(budget / (pl.u_slot + pl.m_slot));
   if (slots < 4) return pl;
@@ -740,6 +769,8 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   P.passes = passes;
   P.n_steps = g.n_blk + pl.L2;
   P.n_items = g.n_blk * (pl.n_cg + pl.n_gg + pl.n_ig);
+  P.discard = 0;   // measured neutral-to-slower on c2 (DRAM is not the limiter); kept as an option
+  if (const char* env = getenv("WF_DISCARD")) P.discard = atoi(env);
   P.wreg = pl.wreg; P.trows = pl.trows; P.plane = pl.plane;
   P.f_desc_off = pl.f_desc_off; P.f_max_rows = pl.f_max_rows;
   P.f_bulk = pl.f_bulk; P.f_shift = pl.f_shift;
