@@ -274,3 +274,26 @@ def test_persistent_kernel_forced_on_small_layers(t, monkeypatch):
         s, _ = _run("three_stage", x, pack, spec, t)
         assert np.array_equal(f, s), (t, dims)
         assert O.max_rel_error(f, O.direct_conv_f64(x, w, spec)) <= TOL[t], (t, dims)
+
+
+def test_randomized_sweep_like_reference_acceptance():
+    """50 random layer specs (the reference's acceptance sweep shape,
+    tests/test_acceptance.py:88-127, seed 20240814): fused within tolerance
+    of FP64 direct and bitwise equal to three-stage, for T in {4, 6, 7, 8}."""
+    rng = np.random.default_rng(20240814)
+    worst = 0.0
+    for i in range(50):
+        t = int(rng.choice((4, 6, 7, 8)))
+        spec = wf.LayerSpec(int(rng.integers(1, 3)), int(rng.integers(1, 17)), int(rng.integers(1, 17)),
+                            int(rng.integers(5, 33)), int(rng.integers(5, 33)), 3,
+                            int(rng.integers(0, 2)), int(rng.integers(0, 2)))
+        x = wf.new_tensor(spec.input_dims(), seed=20240814 + 7 * i)
+        w = wf.new_tensor(spec.kernel_dims(), seed=20240814 + 7 * i + 1)
+        pack = wf.transform_kernels(w, wf.make_basis(t))
+        f, _ = _run("fused", x.data, pack, spec, t)
+        s, _ = _run("three_stage", x.data, pack, spec, t)
+        assert np.array_equal(f, s), (i, t, spec)
+        err = O.max_rel_error(f, O.direct_conv_f64(x.data, w.data, spec))
+        worst = max(worst, err)
+        assert err <= TOL[t], (i, t, spec, err)
+    assert worst > 0.0
