@@ -42,6 +42,7 @@ struct PersistParams {
   int passes;
   int n_steps, n_items;
   int discard;                 // drop consumed ring lines from L2 (WF_DISCARD=0 disables)
+  int split_f;                 // >0: CTAs [0, split_f) run only F items, the rest G and I items
   int wreg, trows, plane; // F staging geometry
   int f_desc_off, f_max_rows;  // F row-descriptor table (bytes into smem, capacity)
   int stages;                  // G smem pipeline depth
@@ -512,9 +513,34 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
   int step = 0, step_base = 0, nf = 0, ng = 0;
   int next_item = 0;
   int step_items = 0;
+  // role split (P.split_f > 0): forward-only CTAs take F items from their
+  // own queue in block order; the others take G and I items (step s: G of
+  // block s, then I of block s - (L2 - L1)) from a second queue
+  const bool split = P.split_f > 0;
+  const bool role_f = split && static_cast<int>(blockIdx.x) < P.split_f;
+  if (split && !role_f) head = P.counters + 1 + 3 * nb;
   auto decode = [&](int* dst) {
     const int item = next_item;
     next_item = atomicAdd(head, 1);
+    if (split) {
+      if (role_f) {
+        if (item >= nb * P.n_cg) { dst[0] = -1; return; }
+        dst[0] = 0; dst[1] = item / P.n_cg; dst[2] = item - dst[1] * P.n_cg;
+        return;
+      }
+      if (item >= nb * (P.n_gg + P.n_ig)) { dst[0] = -1; return; }
+      const int lag2 = P.L2 - P.L1;
+      while (item >= step_base + step_items) {
+        step_base += step_items;
+        ++step;
+        step_items = (step < nb ? P.n_gg : 0) + (step >= lag2 && step - lag2 < nb ? P.n_ig : 0);
+      }
+      const int k = item - step_base;
+      const int ngs = step < nb ? P.n_gg : 0;
+      if (k < ngs) { dst[0] = 1; dst[1] = step; dst[2] = k; }
+      else { dst[0] = 2; dst[1] = step - lag2; dst[2] = k - ngs; }
+      return;
+    }
     if (item >= P.n_items) {
       dst[0] = -1;
       return;
@@ -531,7 +557,8 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
   };
   if (tid == kDecodeTid) {
     next_item = atomicAdd(head, 1);
-    step_items = items_in_step(P, 0, nf, ng);
+    if (split) step_items = (0 < nb ? P.n_gg : 0) + (0 >= P.L2 - P.L1 ? P.n_ig : 0);
+    else step_items = items_in_step(P, 0, nf, ng);
     decode(item_s[0]);
   }
   __syncthreads();
@@ -717,7 +744,7 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   if (pl.NU > g.n_blk) pl.NU = g.n_blk;
   if (pl.NM > g.n_blk) pl.NM = g.n_blk;
   if (pl.NU <= pl.L1 && pl.NU < g.n_blk) return pl;
-  pl.counters_bytes = static_cast<size_t>(1 + 3 * g.n_blk) * sizeof(int);
+  pl.counters_bytes = static_cast<size_t>(2 + 3 * g.n_blk) * sizeof(int);
   pl.ok = true;
   return pl;
 }
@@ -769,6 +796,8 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   P.passes = passes;
   P.n_steps = g.n_blk + pl.L2;
   P.n_items = g.n_blk * (pl.n_cg + pl.n_gg + pl.n_ig);
+  P.split_f = 0;
+  if (const char* env = getenv("WF_SPLIT")) P.split_f = atoi(env) * sm_count * pl.cps / 100;
   P.discard = 0;   // measured neutral-to-slower on c2 (DRAM is not the limiter); kept as an option
   if (const char* env = getenv("WF_DISCARD")) P.discard = atoi(env);
   P.wreg = pl.wreg; P.trows = pl.trows; P.plane = pl.plane;
