@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--engine", default="fused", choices=["fused", "three_stage"])
     ap.add_argument("--precision", default="3xbf16", choices=["3xbf16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=8, help="batch slices of the host-buffer pipeline")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="batch slices of the host-buffer pipeline")
     return ap.parse_args()
 
 

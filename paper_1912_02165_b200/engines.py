@@ -496,8 +496,12 @@ class HostPipeline:
     path shares the same arithmetic).  Returns after the last download.
     """
 
-    def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None, chunks: int = 8):
+    def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None, chunks: int = 8,
+                 graph: bool = True):
         cfg = config or EngineConfig(kind="fused")
+        self.use_graph = graph
+        self._graph = None
+        self._graph_key = None
         if chunks < 1:
             raise InvalidParameterError("chunks must be >= 1")
         self.spec, self.cfg = spec, cfg
@@ -529,7 +533,31 @@ class HostPipeline:
         self.ev_comp = [torch.cuda.Event() for _ in range(n)]
 
     def __call__(self, x_host, y_host):
-        """x_host (B, C, H, W) and y_host (B, C', H', W'): CPU f32 tensors, ideally pinned."""
+        """x_host (B, C, H, W) and y_host (B, C', H', W'): CPU f32 tensors, ideally pinned.
+
+        With ``graph=True`` (default) the whole chunked pipeline -- copies,
+        kernels and the cross-stream events -- is captured once per
+        (x_host, y_host) pair into a CUDA graph and replayed, so the host
+        issues one launch per call instead of ~10 per slice.
+        """
+        torch = _dev.torch
+        key = (x_host.data_ptr(), y_host.data_ptr())
+        if self.use_graph and x_host.is_pinned() and y_host.is_pinned():
+            if self._graph is None or self._graph_key != key:
+                self._issue(x_host, y_host)                    # warm: attributes, first-launch setup
+                torch.cuda.synchronize(self.dev)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._issue(x_host, y_host)
+                self._graph, self._graph_key = g, key
+            self._graph.replay()
+            torch.cuda.current_stream(self.dev).synchronize()
+            return y_host
+        self._issue(x_host, y_host)
+        self.streams[2].synchronize()
+        return y_host
+
+    def _issue(self, x_host, y_host):
         torch = _dev.torch
         s_in, s_comp, s_out = self.streams
         cur = torch.cuda.current_stream(self.dev)
@@ -547,5 +575,3 @@ class HostPipeline:
                 s_out.wait_event(self.ev_comp[i])
                 y_host[lo:hi].copy_(self.y_dev[lo:hi], non_blocking=True)
         cur.wait_stream(s_out)
-        s_out.synchronize()
-        return y_host
