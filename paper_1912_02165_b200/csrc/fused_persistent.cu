@@ -43,6 +43,7 @@ struct PersistParams {
   int n_steps, n_items;
   int discard;                 // drop consumed ring lines from L2 (WF_DISCARD=0 disables)
   int split_f;                 // >0: CTAs [0, split_f) run only F items, the rest G and I items
+  int only;                    // tuning aid: 1/2/3 = execute only F / G / I items (results invalid)
   int wreg, trows, plane; // F staging geometry
   int f_desc_off, f_max_rows;  // F row-descriptor table (bytes into smem, capacity)
   int stages;                  // G smem pipeline depth
@@ -165,8 +166,15 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
         if (r < z0 || r >= z1)
           for (int s2 = 0; s2 < g.W; ++s2) dst[r * g.W + s2] = 0.0f;
     }
-    __syncthreads();
-    if (tid == 0) mbar_arrive(&sy.fbar);
+    // only the warps that issued copies synchronise before the single
+    // arrival (the others go straight to the mbarrier wait), so a warp that
+    // is still publishing the previous item's completion delays nobody
+    const int nw_issue = min(NT / 32, (units + 31) / 32);
+    if (warp < nw_issue) {
+      if (nw_issue > 1) asm volatile("bar.sync 1, %0;" ::"r"(nw_issue * 32) : "memory");
+      if (tid == 0) mbar_arrive(&sy.fbar);
+    }
+    if (units == 0 && tid == 0) mbar_arrive(&sy.fbar);
     mbar_wait(&sy.fbar, fparity);
   } else {
   // stage input rows (zero padded): one warp per row, lanes along the row
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ GemmSync sy;
   __shared__ uint32_t tmem_slot;
-  __shared__ int item_s[2][3];       // double-buffered: kind, block, sub-index (or -1: done)
+  __shared__ int item_s[2][4];       // double-buffered: kind, block, sub-index (or -1: done), deps ready
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nb = P.g.n_blk;
   int* head = P.counters;
@@ -522,6 +530,7 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
   auto decode = [&](int* dst) {
     const int item = next_item;
     next_item = atomicAdd(head, 1);
+    dst[3] = 0;
     if (split) {
       if (role_f) {
         if (item >= nb * P.n_cg) { dst[0] = -1; return; }
@@ -566,13 +575,27 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
     const int* cur = item_s[it & 1];
     const int kind = cur[0], b = cur[1], sub = cur[2];
     if (kind < 0) break;
-    if (tid == kDecodeTid) decode(item_s[(it + 1) & 1]);
+    if (tid == kDecodeTid) {
+      // decode the next item and check its dependencies now, one item
+      // ahead: when they are already complete its warps skip the polling
+      int* nx = item_s[(it + 1) & 1];
+      decode(nx);
+      const int nk = nx[0], nbk = nx[1];
+      bool ready = false;
+      if (nk == 0) ready = nbk < P.NU || ld_acquire(doneG + (nbk - P.NU)) >= P.n_gg;
+      else if (nk == 1) ready = ld_acquire(doneF + nbk) >= P.n_cg &&
+                                (nbk < P.NM || ld_acquire(doneI + (nbk - P.NM)) >= P.n_ig);
+      else if (nk == 2) ready = ld_acquire(doneG + nbk) >= P.n_gg;
+      nx[3] = ready ? 1 : 0;
+    }
     long long t_a = 0, t_b = 0;
     unsigned long long g_a = 0;
     if (g_prof_on && tid == 0) { t_a = clock64(); g_a = gtimer(); }
     // Dependency wait, per warp (lane 0 acquires, __syncwarp orders the
     // lanes after it): no CTA barrier at the start of an item.
-    if ((tid & 31) == 0) {
+    if (cur[3]) {
+      if (kind == 1 && tid == 0) fence_proxy_async_global();          // U read by bulk copies
+    } else if ((tid & 31) == 0) {
       if (kind == 0) {
         if (b >= P.NU) spin_until(doneG + (b - P.NU), P.n_gg);          // U slot free
       } else if (kind == 1) {
@@ -585,7 +608,9 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
     }
     __syncwarp();
     if (g_prof_on && tid == 0) t_b = clock64();
-    if (kind == 0) {                                       // ---- F(b, sub)
+    if (P.only && P.only != kind + 1) {
+      // tuning aid (WF_ONLY=1/2/3): items of the other kinds are skipped
+    } else if (kind == 0) {                                // ---- F(b, sub)
       run_forward_item<T, NT, KC>(P, b, sub, smem, sy, fcount & 1);
       ++fcount;
     } else if (kind == 1) {                                // ---- G(b, sub)
@@ -796,6 +821,8 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   P.passes = passes;
   P.n_steps = g.n_blk + pl.L2;
   P.n_items = g.n_blk * (pl.n_cg + pl.n_gg + pl.n_ig);
+  P.only = 0;
+  if (const char* env = getenv("WF_ONLY")) P.only = atoi(env);
   P.split_f = 0;
   if (const char* env = getenv("WF_SPLIT")) P.split_f = atoi(env) * sm_count * pl.cps / 100;
   P.discard = 0;   // measured neutral-to-slower on c2 (DRAM is not the limiter); kept as an option
