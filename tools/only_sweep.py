@@ -10,7 +10,7 @@ dev = torch.device("cuda", 0)
 pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
 xd = torch.from_numpy(x).to(dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-for only in ("4", "1", "2", "3"):
+for only in ("4", "6", "5", "1"):
     os.environ["WF_ONLY"] = only
     plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=t, device=dev))
     ts = []
@@ -19,5 +19,5 @@ for only in ("4", "1", "2", "3"):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); plan(xd); b.record(); b.synchronize()
         if i >= 2: ts.append(a.elapsed_time(b) * 1e3)
-    print(f"only={only} ({["all", "F", "G", "I", "none"][int(only)]}): median {np.median(ts):7.1f} us", flush=True)
+    print(f"only={only} ({["all", "F", "G", "I", "none", "F-nostore", "F-staging-only"][int(only)]}): median {np.median(ts):7.1f} us", flush=True)
 os.environ.pop("WF_ONLY")
