@@ -10,7 +10,7 @@ dev = torch.device("cuda", 0)
 pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
 xd = torch.from_numpy(x).to(dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-for only in ("4", "6", "5", "1"):
+for only in ("4", "1", "2", "3"):
     os.environ["WF_ONLY"] = only
     plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=t, device=dev))
     ts = []
