@@ -114,8 +114,9 @@ struct GemmSync {
 };
 
 // ------------------------------------------------------------------ F item
+// Returns whether the staging mbarrier was used (one phase consumed).
 template <int T, int NT, int KC>
-__device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t* smem, GemmSync& sy,
+__device__ bool run_forward_item(const PersistParams& P, int b, int cg, uint8_t* smem, GemmSync& sy,
                                  int fparity) {
   const Geo& g = P.g;
   float* xs = reinterpret_cast<float*>(smem);
@@ -133,6 +134,24 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
   const int nrows = tlast >= t0 ? tlast / g.tiles_x - gr0 + 1 : 0;
   const int row_elems = T * P.wreg;
   const int total_rows = CPC * nrows * T;
+  if (cbase >= g.C) {
+    // a channel group made only of K padding (C < Cpad): its U entries are
+    // zeros -- no staging, no transform
+    const int pairs = CPC / 2, tpw = 32 / pairs;
+    const int tl = (warp % (P.ftiles / tpw)) * tpw + lane % tpw;
+    const int q = lane / tpw;
+    if (warp < P.ftiles / tpw) {
+      const size_t slab = static_cast<size_t>(kBlockTiles) * g.Cpad * 2;
+      uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * T * T * 2 * slab +
+                     slab_off(tb0 + tl, cbase + 2 * q, kBlockTiles, g.Cpad);
+#pragma unroll 4
+      for (int p = 0; p < T * T; ++p) {
+        *reinterpret_cast<uint32_t*>(dst + static_cast<size_t>(p) * 2 * slab) = 0u;
+        *reinterpret_cast<uint32_t*>(dst + static_cast<size_t>(p) * 2 * slab + slab) = 0u;
+      }
+    }
+    return false;
+  }
   long long tprof = 0;
   if (g_prof_on && tid == 0) tprof = clock64();
   if (P.f_bulk) {
@@ -243,7 +262,7 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
   const int tile = t0 + tl;
   const int c0 = cbase + 2 * q;
   float2 u2[T][T];
-  if (P.only == 6) return;               // tuning aid: staging only
+  if (P.only == 6) return true;          // tuning aid: staging only
   if (tile < g.n_tile && warp < nwarps_used) {
     const int per_img = g.tiles_y * g.tiles_x;
     const int bi = tile / per_img;
@@ -319,6 +338,7 @@ __device__ void run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
       }
   }
   prof_mark(10, tprof);
+  return true;
 }
 
 // ------------------------------------------------------------------ G item
@@ -639,8 +659,7 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
     if (P.only && P.only != kind + 1 && !((P.only == 5 || P.only == 6) && kind == 0)) {
       // tuning aid (WF_ONLY=1/2/3): items of the other kinds are skipped
     } else if (kind == 0) {                                // ---- F(b, sub)
-      run_forward_item<T, NT, KC>(P, b, sub, smem, sy, fcount & 1);
-      ++fcount;
+      if (run_forward_item<T, NT, KC>(P, b, sub, smem, sy, fcount & 1)) ++fcount;
     } else if (kind == 1) {                                // ---- G(b, sub)
       tc_fence_after();
       run_gemm_item<NT, KC>(P, b, sub, smem, sy, tmem, gsteps, tuse);
