@@ -762,7 +762,7 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   pl.gp = (512 / pl.cps) / g.Cppad;
   if (pl.gp > 8) pl.gp = 8;
   if (pl.gp > g.T * g.T) pl.gp = g.T * g.T;
-  pl.igc = 8;                              // c' per I item (thread = tile x c' sub-lane)
+  pl.igc = getenv("WF_IGC") ? atoi(getenv("WF_IGC")) : 8;   // c' per I item (thread = tile x c' sub-lane)
   pl.n_cg = (kBlockTiles / pl.ftiles) * (g.Cpad / pl.cpc);
   pl.n_gg = ceil_div(g.T * g.T, pl.gp);
   pl.n_ig = ceil_div(g.Cp, pl.igc);
