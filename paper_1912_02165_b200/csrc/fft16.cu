@@ -65,10 +65,26 @@ __global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __rest
       float row[16];
       if (rvalid && ch < g.C) {
         const float* src = x + ((static_cast<size_t>(b) * g.C + ch) * g.H + iy) * g.W;
+        const int sh = ox & 3;                       // window start inside its 16-byte word
+        if ((g.W & 3) == 0 && ox >= 0 && ox - sh + 20 <= g.W) {
+          // interior window of a 16-byte aligned row: five 16-byte loads
+          // cover columns [ox - sh, ox - sh + 20) (instead of 16 scalar loads)
+          float v[20];
+          const float4* s4 = reinterpret_cast<const float4*>(src + ox - sh);
 #pragma unroll
-        for (int s = 0; s < 16; ++s) {
-          const int ix = ox + s;
-          row[s] = (ix >= 0 && ix < g.W) ? __ldg(src + ix) : 0.0f;
+          for (int i = 0; i < 5; ++i) {
+            const float4 q = __ldg(s4 + i);
+            v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+          }
+#pragma unroll
+          for (int s = 0; s < 16; ++s)
+            row[s] = sh == 0 ? v[s] : sh == 1 ? v[s + 1] : sh == 2 ? v[s + 2] : v[s + 3];
+        } else {
+#pragma unroll
+          for (int s = 0; s < 16; ++s) {
+            const int ix = ox + s;
+            row[s] = (ix >= 0 && ix < g.W) ? __ldg(src + ix) : 0.0f;
+          }
         }
       } else {
 #pragma unroll
@@ -216,9 +232,15 @@ __global__ void __launch_bounds__(kInvThreads) fft_inverse_kernel(const float* _
     float out[14];
     fft::irfft16<14>(zr, zi, out);
     float* dst = y + ((static_cast<size_t>(b) * g.Cp + cp) * g.Ho + oy) * g.Wo + ox;
+    if ((g.Wo & 1) == 0 && ox + 14 <= g.Wo) {      // 8-byte aligned full row segment
 #pragma unroll
-    for (int s2 = 0; s2 < 14; ++s2)
-      if (ox + s2 < g.Wo) dst[s2] = out[s2] * (1.0f / 256.0f);
+      for (int s2 = 0; s2 < 14; s2 += 2)
+        *reinterpret_cast<float2*>(dst + s2) = make_float2(out[s2] * (1.0f / 256.0f), out[s2 + 1] * (1.0f / 256.0f));
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < 14; ++s2)
+        if (ox + s2 < g.Wo) dst[s2] = out[s2] * (1.0f / 256.0f);
+    }
   }
 }
 
