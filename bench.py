@@ -35,9 +35,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Direct-conv-equivalent TFLOP/s per layer & fraction of B200 roofline"
 CONFIGS = {
-    # name: (B per GPU, C, C', H=W, tile, weight std rule)
-    "c2": (64, 64, 64, 56, 6, "he"),
-    "c1": (1, 64, 64, 56, 4, "inv_sqrt"),
+    # name: (B per GPU, C, C', H=W, tile, weight std rule, input distribution)
+    "c2": (64, 64, 64, 56, 6, "he", "normal"),
+    "c1": (1, 64, 64, 56, 4, "inv_sqrt", "normal"),
+    # c5 (the sweep / scaling config) at its C = 64, 56x56 point: B = 256 per GPU
+    "c5": (256, 64, 64, 56, 8, "he", "uniform"),
 }
 
 
@@ -57,10 +59,13 @@ def parse():
 
 def layer_inputs(cfg_name, batch=None, seed=1234):
     import paper_1912_02165_b200 as wf
-    b, c, cp, hw, t, rule = CONFIGS[cfg_name]
+    b, c, cp, hw, t, rule, dist = CONFIGS[cfg_name]
     spec = wf.LayerSpec(batch or b, c, cp, hw, hw, 3, 1, 1)
     rng = np.random.default_rng(seed)
-    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    if dist == "uniform":
+        x = rng.uniform(-1.0, 1.0, spec.input_dims()).astype(np.float32)
+    else:
+        x = rng.standard_normal(spec.input_dims()).astype(np.float32)
     std = np.sqrt(2.0 / (9 * c)) if rule == "he" else 1.0 / np.sqrt(9 * c)
     w = (np.random.default_rng(seed + 1).standard_normal(spec.kernel_dims()) * std).astype(np.float32)
     return spec, t, x, w
@@ -231,7 +236,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic N(0,1) inputs, He-normal weights (seeded)",
+        "data": f"synthetic {'U(-1,1)' if CONFIGS[args.config][6] == 'uniform' else 'N(0,1)'} inputs, "
+                "He-normal weights (seeded)",
         "config": {"workload": f"{args.config}: F(4x4,3x3) conv, B={b_total}, C=C'={spec.in_channels}, "
                                f"{spec.height}x{spec.width}, pad 1 (CPU sample: {sample_b} image(s) per step)",
                    "tile": t, "engine": "fused (reference algorithm, R=24)"},
@@ -352,7 +358,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 io, bf16x3 split tensor-core (f32 accumulate)"
             if args.precision == "3xbf16" else "f32 io, bf16 tensor-core",
-            "data": "synthetic: seeded N(0,1) inputs, He-normal weights (no dataset in the reference)",
+            "data": f"synthetic: seeded {'U(-1,1)' if CONFIGS[args.config][6] == 'uniform' else 'N(0,1)'} "
+                    "inputs, He-normal weights (no dataset in the reference)",
             "config": {"workload": f"{args.config}: Winograd F({t - 2}x{t - 2},3x3) conv, B={b_total} "
                                    f"({spec.batch}/GPU), C=C'={spec.in_channels}, {spec.height}x{spec.width}, "
                                    f"stride 1, pad 1", "engine": args.engine, "tile": t,
