@@ -761,6 +761,7 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   if (g.Cpad % pl.cpc != 0 || g.Cppad > 128) return pl;
   pl.gp = (512 / pl.cps) / g.Cppad;
   if (pl.gp > 8) pl.gp = 8;
+  if (const char* env = getenv("WF_GP")) pl.gp = std::max(1, std::min(pl.gp, atoi(env)));
   if (pl.gp > g.T * g.T) pl.gp = g.T * g.T;
   pl.igc = getenv("WF_IGC") ? atoi(getenv("WF_IGC")) : 8;   // c' per I item (thread = tile x c' sub-lane)
   pl.n_cg = (kBlockTiles / pl.ftiles) * (g.Cpad / pl.cpc);
