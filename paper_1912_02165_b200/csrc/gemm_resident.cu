@@ -9,7 +9,8 @@
 // transformed tiles U stream in, through a 4-deep mbarrier pipeline of
 // bulk async copies; accumulators rotate through 4 TMEM buffers so the
 // epilogue of block k overlaps the MMAs of block k+1.
-//   warp 0: producer, warp 1: TMEM alloc + MMA issuer, warps 2..5: epilogue.
+//   warp 0: producer, warp 1: TMEM alloc + MMA issuer, warps 2..9: epilogue
+//   (two warps per TMEM lane quadrant, each draining half of the columns).
 #include <cuda_bf16.h>
 #include "common.cuh"
 #include "sm100.cuh"
@@ -17,7 +18,8 @@
 
 namespace wf {
 
-constexpr int kResThreads = 192;
+constexpr int kResThreads = 320;
+constexpr int kResEpiWarps = 8;
 constexpr int kResStages = 4;
 constexpr int kResAcc = 4;
 
@@ -48,7 +50,7 @@ __global__ void __launch_bounds__(kResThreads, 1) gemm_resident_kernel(ResParams
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kResStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-    for (int a = 0; a < kResAcc; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < kResAcc; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kResEpiWarps); }
     mbar_init(&vfull, 1);
     mbar_init(&vempty, 1);
     fence_mbar_init();
@@ -142,7 +144,10 @@ __global__ void __launch_bounds__(kResThreads, 1) gemm_resident_kernel(ResParams
     }
   } else {
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;               // which half of the columns
     const int row = q * 32 + lane_id();
+    const int split = (NC / 16 / 2) * 16;           // 16-column chunks, first half to half 0
+    const int c_lo = half ? split : 0, c_hi = half ? NC : split;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int it = lo_it; it < hi_it; ++it) {
@@ -152,14 +157,23 @@ __global__ void __launch_bounds__(kResThreads, 1) gemm_resident_kernel(ResParams
       const int tile = blk * kBlockTiles + row;
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * NC;
       float* mrow = P.M + static_cast<size_t>(p) * P.Cp * P.ldm + tile;
-      for (int c = 0; c < NC; c += 16) {
+      const bool live = tile < P.n_valid;
+      for (int c = c_lo; c < c_hi; c += 16) {
         float v[16];
         tmem_ld16(taddr + c, v);
         tmem_ld_wait();
-        if (tile < P.n_valid) {
+        if (live) {
+          float* dst = mrow + static_cast<size_t>(c) * P.ldm;
+          if (c + 16 <= P.Cp) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c + i < P.Cp) mrow[static_cast<size_t>(c + i) * P.ldm] = v[i];
+            for (int i = 0; i < 16; ++i) { *dst = v[i]; dst += P.ldm; }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (c + i < P.Cp) *dst = v[i];
+              dst += P.ldm;
+            }
+          }
         }
       }
       tc_fence_before();
