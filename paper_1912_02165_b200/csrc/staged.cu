@@ -76,9 +76,11 @@ __global__ void __launch_bounds__(256) forward_slab_kernel(const float* __restri
 // accumulated in TMEM, K streamed in 64-channel blocks by bulk copies.
 //   warp 0      : bulk-copy producer (A hi/lo, B hi/lo K-block per stage)
 //   warp 1      : TMEM allocator + single-thread MMA issuer
-//   warps 2..5  : epilogue, TMEM -> registers -> M (f32, [p][c'][tile])
+//   warps 2..9  : epilogue, TMEM -> registers -> M (f32, [p][c'][tile]);
+//                 two warps per TMEM lane quarter, each half of the columns
 // 3xBF16: D = Uhi*Vhi + Uhi*Vlo + Ulo*Vhi (f32 accumulate); 1 pass for bf16.
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;
+constexpr int kGemmEpiWarps = 8;
 
 struct GemmParams {
   const uint8_t* U;  // [p][blk][hl] slabs of 128 x Cpad
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmPara
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], kGemmEpiWarps);
     }
     fence_mbar_init();
   }
@@ -196,9 +198,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmPara
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    // epilogue warps 2..9 -> TMEM lane quarter (warp % 4), column half
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = q * 32 + lane_id();
+    const int split = (P.NC / 16 / 2) * 16;
+    const int c_lo = half ? split : 0, c_hi = half ? P.NC : split;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -209,15 +214,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmPara
       tc_fence_after();
       const int tile = blk * kBlockTiles + row;
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * P.NC;
-      for (int c = 0; c < P.NC; c += 16) {
+      for (int c = c_lo; c < c_hi; c += 16) {
         float v[16];
         tmem_ld16(taddr + c, v);
         tmem_ld_wait();
         if (tile < P.n_valid) {
+          const int cp0 = nc * P.NC + c;
+          float* dst = P.M + (static_cast<size_t>(p) * P.Cp + cp0) * P.ldm + tile;
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const int cp = nc * P.NC + c + i;
-            if (cp < P.Cp) P.M[(static_cast<size_t>(p) * P.Cp + cp) * P.ldm + tile] = v[i];
+            if (cp0 + i < P.Cp) *dst = v[i];
+            dst += P.ldm;
           }
         }
       }
