@@ -831,7 +831,14 @@ static int persist_min_blocks() {
   const char* env = getenv("WF_PERSIST_MIN_BLOCKS");
   return env ? atoi(env) : 16;
 }
-bool persistent_fits(const Geo& g) { return g.n_blk >= persist_min_blocks() && persist_plan(g).ok; }
+// Very narrow layers (Cpad = 16) have too little work per item for the
+// persistent pipeline unless they are large (measured on c5).
+bool persistent_fits(const Geo& g) {
+  const int min_blocks = persist_min_blocks();
+  if (g.n_blk < min_blocks) return false;
+  if (g.Cpad < 32 && g.n_blk < 4 * min_blocks) return false;
+  return persist_plan(g).ok;
+}
 
 size_t persistent_scratch_bytes(const Geo& g) {
   const PersistPlan pl = persist_plan(g);
