@@ -4,14 +4,21 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xptxas -v -diag-suppress 1886 $(EXTRA)
 SRC := $(wildcard paper_1912_02165_b200/csrc/*.cu)
 HDR := $(wildcard paper_1912_02165_b200/csrc/*.cuh) include/winofuse_b200.h
+OBJDIR := build
+OBJ := $(patsubst paper_1912_02165_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
 LIB := paper_1912_02165_b200/libwinofuse_b200.so
 
 all: $(LIB)
 
-$(LIB): $(SRC) $(HDR)
-	$(NVCC) $(NVFLAGS) -shared $(SRC) -o $@ 2> build_ptxas.log || (cat build_ptxas.log; false)
+$(OBJDIR)/%.o: paper_1912_02165_b200/csrc/%.cu $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared $(OBJ) -o $@
+	cat $(OBJDIR)/*.ptxas.log > build_ptxas.log
 
 clean:
-	rm -f $(LIB) build_ptxas.log
+	rm -rf $(LIB) build_ptxas.log $(OBJDIR)
 
 .PHONY: all clean

@@ -165,6 +165,118 @@ __device__ __forceinline__ void inverse_transform2(const float2 (&mm)[T][T], flo
     }
 }
 
+// ------------------------------------------------------------------------
+// F(4x4, 3x3) (T = 6) specialisations: the 1-D transforms factored into
+// shared sums (14 adds/FMAs instead of 22 for B^T, 10 instead of 18 for A^T)
+// with the coefficients of the reference basis (basis_tables.cuh: bt<6>,
+// at<6>).  Every path (fused, three-stage, reference-layout stage kernels)
+// uses these, scalar or packed f32x2 with per element the same operations,
+// so fused and three-stage results stay bitwise equal.
+struct ScalarOps {
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float fma(float c, float x, float acc) { return __fmaf_rn(c, x, acc); }
+};
+struct PairOps {
+  static __device__ __forceinline__ float2 add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+  // a - b == fma(b, -1, a) exactly (one rounding, like the scalar subtraction)
+  static __device__ __forceinline__ float2 sub(float2 a, float2 b) {
+    return __ffma2_rn(b, make_float2(-1.0f, -1.0f), a);
+  }
+  static __device__ __forceinline__ float2 fma(float c, float2 x, float2 acc) {
+    return __ffma2_rn(make_float2(c, c), x, acc);
+  }
+};
+// u = B^T x for one line of 6 (in place):
+//   u0 = 4x0 - 5x2 + x4        = 4(x0 - x2) + (x4 - x2)
+//   u1 = -4x1 - 4x2 + x3 + x4  = (x3 + x4) - 4(x1 + x2)
+//   u2 = 4x1 - 4x2 - x3 + x4   = (x4 - x3) + 4(x1 - x2)
+//   u3 = -2x1 - x2 + 2x3 + x4  = (x4 - x2) + 2(x3 - x1)
+//   u4 = 2x1 - x2 - 2x3 + x4   = (x4 - x2) - 2(x3 - x1)
+//   u5 = -4x1 + 5x3 - x5       = 4(x3 - x1) + (x3 - x5)
+template <class O, class V>
+__device__ __forceinline__ void bt6_line(V& x0, V& x1, V& x2, V& x3, V& x4, V& x5) {
+  const V a = O::add(x3, x4), b = O::add(x1, x2);
+  const V c = O::sub(x4, x3), d = O::sub(x1, x2);
+  const V e = O::sub(x4, x2), f = O::sub(x3, x1);
+  const V g = O::sub(x0, x2), h = O::sub(x3, x5);
+  x0 = O::fma(4.0f, g, e);
+  x1 = O::fma(-4.0f, b, a);
+  x2 = O::fma(4.0f, d, c);
+  x3 = O::fma(2.0f, f, e);
+  x4 = O::fma(-2.0f, f, e);
+  x5 = O::fma(4.0f, f, h);
+}
+// y = A^T m for one line of 6 -> 4:
+//   y0 = m0 + m1 + m2 + m3 + m4     = (m0 + p) + r
+//   y1 = m1 - m2 + 2m3 - 2m4        = q + 2s
+//   y2 = m1 + m2 + 4m3 + 4m4        = p + 4r
+//   y3 = m1 - m2 + 8m3 - 8m4 - m5   = (q - m5) + 8s
+// with p = m1 + m2, q = m1 - m2, r = m3 + m4, s = m3 - m4
+template <class O, class V>
+__device__ __forceinline__ void at6_line(V m0, V m1, V m2, V m3, V m4, V m5, V& y0, V& y1, V& y2, V& y3) {
+  const V p = O::add(m1, m2), q = O::sub(m1, m2), r = O::add(m3, m4), s = O::sub(m3, m4);
+  y0 = O::add(O::add(m0, p), r);
+  y1 = O::fma(2.0f, s, q);
+  y2 = O::fma(4.0f, r, p);
+  y3 = O::fma(8.0f, s, O::sub(q, m5));
+}
+template <class O, class V>
+__device__ __forceinline__ void forward6_inplace(V (&u)[6][6]) {
+#pragma unroll
+  for (int s = 0; s < 6; ++s) bt6_line<O>(u[0][s], u[1][s], u[2][s], u[3][s], u[4][s], u[5][s]);
+#pragma unroll
+  for (int r = 0; r < 6; ++r) bt6_line<O>(u[r][0], u[r][1], u[r][2], u[r][3], u[r][4], u[r][5]);
+}
+template <class O, class V>
+__device__ __forceinline__ void forward6(const V (&x)[6][6], V (&u)[6][6]) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int s = 0; s < 6; ++s) u[r][s] = x[r][s];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) bt6_line<O>(u[0][s], u[1][s], u[2][s], u[3][s], u[4][s], u[5][s]);
+#pragma unroll
+  for (int r = 0; r < 6; ++r) bt6_line<O>(u[r][0], u[r][1], u[r][2], u[r][3], u[r][4], u[r][5]);
+}
+// same operations as inverse6, with the column pass written over mm
+template <class O, class V>
+__device__ __forceinline__ void inverse6_inplace(V (&mm)[6][6], V (&y)[4][4]) {
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    V t0, t1, t2, t3;
+    at6_line<O>(mm[0][s], mm[1][s], mm[2][s], mm[3][s], mm[4][s], mm[5][s], t0, t1, t2, t3);
+    mm[0][s] = t0; mm[1][s] = t1; mm[2][s] = t2; mm[3][s] = t3;
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) at6_line<O>(mm[r][0], mm[r][1], mm[r][2], mm[r][3], mm[r][4], mm[r][5], y[r][0], y[r][1], y[r][2], y[r][3]);
+}
+template <class O, class V>
+__device__ __forceinline__ void inverse6(const V (&mm)[6][6], V (&y)[4][4]) {
+  V t[4][6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s)
+    at6_line<O>(mm[0][s], mm[1][s], mm[2][s], mm[3][s], mm[4][s], mm[5][s], t[0][s], t[1][s], t[2][s], t[3][s]);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) at6_line<O>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], y[r][0], y[r][1], y[r][2], y[r][3]);
+}
+template <>
+__device__ __forceinline__ void forward_transform<6>(const float (&x)[6][6], float (&u)[6][6]) {
+  forward6<ScalarOps>(x, u);
+}
+template <>
+__device__ __forceinline__ void forward_transform2<6>(const float2 (&x)[6][6], float2 (&u)[6][6]) {
+  forward6<PairOps>(x, u);
+}
+template <>
+__device__ __forceinline__ void inverse_transform<6>(const float (&mm)[6][6], float (&y)[4][4]) {
+  inverse6<ScalarOps>(mm, y);
+}
+template <>
+__device__ __forceinline__ void inverse_transform2<6>(const float2 (&mm)[6][6], float2 (&y)[4][4]) {
+  inverse6<PairOps>(mm, y);
+}
+
 // Zero-filled T x T input window for one (tile, channel) (reference
 // kernels.py:73-86: origin (ty*m - pad_lo, tx*m - pad_lo), implicit padding).
 template <int T>

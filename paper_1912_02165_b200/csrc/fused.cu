@@ -45,6 +45,7 @@ static int wave_blocks(const Geo& g) {
 }
 
 size_t fused_scratch_bytes(const Geo& g, int /*r*/) {
+  if (ws_fits(g)) return ws_scratch_bytes(g);
   if (persistent_fits(g)) return persistent_scratch_bytes(g);
   return static_cast<size_t>(kLanes) * wave_blocks(g) * block_bytes(g);
 }
@@ -71,6 +72,7 @@ static LaneResources& lane_resources() {
 
 cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
                       int passes, int /*r*/, int sm_count, cudaStream_t st) {
+  if (ws_fits(g)) return run_fused_ws(x, vpack, y, scratch, g, passes, sm_count, st);
   if (persistent_fits(g)) return run_fused_persistent(x, vpack, y, scratch, g, passes, sm_count, st);
   const int wb = wave_blocks(g);
   const size_t P = static_cast<size_t>(g.P);

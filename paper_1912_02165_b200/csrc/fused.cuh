@@ -13,6 +13,11 @@ bool persistent_fits(const Geo& g);
 size_t persistent_scratch_bytes(const Geo& g);
 cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
                                  int passes, int sm_count, cudaStream_t st);
+// Warp-specialised persistent kernel (fused_ws.cu): F(4x4,3x3), C = C' = 64.
+bool ws_fits(const Geo& g);
+size_t ws_scratch_bytes(const Geo& g);
+cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g, int passes,
+                         int sm_count, cudaStream_t st);
 cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
                       int passes, int r, int sm_count, cudaStream_t st);
 

@@ -1,0 +1,585 @@
+// fused_ws.cu -- conv_fused as ONE warp-specialised persistent kernel
+// (F(4x4,3x3), C = C' = 64: the c2 benchmark layer and the 64-channel
+// ResNet / VGG layers).
+//
+// The reference's fused engine (engines.py:317-444) keeps a task's
+// transformed tiles in the shared last-level cache between its three
+// stages.  Here every SM runs all three stages at once, each on its own
+// warps, and the transformed tiles U and the products M live in L2-resident
+// rings between them:
+//   warp 0      G producer: bulk copies of U (half-K blocks) and V into smem
+//   warp 1      G issuer: tcgen05.mma 3xBF16, f32 accumulators in TMEM
+//               (2 x 4 positions x 64 columns, double buffered)
+//   warps 4-7   G epilogue: tcgen05.ld -> M ring (f32, c' pairs interleaved)
+//   warp 2      F/I producer: bulk copies of input rows (F) or M (I) into a
+//               2-slot smem ring
+//   warps 8-15  F/I workers: forward transform + bf16 hi/lo split -> U ring
+//               (F units) or inverse transform -> output (I units)
+//   warp 3      publisher: per-unit completion (fence + atomic) to the
+//               per-block counters other SMs wait on
+// Work is assigned statically (CTA k takes every grid-th unit of each
+// queue).  Every queue walks the total order "step s: F(s), G(s - L1),
+// I(s - L2)" with L1 < NU and L2 - L1 < NM, so every dependency points to
+// an earlier step and, with all CTAs co-resident, the lowest unfinished
+// unit is always runnable: no deadlock, and no role ever waits on another
+// role of its own CTA except through its pipeline.
+#include <algorithm>
+#include <cstdlib>
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "sm100.cuh"
+#include "fused.cuh"
+
+namespace wf {
+namespace ws {
+
+constexpr int NT = 512;
+constexpr int kC = 64;                                   // C = C' = Cpad = Cppad
+constexpr int kT = 6;
+constexpr int kP = kT * kT;
+constexpr int kGP = 4;                                   // positions per G unit
+constexpr int kNGG = kP / kGP;                           // 9 G units per block
+constexpr int kCPC = 8;                                  // channels per F unit
+constexpr int kFT = 64;                                  // tiles per F unit
+constexpr int kNCG = (kBlockTiles / kFT) * (kC / kCPC);  // 16 F units per block
+constexpr int kIPairs = 2;                               // c' pairs per I unit
+constexpr int kNIG = kC / (2 * kIPairs);                 // 16 I units per block
+constexpr int kAStages = 3;
+constexpr uint32_t kAHalf = kBlockTiles * 32 * 2;        // 8 KB: hi or lo, 128 rows x 32 k
+constexpr uint32_t kAStage = 2 * kAHalf;                 // 16 KB
+constexpr uint32_t kBSlab = kC * kC * 2;                 // 8 KB: V hi or lo of one position
+constexpr uint32_t kBBuf = 2 * kBSlab;                   // 16 KB
+constexpr size_t kUPos = 4 * kAHalf;                     // 32 KB: [hl][kb] half-K blocks
+constexpr size_t kUSlot = kP * kUPos;                    // 1.18 MB
+constexpr size_t kMPos = static_cast<size_t>(kC) * kBlockTiles * 4;   // 32 KB: [pair][tile][2]
+constexpr size_t kMSlot = kP * kMPos;
+constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;    // 2 KB staged per position (I unit)
+constexpr uint32_t kFISlot = 72 * 1024;                  // F staging or I staging
+constexpr uint32_t kOffB = kAStages * kAStage;           // 48 KB
+constexpr uint32_t kOffFI = kOffB + 2 * kBBuf;           // 80 KB
+constexpr uint32_t kSmem = kOffFI + 2 * kFISlot;         // 224 KB
+
+struct Params {
+  const float* x;
+  float* y;
+  const uint8_t* vpack;   // standard MMA pack: per position hi / lo slabs of 64 x 64 (kblock, kc = 64)
+  uint8_t* uring;         // NU slots x kUSlot
+  float* mring;           // NM slots x kMSlot
+  int* counters;          // doneF, doneG, doneI (n_blk each)
+  Geo g;
+  int NU, NM, L2;
+  int passes;
+  int plane;              // floats per staged channel of an F unit
+  int n_fi;               // F/I queue length
+  int grid;
+};
+
+struct Sync {
+  uint64_t a_full[kAStages], a_empty[kAStages];
+  uint64_t b_full[2], b_empty[2];
+  uint64_t tfull[2][kGP], tempty[2];
+  uint64_t fi_full[2], fi_empty[2];
+  int fi_cnt, g_cnt;       // completed F/I (x8 warps) and G (x4 warps) units of this CTA
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const int* p, int target) {
+  if (ld_acquire_gpu(p) >= target) return;
+  while (ld_relaxed_gpu(p) < target) __nanosleep(64);
+  (void)ld_acquire_gpu(p);
+}
+__device__ __forceinline__ int ld_acquire_cta_smem(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_cta_smem(int* p, int v) {
+  asm volatile("red.release.cta.shared::cta.add.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// The F/I queue: step s holds the kNCG F units of block s (s < n_blk) and
+// then the kNIG I units of block s - L2.  Walked incrementally (indices only grow).
+struct FIWalker {
+  int step = 0, base = 0, items = 0;
+  __device__ void init(const Params& P) { items = count(P, 0); }
+  __device__ static int count(const Params& P, int s) {
+    const int nb = P.g.n_blk;
+    return (s < nb ? kNCG : 0) + (s >= P.L2 && s - P.L2 < nb ? kNIG : 0);
+  }
+  // -> kind (0 = F, 2 = I), block, sub
+  __device__ void decode(const Params& P, int u, int& kind, int& b, int& sub) {
+    while (u >= base + items) {
+      base += items;
+      ++step;
+      items = count(P, step);
+    }
+    const int k = u - base;
+    const int nf = step < P.g.n_blk ? kNCG : 0;
+    if (k < nf) { kind = 0; b = step; sub = k; }
+    else { kind = 2; b = step - P.L2; sub = k - nf; }
+  }
+};
+
+// ------------------------------------------------------------ F/I producer
+__device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
+  const Geo& g = P.g;
+  const int lane = threadIdx.x & 31;
+  const int* doneG = P.counters + g.n_blk;
+  FIWalker wk;
+  wk.init(P);
+  int it = 0;
+  for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
+    int kind, b, sub;
+    wk.decode(P, u, kind, b, sub);
+    const int slot = it & 1;
+    uint8_t* dstbase = smem + kOffFI + slot * kFISlot;
+    if (lane == 0) {
+      if (kind == 0) {
+        if (b >= P.NU) spin_until(doneG + (b - P.NU), kNGG);     // U slot free
+      } else {
+        spin_until(doneG + b, kNGG);                               // M complete
+        fence_proxy_async_global();
+      }
+      mbar_wait(&sy.fi_empty[slot], ((it >> 1) & 1) ^ 1);
+    }
+    __syncwarp();
+    fence_proxy_async_smem();
+    if (kind == 0) {
+      const int part = sub / (kC / kCPC), cg = sub % (kC / kCPC);
+      const int t0 = b * kBlockTiles + part * kFT;
+      const int tlast = min(t0 + kFT, g.n_tile) - 1;
+      const int gr0 = t0 / g.tiles_x;
+      const int nrows = tlast >= t0 ? tlast / g.tiles_x - gr0 + 1 : 0;
+      float* xs = reinterpret_cast<float*>(dstbase);
+      for (int cu = lane; cu < kCPC * nrows; cu += 32) {
+        const int j = cu % nrows, cl = cu / nrows;
+        const int gr = gr0 + j;
+        const int bi = gr / g.tiles_y, ty = gr - bi * g.tiles_y;
+        const int y0 = ty * g.m - g.pad_lo;
+        const int ya = max(y0, 0), yb = min(y0 + kT, g.H);
+        const int c = cg * kCPC + cl;
+        float* dst = xs + cl * P.plane + j * kT * g.W;
+        if (yb > ya) {
+          const uint32_t bytes = static_cast<uint32_t>((yb - ya) * g.W * 4);
+          mbar_add_tx(&sy.fi_full[slot], bytes);
+          bulk_g2s(dst + (ya - y0) * g.W, P.x + ((static_cast<size_t>(bi) * g.C + c) * g.H + ya) * g.W, bytes,
+                   &sy.fi_full[slot]);
+        }
+        for (int r = 0; r < kT; ++r)
+          if (r < ya - y0 || r >= yb - y0)
+            for (int s2 = 0; s2 < g.W; ++s2) dst[r * g.W + s2] = 0.0f;
+      }
+    } else {
+      const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * kMSlot +
+                            static_cast<size_t>(2 * sub) * kBlockTiles * 8;
+      for (int p = lane; p < kP; p += 32) {
+        mbar_add_tx(&sy.fi_full[slot], kIPos);
+        bulk_g2s(dstbase + p * kIPos, msrc + p * kMPos, kIPos, &sy.fi_full[slot]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
+  }
+}
+
+// ------------------------------------------------------------- F/I workers
+__device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
+  const Geo& g = P.g;
+  const int wtid = threadIdx.x - 256, lane = threadIdx.x & 31, wl = wtid >> 5;
+  FIWalker wk;
+  wk.init(P);
+  int it = 0;
+  for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
+    int kind, b, sub;
+    wk.decode(P, u, kind, b, sub);
+    const int slot = it & 1;
+    const uint8_t* src = smem + kOffFI + slot * kFISlot;
+    mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
+    if (kind == 0) {
+      // ---- F(b, sub): thread = (tile tl, channel pair q); a warp = 8 tiles
+      // (one core-matrix row group) x 4 pairs (one 8-channel k group), so
+      // every store instruction writes one contiguous 128-byte core matrix
+      const int part = sub / (kC / kCPC), cg = sub % (kC / kCPC);
+      const int tb0 = part * kFT;
+      const int t0 = b * kBlockTiles + tb0;
+      const int gr0 = t0 / g.tiles_x;
+      const int tl = wl * 8 + (lane & 7), q = lane >> 3;
+      const int tile = t0 + tl;
+      const bool live = tile < g.n_tile;
+      float2 w[kT][kT];
+      if (live) {
+        const int per_img = g.tiles_y * g.tiles_x;
+        const int bi = tile / per_img;
+        const int rem = tile - bi * per_img;
+        const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+        const int j = bi * g.tiles_y + ty - gr0;
+        const int x0 = tx * g.m - g.pad_lo;
+        const float* pa = reinterpret_cast<const float*>(src) + (2 * q) * P.plane + j * kT * g.W + x0;
+        const float* pb = pa + P.plane;
+        if (g.pad_lo == 1 && x0 >= 3 && x0 + kT <= g.W) {
+          // interior window: two aligned 16-byte loads + one scalar per row
+#pragma unroll
+          for (int r = 0; r < kT; ++r) {
+            const float* ra = pa + r * g.W - 3;
+            const float* rb = pb + r * g.W - 3;
+            const float4 a0 = *reinterpret_cast<const float4*>(ra), a1 = *reinterpret_cast<const float4*>(ra + 4);
+            const float4 b0 = *reinterpret_cast<const float4*>(rb), b1 = *reinterpret_cast<const float4*>(rb + 4);
+            w[r][0] = make_float2(a0.w, b0.w);
+            w[r][1] = make_float2(a1.x, b1.x);
+            w[r][2] = make_float2(a1.y, b1.y);
+            w[r][3] = make_float2(a1.z, b1.z);
+            w[r][4] = make_float2(a1.w, b1.w);
+            w[r][5] = make_float2(ra[8], rb[8]);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < kT; ++r)
+#pragma unroll
+            for (int s = 0; s < kT; ++s) {
+              const bool in = x0 + s >= 0 && x0 + s < g.W;
+              w[r][s] = in ? make_float2(pa[r * g.W + s], pb[r * g.W + s]) : make_float2(0.0f, 0.0f);
+            }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window in registers: slot free
+      if (live) {
+        forward6_inplace<PairOps>(w);     // == forward_transform2<6> (same operations, in place)
+        const int row = tb0 + tl, c0 = cg * kCPC + 2 * q;
+        uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * kUSlot + (c0 >> 5) * kAHalf +
+                       (row >> 3) * 512 + ((c0 & 31) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2;
+#pragma unroll
+        for (int r = 0; r < kT; ++r)
+#pragma unroll
+          for (int s = 0; s < kT; ++s) {
+            uint32_t hi, lo;
+            split_bf16x2(w[r][s], hi, lo);
+            uint8_t* p = dst + (r * kT + s) * kUPos;
+            *reinterpret_cast<uint32_t*>(p) = hi;
+            *reinterpret_cast<uint32_t*>(p + 2 * kAHalf) = lo;
+          }
+      }
+    } else {
+      // ---- I(b, sub): thread = (tile, c' pair); 36 staged float2 per thread
+      const int tl = wtid & (kBlockTiles - 1), pr = wtid >> 7;
+      const int tile = b * kBlockTiles + tl;
+      float2 mm[kT][kT];
+      const float2* ms = reinterpret_cast<const float2*>(src + pr * kBlockTiles * 8) + tl;
+#pragma unroll
+      for (int r = 0; r < kT; ++r)
+#pragma unroll
+        for (int s = 0; s < kT; ++s) mm[r][s] = ms[(r * kT + s) * (kIPos / 8)];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
+      if (tile < g.n_tile) {
+        float2 out[kT - 2][kT - 2];
+        inverse6_inplace<PairOps>(mm, out);     // == inverse_transform2<6>
+        const int per_img = g.tiles_y * g.tiles_x;
+        const int bi = tile / per_img;
+        const int rem = tile - bi * per_img;
+        const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+        constexpr int MO = kT - 2;
+        const int oy = ty * MO, ox = tx * MO;
+        const bool vec = oy + MO <= g.Ho && ox + MO <= g.Wo && (g.Wo & 3) == 0;
+        const size_t plane = static_cast<size_t>(g.Ho) * g.Wo;
+        const int cp = 4 * sub + 2 * pr;
+        float* ybase = P.y + (static_cast<size_t>(bi) * g.Cp + cp) * plane + static_cast<size_t>(oy) * g.Wo + ox;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float* dst = ybase + h * plane;
+          if (vec) {
+#pragma unroll
+            for (int r = 0; r < MO; ++r)
+              *reinterpret_cast<float4*>(dst + r * g.Wo) =
+                  h ? make_float4(out[r][0].y, out[r][1].y, out[r][2].y, out[r][3].y)
+                    : make_float4(out[r][0].x, out[r][1].x, out[r][2].x, out[r][3].x);
+          } else {
+#pragma unroll
+            for (int r = 0; r < MO; ++r)
+#pragma unroll
+              for (int s = 0; s < MO; ++s)
+                if (oy + r < g.Ho && ox + s < g.Wo) dst[r * g.Wo + s] = h ? out[r][s].y : out[r][s].x;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) red_release_cta_smem(&sy.fi_cnt, 1);
+  }
+}
+
+// -------------------------------------------------------------- G producer
+__device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
+  const Geo& g = P.g;
+  const int* doneF = P.counters;
+  const int* doneI = P.counters + 2 * g.n_blk;
+  int a_it = 0, b_it = 0;
+  for (int v = blockIdx.x; v < n_g; v += P.grid) {
+    const int b = v / kNGG, gg = v - b * kNGG;
+    spin_until(doneF + b, kNCG);                                   // U complete
+    if (b >= P.NM) spin_until(doneI + (b - P.NM), kNIG);           // M slot free
+    fence_proxy_async_global();
+    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * kUSlot;
+    for (int pl = 0; pl < kGP; ++pl) {
+      const int p = gg * kGP + pl;
+      const int pb = b_it & 1;
+      mbar_wait(&sy.b_empty[pb], ((b_it >> 1) & 1) ^ 1);
+      uint8_t* bdst = smem + kOffB + pb * kBBuf;
+      mbar_expect_tx(&sy.b_full[pb], kBBuf);
+      bulk_g2s(bdst, P.vpack + static_cast<size_t>(p) * kBBuf, kBBuf, &sy.b_full[pb]);
+      ++b_it;
+      for (int kb = 0; kb < 2; ++kb) {
+        const int st = a_it % kAStages;
+        mbar_wait(&sy.a_empty[st], ((a_it / kAStages) & 1) ^ 1);
+        uint8_t* adst = smem + st * kAStage;
+        mbar_expect_tx(&sy.a_full[st], kAStage);
+        const uint8_t* asrc = uslot + p * kUPos + kb * kAHalf;
+        bulk_g2s(adst, asrc, kAHalf, &sy.a_full[st]);                          // hi
+        bulk_g2s(adst + kAHalf, asrc + 2 * kAHalf, kAHalf, &sy.a_full[st]);    // lo
+        ++a_it;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- G issuer
+__device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
+  const uint32_t idesc = idesc_bf16(kBlockTiles, kC);
+  int a_it = 0, b_it = 0, k = 0;
+  for (int v = blockIdx.x; v < n_g; v += P.grid, ++k) {
+    const int buf = k & 1;
+    mbar_wait(&sy.tempty[buf], ((k >> 1) & 1) ^ 1);
+    tc_fence_after();
+    for (int pl = 0; pl < kGP; ++pl) {
+      const int pb = b_it & 1;
+      mbar_wait(&sy.b_full[pb], (b_it >> 1) & 1);
+      const uint32_t sb = smem_u32(smem + kOffB + pb * kBBuf);
+      const uint32_t dcol = sy.tmem + buf * (kGP * kC) + pl * kC;
+      for (int kb = 0; kb < 2; ++kb) {
+        const int st = a_it % kAStages;
+        mbar_wait(&sy.a_full[st], (a_it / kAStages) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + st * kAStage);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const uint64_t ahi = smem_desc(sa + s * 256, 128, 512);
+          const uint64_t alo = smem_desc(sa + kAHalf + s * 256, 128, 512);
+          const uint64_t bhi = smem_desc(sb + kb * 512 + s * 256, 128, 1024);
+          const uint64_t blo = smem_desc(sb + kBSlab + kb * 512 + s * 256, 128, 1024);
+          const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
+          if (P.passes > 1) {
+            mma_bf16_ss(dcol, alo, bhi, idesc, first);
+            mma_bf16_ss(dcol, ahi, blo, idesc, 1u);
+            mma_bf16_ss(dcol, ahi, bhi, idesc, 1u);
+          } else {
+            mma_bf16_ss(dcol, ahi, bhi, idesc, first);
+          }
+        }
+        mma_commit(&sy.a_empty[st]);
+        ++a_it;
+      }
+      mma_commit(&sy.b_empty[pb]);
+      mma_commit(&sy.tfull[buf][pl]);
+      ++b_it;
+    }
+  }
+}
+
+// -------------------------------------------------------------- G epilogue
+__device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
+  const int lane = threadIdx.x & 31, qd = (threadIdx.x >> 5) & 3;
+  const int row = qd * 32 + lane;
+  int k = 0;
+  for (int v = blockIdx.x; v < n_g; v += P.grid, ++k) {
+    const int b = v / kNGG, gg = v - b * kNGG;
+    const int buf = k & 1;
+    const bool live = b * kBlockTiles + row < P.g.n_tile;
+    float* mslot = P.mring + static_cast<size_t>(b % P.NM) * (kMSlot / 4);
+    for (int pl = 0; pl < kGP; ++pl) {
+      mbar_wait(&sy.tfull[buf][pl], (k >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (kGP * kC) + pl * kC;
+      float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * kGP + pl) * (kMPos / 4)) + row;
+#pragma unroll
+      for (int c = 0; c < kC; c += 16) {
+        float vv[16];
+        tmem_ld16(taddr + c, vv);
+        tmem_ld_wait();
+        if (live) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) __stcg(mrow + (c / 2 + i) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]));
+        }
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&sy.tempty[buf]);
+      red_release_cta_smem(&sy.g_cnt, 1);
+    }
+  }
+}
+
+// --------------------------------------------------------------- publisher
+__device__ void publisher(const Params& P, Sync& sy, int n_g) {
+  if ((threadIdx.x & 31) != 0) return;
+  int* doneF = P.counters;
+  int* doneG = doneF + P.g.n_blk;
+  int* doneI = doneG + P.g.n_blk;
+  FIWalker wk;
+  wk.init(P);
+  int uf = blockIdx.x, kf = 0;        // next F/I unit of this CTA, its ordinal
+  int vg = blockIdx.x, kg = 0;        // next G unit, its ordinal
+  while (uf < P.n_fi || vg < n_g) {
+    bool progress = false;
+    if (uf < P.n_fi && ld_acquire_cta_smem(&sy.fi_cnt) >= 8 * (kf + 1)) {
+      int kind, b, sub;
+      wk.decode(P, uf, kind, b, sub);
+      __threadfence();
+      atomicAdd((kind == 0 ? doneF : doneI) + b, 1);
+      uf += P.grid;
+      ++kf;
+      progress = true;
+    }
+    if (vg < n_g && ld_acquire_cta_smem(&sy.g_cnt) >= 4 * (kg + 1)) {
+      __threadfence();
+      atomicAdd(doneG + vg / kNGG, 1);
+      vg += P.grid;
+      ++kg;
+      progress = true;
+    }
+    if (!progress) __nanosleep(32);
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ Sync sy;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kAStages; ++s) { mbar_init(&sy.a_full[s], 1); mbar_init(&sy.a_empty[s], 1); }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sy.b_full[s], 1);
+      mbar_init(&sy.b_empty[s], 1);
+      for (int p = 0; p < kGP; ++p) mbar_init(&sy.tfull[s][p], 1);
+      mbar_init(&sy.tempty[s], 4);
+      mbar_init(&sy.fi_full[s], 1);
+      mbar_init(&sy.fi_empty[s], 8);
+    }
+    sy.fi_cnt = 0;
+    sy.g_cnt = 0;
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&sy.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const int n_g = P.g.n_blk * kNGG;
+  if (warp == 0) {
+    if (lane_id() == 0) g_producer(P, smem, sy, n_g);
+  } else if (warp == 1) {
+    if (lane_id() == 0) g_issuer(P, smem, sy, n_g);
+  } else if (warp == 2) {
+    fi_producer(P, smem, sy);
+  } else if (warp == 3) {
+    publisher(P, sy, n_g);
+  } else if (warp < 8) {
+    g_epilogue(P, sy, n_g);
+  } else {
+    fi_workers(P, smem, sy);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(sy.tmem);
+  }
+}
+
+struct Plan {
+  bool ok;
+  int NU, NM, L2, plane;
+  size_t counters_bytes;
+};
+
+static Plan plan(const Geo& g) {
+  Plan pl = {};
+  if (g.fft || g.T != kT || g.C != kC || g.Cp != kC || g.Cpad != kC || g.Cppad != kC) return pl;
+  if (g.W % 4 != 0 || g.m != 4) return pl;
+  const int trows = ceil_div(kFT - 1, g.tiles_x) + 1;
+  pl.plane = round_up(trows * kT * g.W, 32) + 16;
+  if (static_cast<size_t>(kCPC) * pl.plane * 4 > kFISlot) return pl;
+  size_t budget = 150ull << 20;
+  if (const char* e = getenv("WF_WS_BUDGET_MB")) budget = static_cast<size_t>(atoi(e)) << 20;
+  int slots = static_cast<int>(budget / (kUSlot + kMSlot));
+  if (slots < 4) slots = 4;
+  pl.NU = std::min(slots / 2, g.n_blk);
+  pl.NM = std::min(slots - slots / 2, g.n_blk);
+  int lag = 24;
+  if (const char* e = getenv("WF_WS_LAG")) lag = atoi(e);
+  // deadlock freedom: some L1 with 1 <= L1 < NU (when F waits on G) and L2 - L1 < NM
+  const int lmax = (pl.NU >= g.n_blk ? g.n_blk + pl.NM : pl.NU + pl.NM - 2);
+  if (lag > lmax) lag = lmax;
+  if (lag < 2) lag = 2;
+  pl.L2 = lag;
+  if (pl.NU < 2 && pl.NU < g.n_blk) return pl;
+  pl.counters_bytes = static_cast<size_t>(3 * g.n_blk) * sizeof(int);
+  pl.ok = true;
+  return pl;
+}
+
+}  // namespace ws
+
+bool ws_fits(const Geo& g) {
+  if (const char* e = getenv("WF_WS")) if (atoi(e) == 0) return false;
+  return ws::plan(g).ok;
+}
+
+size_t ws_scratch_bytes(const Geo& g) {
+  const ws::Plan pl = ws::plan(g);
+  if (!pl.ok) return 0;
+  return round_up(static_cast<int>(pl.counters_bytes), 1024) + pl.NU * ws::kUSlot + pl.NM * ws::kMSlot;
+}
+
+cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g, int passes,
+                         int sm_count, cudaStream_t st) {
+  const ws::Plan pl = ws::plan(g);
+  if (!pl.ok) return cudaErrorInvalidValue;
+  ws::Params P;
+  P.x = x; P.y = y; P.vpack = vpack;
+  P.counters = reinterpret_cast<int*>(scratch);
+  P.uring = scratch + round_up(static_cast<int>(pl.counters_bytes), 1024);
+  P.mring = reinterpret_cast<float*>(P.uring + pl.NU * ws::kUSlot);
+  P.g = g;
+  P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
+  P.passes = passes;
+  P.plane = pl.plane;
+  P.n_fi = g.n_blk * (ws::kNCG + ws::kNIG);
+  P.grid = sm_count;
+  cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
+  if (e != cudaSuccess) return e;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(ws::fused_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ws::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  note_launch();
+  ws::fused_ws_kernel<<<sm_count, ws::NT, ws::kSmem, st>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace wf
