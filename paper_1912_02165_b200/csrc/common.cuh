@@ -221,12 +221,15 @@ __device__ __forceinline__ void at6_line(V m0, V m1, V m2, V m3, V m4, V m5, V& 
   y2 = O::fma(4.0f, r, p);
   y3 = O::fma(8.0f, s, O::sub(q, m5));
 }
+// Order: every window row first (B^T along the row), then every column --
+// the streaming order of the fused kernel, which transforms each staged row
+// as it is loaded and emits one column of positions at a time.
 template <class O, class V>
 __device__ __forceinline__ void forward6_inplace(V (&u)[6][6]) {
 #pragma unroll
-  for (int s = 0; s < 6; ++s) bt6_line<O>(u[0][s], u[1][s], u[2][s], u[3][s], u[4][s], u[5][s]);
-#pragma unroll
   for (int r = 0; r < 6; ++r) bt6_line<O>(u[r][0], u[r][1], u[r][2], u[r][3], u[r][4], u[r][5]);
+#pragma unroll
+  for (int s = 0; s < 6; ++s) bt6_line<O>(u[0][s], u[1][s], u[2][s], u[3][s], u[4][s], u[5][s]);
 }
 template <class O, class V>
 __device__ __forceinline__ void forward6(const V (&x)[6][6], V (&u)[6][6]) {
@@ -234,10 +237,7 @@ __device__ __forceinline__ void forward6(const V (&x)[6][6], V (&u)[6][6]) {
   for (int r = 0; r < 6; ++r)
 #pragma unroll
     for (int s = 0; s < 6; ++s) u[r][s] = x[r][s];
-#pragma unroll
-  for (int s = 0; s < 6; ++s) bt6_line<O>(u[0][s], u[1][s], u[2][s], u[3][s], u[4][s], u[5][s]);
-#pragma unroll
-  for (int r = 0; r < 6; ++r) bt6_line<O>(u[r][0], u[r][1], u[r][2], u[r][3], u[r][4], u[r][5]);
+  forward6_inplace<O>(u);
 }
 // same operations as inverse6, with the column pass written over mm
 template <class O, class V>

@@ -72,6 +72,32 @@ struct Params {
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
   int grid;
+  int prof;
+};
+
+// Optional per-CTA role accounting (WF_WS_PROF=1; tools/ws_prof.py):
+// clock64 cycles per slot, globaltimer ns for the role end times.
+constexpr int kProfSlots = 32;
+__device__ unsigned long long g_wsprof[1024 * kProfSlots];
+enum ProfSlot {
+  kGPDep, kGPStage, kGIFull, kGITempty, kGEWait, kGEBusy, kFPDep, kFPSlot, kFWWait, kFWF, kFWI, kPubFence,
+  kStart, kEndGP, kEndGI, kEndGE, kEndFP, kEndFW, kEndPub, kNF, kNI, kFWLoop
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__shared__ unsigned long long s_prof[kProfSlots];   // accumulated in smem, flushed at exit
+// Compiled in only for the profiling instantiation of the kernel.
+template <bool ON>
+struct ProfT {
+  bool on;
+  __device__ ProfT(bool flag) : on(ON && flag) {}
+  __device__ long long now() const { return (ON && on) ? clock64() : 0; }
+  __device__ void add(int slot, long long t0) const { if (ON && on) s_prof[slot] += clock64() - t0; }
+  __device__ void inc(int slot) const { if (ON && on) s_prof[slot] += 1; }
+  __device__ void end(int slot) const { if (ON && on) g_wsprof[blockIdx.x * kProfSlots + slot] = gtimer(); }
 };
 
 struct Sync {
@@ -106,38 +132,56 @@ __device__ __forceinline__ int ld_acquire_cta_smem(const int* p) {
 __device__ __forceinline__ void red_release_cta_smem(int* p, int v) {
   asm volatile("red.release.cta.shared::cta.add.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
+// Publish one completed unit: release at gpu scope (orders every write this
+// thread performed or observed -- the other warps' stores, through the CTA
+// scope acquire that preceded it -- before the counter increment).
+__device__ __forceinline__ void red_release_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_acqrel_cta_smem(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // The F/I queue: step s holds the kNCG F units of block s (s < n_blk) and
-// then the kNIG I units of block s - L2.  Walked incrementally (indices only grow).
+// then the kNIG I units of block s - L2.  Closed-form decode (no state
+// carried across units: nothing to keep live through the transforms).
 struct FIWalker {
-  int step = 0, base = 0, items = 0;
-  __device__ void init(const Params& P) { items = count(P, 0); }
-  __device__ static int count(const Params& P, int s) {
-    const int nb = P.g.n_blk;
-    return (s < nb ? kNCG : 0) + (s >= P.L2 && s - P.L2 < nb ? kNIG : 0);
-  }
+  __device__ void init(const Params&) {}
   // -> kind (0 = F, 2 = I), block, sub
-  __device__ void decode(const Params& P, int u, int& kind, int& b, int& sub) {
-    while (u >= base + items) {
-      base += items;
-      ++step;
-      items = count(P, step);
+  __device__ void decode(const Params& P, int u, int& kind, int& b, int& sub) const {
+    const int nb = P.g.n_blk, L = P.L2;
+    static_assert(kNCG == kNIG, "closed-form decode assumes equal F and I units per block");
+    constexpr int n = kNCG;
+    if (L >= nb) {                       // all F steps come before the first I step
+      if (u < n * nb) { kind = 0; b = u / n; sub = u - b * n; }
+      else { kind = 2; b = (u - n * nb) / n; sub = (u - n * nb) - b * n; }
+      return;
     }
-    const int k = u - base;
-    const int nf = step < P.g.n_blk ? kNCG : 0;
-    if (k < nf) { kind = 0; b = step; sub = k; }
-    else { kind = 2; b = step - P.L2; sub = k - nf; }
+    if (u < n * L) { kind = 0; b = u / n; sub = u - b * n; return; }
+    const int u2 = u - n * L;
+    if (u2 < 2 * n * (nb - L)) {         // steps L .. nb-1: F(s) then I(s - L)
+      const int s = u2 / (2 * n), k = u2 - s * 2 * n;
+      if (k < n) { kind = 0; b = L + s; sub = k; }
+      else { kind = 2; b = s; sub = k - n; }
+      return;
+    }
+    const int u3 = u2 - 2 * n * (nb - L);  // steps nb ..: I only
+    kind = 2; b = nb - L + u3 / n; sub = u3 - (u3 / n) * n;
   }
 };
 
 // ------------------------------------------------------------ F/I producer
+template <bool PROF>
 __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
   const Geo& g = P.g;
   const int lane = threadIdx.x & 31;
   const int* doneG = P.counters + g.n_blk;
+  const ProfT<PROF> pf(P.prof && lane == 0);
   FIWalker wk;
   wk.init(P);
   int it = 0;
@@ -147,13 +191,17 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     const int slot = it & 1;
     uint8_t* dstbase = smem + kOffFI + slot * kFISlot;
     if (lane == 0) {
+      long long t0 = pf.now();
       if (kind == 0) {
         if (b >= P.NU) spin_until(doneG + (b - P.NU), kNGG);     // U slot free
       } else {
         spin_until(doneG + b, kNGG);                               // M complete
         fence_proxy_async_global();
       }
+      pf.add(kFPDep, t0);
+      t0 = pf.now();
       mbar_wait(&sy.fi_empty[slot], ((it >> 1) & 1) ^ 1);
+      pf.add(kFPSlot, t0);
     }
     __syncwarp();
     fence_proxy_async_smem();
@@ -193,12 +241,16 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
   }
+  pf.end(kEndFP);
 }
 
 // ------------------------------------------------------------- F/I workers
+template <bool PROF>
 __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
   const Geo& g = P.g;
   const int wtid = threadIdx.x - 256, lane = threadIdx.x & 31, wl = wtid >> 5;
+  const ProfT<PROF> pf(P.prof && wtid == 0);
+  const long long tloop = pf.now();
   FIWalker wk;
   wk.init(P);
   int it = 0;
@@ -207,7 +259,10 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     wk.decode(P, u, kind, b, sub);
     const int slot = it & 1;
     const uint8_t* src = smem + kOffFI + slot * kFISlot;
+    long long t0 = pf.now();
     mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
+    pf.add(kFWWait, t0);
+    t0 = pf.now();
     if (kind == 0) {
       // ---- F(b, sub): thread = (tile tl, channel pair q); a warp = 8 tiles
       // (one core-matrix row group) x 4 pairs (one 8-channel k group), so
@@ -229,121 +284,135 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
         const int x0 = tx * g.m - g.pad_lo;
         const float* pa = reinterpret_cast<const float*>(src) + (2 * q) * P.plane + j * kT * g.W + x0;
         const float* pb = pa + P.plane;
-        if (g.pad_lo == 1 && x0 >= 3 && x0 + kT <= g.W) {
-          // interior window: two aligned 16-byte loads + one scalar per row
+        // window columns [x0, x0 + 6) with x0 = 4 tx - 1: two aligned 16-byte
+        // loads [x0 - 3, x0 + 5) plus one scalar per row, branch free; the
+        // image's left / right padding column is masked (the loads there read
+        // neighbouring staged data, inside the slot).  Each row is transformed
+        // (B^T along the row) as soon as it is loaded.
+        const bool lo_ok = x0 >= 0, hi_ok = x0 + kT <= g.W;
 #pragma unroll
-          for (int r = 0; r < kT; ++r) {
-            const float* ra = pa + r * g.W - 3;
-            const float* rb = pb + r * g.W - 3;
-            const float4 a0 = *reinterpret_cast<const float4*>(ra), a1 = *reinterpret_cast<const float4*>(ra + 4);
-            const float4 b0 = *reinterpret_cast<const float4*>(rb), b1 = *reinterpret_cast<const float4*>(rb + 4);
-            w[r][0] = make_float2(a0.w, b0.w);
-            w[r][1] = make_float2(a1.x, b1.x);
-            w[r][2] = make_float2(a1.y, b1.y);
-            w[r][3] = make_float2(a1.z, b1.z);
-            w[r][4] = make_float2(a1.w, b1.w);
-            w[r][5] = make_float2(ra[8], rb[8]);
-          }
-        } else {
-#pragma unroll
-          for (int r = 0; r < kT; ++r)
-#pragma unroll
-            for (int s = 0; s < kT; ++s) {
-              const bool in = x0 + s >= 0 && x0 + s < g.W;
-              w[r][s] = in ? make_float2(pa[r * g.W + s], pb[r * g.W + s]) : make_float2(0.0f, 0.0f);
-            }
+        for (int r = 0; r < kT; ++r) {
+          const float* ra = pa + r * g.W - 3;
+          const float* rb = pb + r * g.W - 3;
+          const float4 a0 = *reinterpret_cast<const float4*>(ra), a1 = *reinterpret_cast<const float4*>(ra + 4);
+          const float4 b0 = *reinterpret_cast<const float4*>(rb), b1 = *reinterpret_cast<const float4*>(rb + 4);
+          const float a5 = ra[8], b5 = rb[8];
+          w[r][0] = lo_ok ? make_float2(a0.w, b0.w) : make_float2(0.0f, 0.0f);
+          w[r][1] = make_float2(a1.x, b1.x);
+          w[r][2] = make_float2(a1.y, b1.y);
+          w[r][3] = make_float2(a1.z, b1.z);
+          w[r][4] = make_float2(a1.w, b1.w);
+          w[r][5] = hi_ok ? make_float2(a5, b5) : make_float2(0.0f, 0.0f);
+          bt6_line<PairOps>(w[r][0], w[r][1], w[r][2], w[r][3], w[r][4], w[r][5]);
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window in registers: slot free
+      if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window consumed: slot free
       if (live) {
-        forward6_inplace<PairOps>(w);     // == forward_transform2<6> (same operations, in place)
+        // columns: B^T down each column, then one column of positions
+        // (r, s), r = 0..5, split and stored (== forward_transform2<6>)
         const int row = tb0 + tl, c0 = cg * kCPC + 2 * q;
         uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * kUSlot + (c0 >> 5) * kAHalf +
                        (row >> 3) * 512 + ((c0 & 31) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2;
 #pragma unroll
-        for (int r = 0; r < kT; ++r)
+        for (int s = 0; s < kT; ++s) {
+          bt6_line<PairOps>(w[0][s], w[1][s], w[2][s], w[3][s], w[4][s], w[5][s]);
 #pragma unroll
-          for (int s = 0; s < kT; ++s) {
+          for (int r = 0; r < kT; ++r) {
             uint32_t hi, lo;
             split_bf16x2(w[r][s], hi, lo);
             uint8_t* p = dst + (r * kT + s) * kUPos;
             *reinterpret_cast<uint32_t*>(p) = hi;
             *reinterpret_cast<uint32_t*>(p + 2 * kAHalf) = lo;
           }
+        }
       }
     } else {
       // ---- I(b, sub): thread = (tile, c' pair); 36 staged float2 per thread
       const int tl = wtid & (kBlockTiles - 1), pr = wtid >> 7;
       const int tile = b * kBlockTiles + tl;
-      float2 mm[kT][kT];
+      // column pass as the staged products are read (A^T down each column),
+      // then one output row at a time (== inverse_transform2<6>)
+      constexpr int MO = kT - 2;
+      float2 t[MO][kT];
       const float2* ms = reinterpret_cast<const float2*>(src + pr * kBlockTiles * 8) + tl;
 #pragma unroll
-      for (int r = 0; r < kT; ++r)
+      for (int s = 0; s < kT; ++s) {
+        float2 m[kT];
 #pragma unroll
-        for (int s = 0; s < kT; ++s) mm[r][s] = ms[(r * kT + s) * (kIPos / 8)];
+        for (int r = 0; r < kT; ++r) m[r] = ms[(r * kT + s) * (kIPos / 8)];
+        at6_line<PairOps>(m[0], m[1], m[2], m[3], m[4], m[5], t[0][s], t[1][s], t[2][s], t[3][s]);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
       if (tile < g.n_tile) {
-        float2 out[kT - 2][kT - 2];
-        inverse6_inplace<PairOps>(mm, out);     // == inverse_transform2<6>
         const int per_img = g.tiles_y * g.tiles_x;
         const int bi = tile / per_img;
         const int rem = tile - bi * per_img;
         const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
-        constexpr int MO = kT - 2;
         const int oy = ty * MO, ox = tx * MO;
         const bool vec = oy + MO <= g.Ho && ox + MO <= g.Wo && (g.Wo & 3) == 0;
         const size_t plane = static_cast<size_t>(g.Ho) * g.Wo;
         const int cp = 4 * sub + 2 * pr;
         float* ybase = P.y + (static_cast<size_t>(bi) * g.Cp + cp) * plane + static_cast<size_t>(oy) * g.Wo + ox;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float* dst = ybase + h * plane;
+        for (int r = 0; r < MO; ++r) {
+          float2 o[MO];
+          at6_line<PairOps>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], o[0], o[1], o[2], o[3]);
           if (vec) {
+            *reinterpret_cast<float4*>(ybase + r * g.Wo) = make_float4(o[0].x, o[1].x, o[2].x, o[3].x);
+            *reinterpret_cast<float4*>(ybase + plane + r * g.Wo) = make_float4(o[0].y, o[1].y, o[2].y, o[3].y);
+          } else if (oy + r < g.Ho) {
 #pragma unroll
-            for (int r = 0; r < MO; ++r)
-              *reinterpret_cast<float4*>(dst + r * g.Wo) =
-                  h ? make_float4(out[r][0].y, out[r][1].y, out[r][2].y, out[r][3].y)
-                    : make_float4(out[r][0].x, out[r][1].x, out[r][2].x, out[r][3].x);
-          } else {
-#pragma unroll
-            for (int r = 0; r < MO; ++r)
-#pragma unroll
-              for (int s = 0; s < MO; ++s)
-                if (oy + r < g.Ho && ox + s < g.Wo) dst[r * g.Wo + s] = h ? out[r][s].y : out[r][s].x;
+            for (int c = 0; c < MO; ++c)
+              if (ox + c < g.Wo) {
+                ybase[r * g.Wo + c] = o[c].x;
+                ybase[plane + r * g.Wo + c] = o[c].y;
+              }
           }
         }
       }
     }
     __syncwarp();
     if (lane == 0) red_release_cta_smem(&sy.fi_cnt, 1);
+    pf.add(kind == 0 ? kFWF : kFWI, t0);
+    pf.inc(kind == 0 ? kNF : kNI);
   }
+  pf.add(kFWLoop, tloop);
+  pf.end(kEndFW);
 }
 
 // -------------------------------------------------------------- G producer
+template <bool PROF>
 __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   const Geo& g = P.g;
   const int* doneF = P.counters;
   const int* doneI = P.counters + 2 * g.n_blk;
+  const ProfT<PROF> pf(P.prof);
   int a_it = 0, b_it = 0;
   for (int v = blockIdx.x; v < n_g; v += P.grid) {
     const int b = v / kNGG, gg = v - b * kNGG;
+    long long t0 = pf.now();
     spin_until(doneF + b, kNCG);                                   // U complete
     if (b >= P.NM) spin_until(doneI + (b - P.NM), kNIG);           // M slot free
+    pf.add(kGPDep, t0);
     fence_proxy_async_global();
     const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * kUSlot;
     for (int pl = 0; pl < kGP; ++pl) {
       const int p = gg * kGP + pl;
       const int pb = b_it & 1;
+      long long t1 = pf.now();
       mbar_wait(&sy.b_empty[pb], ((b_it >> 1) & 1) ^ 1);
+      pf.add(kGPStage, t1);
       uint8_t* bdst = smem + kOffB + pb * kBBuf;
       mbar_expect_tx(&sy.b_full[pb], kBBuf);
       bulk_g2s(bdst, P.vpack + static_cast<size_t>(p) * kBBuf, kBBuf, &sy.b_full[pb]);
       ++b_it;
       for (int kb = 0; kb < 2; ++kb) {
         const int st = a_it % kAStages;
+        long long t2 = pf.now();
         mbar_wait(&sy.a_empty[st], ((a_it / kAStages) & 1) ^ 1);
+        pf.add(kGPStage, t2);
         uint8_t* adst = smem + st * kAStage;
         mbar_expect_tx(&sy.a_full[st], kAStage);
         const uint8_t* asrc = uslot + p * kUPos + kb * kAHalf;
@@ -353,24 +422,33 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
       }
     }
   }
+  pf.end(kEndGP);
 }
 
 // ---------------------------------------------------------------- G issuer
+template <bool PROF>
 __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   const uint32_t idesc = idesc_bf16(kBlockTiles, kC);
+  const ProfT<PROF> pf(P.prof);
   int a_it = 0, b_it = 0, k = 0;
   for (int v = blockIdx.x; v < n_g; v += P.grid, ++k) {
     const int buf = k & 1;
+    long long t0 = pf.now();
     mbar_wait(&sy.tempty[buf], ((k >> 1) & 1) ^ 1);
+    pf.add(kGITempty, t0);
     tc_fence_after();
     for (int pl = 0; pl < kGP; ++pl) {
       const int pb = b_it & 1;
+      long long t1 = pf.now();
       mbar_wait(&sy.b_full[pb], (b_it >> 1) & 1);
+      pf.add(kGIFull, t1);
       const uint32_t sb = smem_u32(smem + kOffB + pb * kBBuf);
       const uint32_t dcol = sy.tmem + buf * (kGP * kC) + pl * kC;
       for (int kb = 0; kb < 2; ++kb) {
         const int st = a_it % kAStages;
+        long long t2 = pf.now();
         mbar_wait(&sy.a_full[st], (a_it / kAStages) & 1);
+        pf.add(kGIFull, t2);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + st * kAStage);
 #pragma unroll
@@ -396,12 +474,15 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
       ++b_it;
     }
   }
+  pf.end(kEndGI);
 }
 
 // -------------------------------------------------------------- G epilogue
+template <bool PROF>
 __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
   const int lane = threadIdx.x & 31, qd = (threadIdx.x >> 5) & 3;
   const int row = qd * 32 + lane;
+  const ProfT<PROF> pf(P.prof && qd == 0 && lane == 0);
   int k = 0;
   for (int v = blockIdx.x; v < n_g; v += P.grid, ++k) {
     const int b = v / kNGG, gg = v - b * kNGG;
@@ -409,7 +490,10 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
     const bool live = b * kBlockTiles + row < P.g.n_tile;
     float* mslot = P.mring + static_cast<size_t>(b % P.NM) * (kMSlot / 4);
     for (int pl = 0; pl < kGP; ++pl) {
+      long long t0 = pf.now();
       mbar_wait(&sy.tfull[buf][pl], (k >> 1) & 1);
+      pf.add(kGEWait, t0);
+      t0 = pf.now();
       tc_fence_after();
       const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (kGP * kC) + pl * kC;
       float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * kGP + pl) * (kMPos / 4)) + row;
@@ -423,19 +507,28 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
           for (int i = 0; i < 8; ++i) __stcg(mrow + (c / 2 + i) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]));
         }
       }
+      pf.add(kGEBusy, t0);
     }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
       mbar_arrive(&sy.tempty[buf]);
-      red_release_cta_smem(&sy.g_cnt, 1);
+      // the last of the 4 epilogue warps to finish publishes the unit
+      if (atom_acqrel_cta_smem(&sy.g_cnt, 1) == 4 * k + 3) {
+        const long long t1 = pf.now();
+        red_release_gpu(P.counters + P.g.n_blk + b, 1);
+        pf.add(kPubFence, t1);
+      }
     }
   }
+  pf.end(kEndGE);
 }
 
 // --------------------------------------------------------------- publisher
+template <bool PROF>
 __device__ void publisher(const Params& P, Sync& sy, int n_g) {
   if ((threadIdx.x & 31) != 0) return;
+  const ProfT<PROF> pf(P.prof);
   int* doneF = P.counters;
   int* doneG = doneF + P.g.n_blk;
   int* doneI = doneG + P.g.n_blk;
@@ -443,28 +536,25 @@ __device__ void publisher(const Params& P, Sync& sy, int n_g) {
   wk.init(P);
   int uf = blockIdx.x, kf = 0;        // next F/I unit of this CTA, its ordinal
   int vg = blockIdx.x, kg = 0;        // next G unit, its ordinal
-  while (uf < P.n_fi || vg < n_g) {
+  while (uf < P.n_fi) {
     bool progress = false;
     if (uf < P.n_fi && ld_acquire_cta_smem(&sy.fi_cnt) >= 8 * (kf + 1)) {
       int kind, b, sub;
       wk.decode(P, uf, kind, b, sub);
-      __threadfence();
-      atomicAdd((kind == 0 ? doneF : doneI) + b, 1);
+      const long long t0 = pf.now();
+      red_release_gpu((kind == 0 ? doneF : doneI) + b, 1);
+      pf.add(kPubFence, t0);
       uf += P.grid;
       ++kf;
       progress = true;
     }
-    if (vg < n_g && ld_acquire_cta_smem(&sy.g_cnt) >= 4 * (kg + 1)) {
-      __threadfence();
-      atomicAdd(doneG + vg / kNGG, 1);
-      vg += P.grid;
-      ++kg;
-      progress = true;
-    }
+    (void)vg; (void)kg; (void)doneG;
     if (!progress) __nanosleep(32);
   }
+  pf.end(kEndPub);
 }
 
+template <bool PROF>
 __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Sync sy;
@@ -481,6 +571,8 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
     }
     sy.fi_cnt = 0;
     sy.g_cnt = 0;
+    for (int i = 0; i < kProfSlots; ++i) s_prof[i] = 0;
+    if (PROF) g_wsprof[blockIdx.x * kProfSlots + kStart] = gtimer();
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&sy.tmem);
@@ -489,17 +581,17 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   tc_fence_after();
   const int n_g = P.g.n_blk * kNGG;
   if (warp == 0) {
-    if (lane_id() == 0) g_producer(P, smem, sy, n_g);
+    if (lane_id() == 0) g_producer<PROF>(P, smem, sy, n_g);
   } else if (warp == 1) {
-    if (lane_id() == 0) g_issuer(P, smem, sy, n_g);
+    if (lane_id() == 0) g_issuer<PROF>(P, smem, sy, n_g);
   } else if (warp == 2) {
-    fi_producer(P, smem, sy);
+    fi_producer<PROF>(P, smem, sy);
   } else if (warp == 3) {
-    publisher(P, sy, n_g);
+    publisher<PROF>(P, sy, n_g);
   } else if (warp < 8) {
-    g_epilogue(P, sy, n_g);
+    g_epilogue<PROF>(P, sy, n_g);
   } else {
-    fi_workers(P, smem, sy);
+    fi_workers<PROF>(P, smem, sy);
   }
   tc_fence_before();
   __syncthreads();
@@ -507,6 +599,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
     tc_fence_after();
     tmem_dealloc<512>(sy.tmem);
   }
+  if (PROF && tid < kProfSlots && (tid < kStart || tid > kEndPub)) g_wsprof[blockIdx.x * kProfSlots + tid] += s_prof[tid];
 }
 
 struct Plan {
@@ -518,7 +611,8 @@ struct Plan {
 static Plan plan(const Geo& g) {
   Plan pl = {};
   if (g.fft || g.T != kT || g.C != kC || g.Cp != kC || g.Cpad != kC || g.Cppad != kC) return pl;
-  if (g.W % 4 != 0 || g.m != 4) return pl;
+  // the branch-free window loads assume pad_lo = 1 and 16-byte aligned rows (W % 4 == 0)
+  if (g.W % 4 != 0 || g.m != 4 || g.pad_lo != 1 || g.W < 8) return pl;
   const int trows = ceil_div(kFT - 1, g.tiles_x) + 1;
   pl.plane = round_up(trows * kT * g.W, 32) + 16;
   if (static_cast<size_t>(kCPC) * pl.plane * 4 > kFISlot) return pl;
@@ -569,17 +663,32 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.plane = pl.plane;
   P.n_fi = g.n_blk * (ws::kNCG + ws::kNIG);
   P.grid = sm_count;
+  P.prof = 0;
+  if (const char* e = getenv("WF_WS_PROF")) P.prof = atoi(e);
   cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
   if (e != cudaSuccess) return e;
   static bool attr = false;
   if (!attr) {
-    e = cudaFuncSetAttribute(ws::fused_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ws::kSmem);
+    e = cudaFuncSetAttribute(ws::fused_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ws::fused_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   note_launch();
-  ws::fused_ws_kernel<<<sm_count, ws::NT, ws::kSmem, st>>>(P);
+  if (P.prof) ws::fused_ws_kernel<true><<<sm_count, ws::NT, ws::kSmem, st>>>(P);
+  else ws::fused_ws_kernel<false><<<sm_count, ws::NT, ws::kSmem, st>>>(P);
   return cudaGetLastError();
 }
 
 }  // namespace wf
+
+// Debug/tuning hook (not part of the public ABI): copy the per-CTA role
+// accounting of the warp-specialised kernel ([cta][32] u64) and reset it.
+extern "C" int wf_debug_ws_profile(unsigned long long* host, int n) {
+  const int cnt = n < 1024 * wf::ws::kProfSlots ? n : 1024 * wf::ws::kProfSlots;
+  cudaError_t e = cudaMemcpyFromSymbol(host, wf::ws::g_wsprof, cnt * sizeof(unsigned long long));
+  static unsigned long long zeros[1024 * wf::ws::kProfSlots] = {0};
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(wf::ws::g_wsprof, zeros, sizeof(zeros));
+  return e == cudaSuccess ? 0 : 4;
+}

@@ -1,0 +1,49 @@
+"""Per-role accounting of the warp-specialised fused kernel (WF_WS_PROF=1) on c2.
+
+    python tools/ws_prof.py [config] [env=val ...]
+"""
+import ctypes, os, sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+os.environ["WF_WS_PROF"] = "1"
+for kv in sys.argv[2:]:
+    k, v = kv.split("=")
+    os.environ[k] = v
+import paper_1912_02165_b200 as wf
+from paper_1912_02165_b200 import _lib
+from bench import layer_inputs
+spec, t, x, w = layer_inputs(sys.argv[1] if len(sys.argv) > 1 else "c2")
+dev = torch.device("cuda", 0)
+pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
+plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=t, device=dev))
+xd = torch.from_numpy(x).to(dev)
+lib = _lib.load()
+N = 1024 * 32
+buf = (ctypes.c_ulonglong * N)()
+lib.wf_debug_ws_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+names = ["G-prod dep wait", "G-prod stage wait", "G-issue full wait", "G-issue tempty wait", "G-epi tfull wait",
+         "G-epi busy", "FI-prod dep wait", "FI-prod slot wait", "FI-work full wait", "FI-work F busy",
+         "FI-work I busy", "publish fence"]
+extra = {21: "FI-work loop total"}
+clk = 1.9e3
+for it in range(3):
+    flush.zero_()
+    torch.cuda.synchronize()
+    lib.wf_debug_ws_profile(buf, N)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); plan(xd); e1.record(); torch.cuda.synchronize()
+    lib.wf_debug_ws_profile(buf, N)
+    a = np.array(buf[:], dtype=np.float64).reshape(1024, 32)
+    ctas = int((a[:, 12] > 0).sum())
+    a = a[:ctas]
+    print(f"step {it}: {e0.elapsed_time(e1)*1e3:.1f} us, {ctas} CTAs, F units/CTA {a[:, 19].mean():.1f}, I {a[:, 20].mean():.1f}")
+    for k, nm in enumerate(names):
+        print(f"   {nm:22s} avg {a[:, k].mean()/clk:7.2f} us  max {a[:, k].max()/clk:7.2f}")
+    for k, nm in extra.items():
+        print(f"   {nm:22s} avg {a[:, k].mean()/clk:7.2f} us  max {a[:, k].max()/clk:7.2f}")
+    st = a[:, 12].min()
+    for k, nm in zip(range(13, 19), ["G-prod", "G-issue", "G-epi", "FI-prod", "FI-work", "publisher"]):
+        e = (a[:, k] - st) / 1e3
+        print(f"   end {nm:10s} min {e.min():7.1f} med {np.median(e):7.1f} max {e.max():7.1f} us")
