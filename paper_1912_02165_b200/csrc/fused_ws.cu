@@ -37,8 +37,13 @@ constexpr int NT = 512;
 constexpr int kC = 64;                                   // C = C' = Cpad = Cppad
 constexpr int kT = 6;
 constexpr int kP = kT * kT;
-constexpr int kGP = 4;                                   // positions per G unit
-constexpr int kNGG = kP / kGP;                           // 9 G units per block
+#ifndef WF_WS_GP
+#define WF_WS_GP 1
+#endif
+constexpr int kGP = WF_WS_GP;                            // positions per G unit
+constexpr int kNGG = kP / kGP;                           // G units per block
+constexpr int kNAcc = 512 / (kGP * kC);                  // TMEM accumulator buffers (units in flight)
+static_assert(kP % kGP == 0 && kNAcc >= 2, "G unit shape");
 constexpr int kCPC = 8;                                  // channels per F unit
 constexpr int kFT = 64;                                  // tiles per F unit
 constexpr int kNCG = (kBlockTiles / kFT) * (kC / kCPC);  // 16 F units per block
@@ -69,6 +74,7 @@ struct Params {
   Geo g;
   int NU, NM, L2;
   int passes;
+  int discard;            // drop consumed U / M ring lines from L2 (WF_WS_DISCARD, default on)
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
   int grid;
@@ -88,7 +94,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-__shared__ unsigned long long s_prof[kProfSlots];   // accumulated in smem, flushed at exit
+__shared__ unsigned long long s_prof[kProfSlots];
+// per-block event times (ns, PROF build): F first start / last end, G first
+// start (deps satisfied) / last end, I first start / last end
+constexpr int kTraceBlocks = 4096;
+__device__ unsigned long long g_wstrace[kTraceBlocks * 8];
+template <bool ON>
+__device__ __forceinline__ void trace(int b, int ev, bool is_min) {
+  if (!ON || b >= kTraceBlocks) return;
+  const unsigned long long t = gtimer();
+  if (is_min) atomicMin(&g_wstrace[b * 8 + ev], t);
+  else atomicMax(&g_wstrace[b * 8 + ev], t);
+}   // accumulated in smem, flushed at exit
 // Compiled in only for the profiling instantiation of the kernel.
 template <bool ON>
 struct ProfT {
@@ -103,9 +120,13 @@ struct ProfT {
 struct Sync {
   uint64_t a_full[kAStages], a_empty[kAStages];
   uint64_t b_full[2], b_empty[2];
-  uint64_t tfull[2][kGP], tempty[2];
+  uint64_t tfull[kNAcc][kGP], tempty[kNAcc];
   uint64_t fi_full[2], fi_empty[2];
-  int fi_cnt, g_cnt;       // completed F/I (x8 warps) and G (x4 warps) units of this CTA
+  // completion counts: F/I unit k adds 8 (one per worker warp) to fi_cnt[k % 4],
+  // G unit k adds 4 (one per epilogue warp) to g_cnt[k % kNAcc].  A warp can
+  // not get a full counter ring ahead of another (the F/I slot ring and the
+  // TMEM buffer ring block it first), so each count is attributed to its unit.
+  int fi_cnt[4], g_cnt[kNAcc];
   uint32_t tmem;
 };
 
@@ -142,6 +163,12 @@ __device__ __forceinline__ int atom_acqrel_cta_smem(int* p, int v) {
   int old;
   asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
   return old;
+}
+// Invalidate one 128-byte L2 line without write-back: ring data that its
+// single consumer has copied into shared memory is dead, so it should
+// neither cost a DRAM write-back nor push live ring lines out of L2.
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -263,6 +290,14 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
     pf.add(kFWWait, t0);
     t0 = pf.now();
+    if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
+    if (kind == 2 && P.discard) {
+      // the unit's 36 x 2 KB of M are in smem now: 576 dead lines, ~2 per thread
+      const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * kMSlot +
+                            static_cast<size_t>(2 * sub) * kBlockTiles * 8;
+      for (int i = wtid; i < kP * (kIPos / 128); i += 256)
+        discard_l2(msrc + (i >> 4) * kMPos + (i & 15) * 128);
+    }
     if (kind == 0) {
       // ---- F(b, sub): thread = (tile tl, channel pair q); a warp = 8 tiles
       // (one core-matrix row group) x 4 pairs (one 8-channel k group), so
@@ -374,7 +409,8 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       }
     }
     __syncwarp();
-    if (lane == 0) red_release_cta_smem(&sy.fi_cnt, 1);
+    if (lane == 0) red_release_cta_smem(&sy.fi_cnt[it & 3], 1);
+    if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 1 : 5, false);
     pf.add(kind == 0 ? kFWF : kFWI, t0);
     pf.inc(kind == 0 ? kNF : kNI);
   }
@@ -396,6 +432,7 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
     spin_until(doneF + b, kNCG);                                   // U complete
     if (b >= P.NM) spin_until(doneI + (b - P.NM), kNIG);           // M slot free
     pf.add(kGPDep, t0);
+    trace<PROF>(b, 2, true);
     fence_proxy_async_global();
     const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * kUSlot;
     for (int pl = 0; pl < kGP; ++pl) {
@@ -428,13 +465,18 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
 // ---------------------------------------------------------------- G issuer
 template <bool PROF>
 __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
+  // the whole warp runs the loop (its lanes drop the consumed U lines from
+  // L2); lane 0 issues the MMAs
+  const int lane = threadIdx.x & 31;
   const uint32_t idesc = idesc_bf16(kBlockTiles, kC);
   const ProfT<PROF> pf(P.prof);
   int a_it = 0, b_it = 0, k = 0;
   for (int v = blockIdx.x; v < n_g; v += P.grid, ++k) {
-    const int buf = k & 1;
+    const int buf = k % kNAcc;
+    const int b = v / kNGG, gg = v - b * kNGG;
+    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * kUSlot;
     long long t0 = pf.now();
-    mbar_wait(&sy.tempty[buf], ((k >> 1) & 1) ^ 1);
+    mbar_wait(&sy.tempty[buf], ((k / kNAcc) & 1) ^ 1);
     pf.add(kGITempty, t0);
     tc_fence_after();
     for (int pl = 0; pl < kGP; ++pl) {
@@ -450,6 +492,17 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
         mbar_wait(&sy.a_full[st], (a_it / kAStages) & 1);
         pf.add(kGIFull, t2);
         tc_fence_after();
+        if (P.discard) {
+          // the stage's hi and lo half-K blocks (2 x 8 KB = 128 lines) are in smem now
+          const uint8_t* asrc = uslot + (gg * kGP + pl) * kUPos + kb * kAHalf;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            discard_l2(asrc + (lane + 32 * i) * 128);
+            discard_l2(asrc + 2 * kAHalf + (lane + 32 * i) * 128);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
         const uint32_t sa = smem_u32(smem + st * kAStage);
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
@@ -467,10 +520,15 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
           }
         }
         mma_commit(&sy.a_empty[st]);
+        }
+        __syncwarp();
         ++a_it;
       }
-      mma_commit(&sy.b_empty[pb]);
-      mma_commit(&sy.tfull[buf][pl]);
+      if (lane == 0) {
+        mma_commit(&sy.b_empty[pb]);
+        mma_commit(&sy.tfull[buf][pl]);
+      }
+      __syncwarp();
       ++b_it;
     }
   }
@@ -486,12 +544,12 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
   int k = 0;
   for (int v = blockIdx.x; v < n_g; v += P.grid, ++k) {
     const int b = v / kNGG, gg = v - b * kNGG;
-    const int buf = k & 1;
+    const int buf = k % kNAcc;
     const bool live = b * kBlockTiles + row < P.g.n_tile;
     float* mslot = P.mring + static_cast<size_t>(b % P.NM) * (kMSlot / 4);
     for (int pl = 0; pl < kGP; ++pl) {
       long long t0 = pf.now();
-      mbar_wait(&sy.tfull[buf][pl], (k >> 1) & 1);
+      mbar_wait(&sy.tfull[buf][pl], (k / kNAcc) & 1);
       pf.add(kGEWait, t0);
       t0 = pf.now();
       tc_fence_after();
@@ -512,13 +570,16 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
-      mbar_arrive(&sy.tempty[buf]);
-      // the last of the 4 epilogue warps to finish publishes the unit
-      if (atom_acqrel_cta_smem(&sy.g_cnt, 1) == 4 * k + 3) {
+      // the last of the 4 epilogue warps to finish publishes the unit (counted
+      // before the buffer is released, so no warp can count a later use of
+      // this buffer first)
+      if (atom_acqrel_cta_smem(&sy.g_cnt[buf], 1) == 4 * (k / kNAcc) + 3) {
         const long long t1 = pf.now();
         red_release_gpu(P.counters + P.g.n_blk + b, 1);
+        trace<PROF>(b, 3, false);
         pf.add(kPubFence, t1);
       }
+      mbar_arrive(&sy.tempty[buf]);
     }
   }
   pf.end(kEndGE);
@@ -538,7 +599,7 @@ __device__ void publisher(const Params& P, Sync& sy, int n_g) {
   int vg = blockIdx.x, kg = 0;        // next G unit, its ordinal
   while (uf < P.n_fi) {
     bool progress = false;
-    if (uf < P.n_fi && ld_acquire_cta_smem(&sy.fi_cnt) >= 8 * (kf + 1)) {
+    if (uf < P.n_fi && ld_acquire_cta_smem(&sy.fi_cnt[kf & 3]) >= 8 * ((kf >> 2) + 1)) {
       int kind, b, sub;
       wk.decode(P, uf, kind, b, sub);
       const long long t0 = pf.now();
@@ -564,13 +625,15 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sy.b_full[s], 1);
       mbar_init(&sy.b_empty[s], 1);
-      for (int p = 0; p < kGP; ++p) mbar_init(&sy.tfull[s][p], 1);
-      mbar_init(&sy.tempty[s], 4);
       mbar_init(&sy.fi_full[s], 1);
       mbar_init(&sy.fi_empty[s], 8);
     }
-    sy.fi_cnt = 0;
-    sy.g_cnt = 0;
+    for (int s = 0; s < kNAcc; ++s) {
+      for (int p = 0; p < kGP; ++p) mbar_init(&sy.tfull[s][p], 1);
+      mbar_init(&sy.tempty[s], 4);
+    }
+    for (int i = 0; i < 4; ++i) sy.fi_cnt[i] = 0;
+    for (int i = 0; i < kNAcc; ++i) sy.g_cnt[i] = 0;
     for (int i = 0; i < kProfSlots; ++i) s_prof[i] = 0;
     if (PROF) g_wsprof[blockIdx.x * kProfSlots + kStart] = gtimer();
     fence_mbar_init();
@@ -583,7 +646,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   if (warp == 0) {
     if (lane_id() == 0) g_producer<PROF>(P, smem, sy, n_g);
   } else if (warp == 1) {
-    if (lane_id() == 0) g_issuer<PROF>(P, smem, sy, n_g);
+    g_issuer<PROF>(P, smem, sy, n_g);
   } else if (warp == 2) {
     fi_producer<PROF>(P, smem, sy);
   } else if (warp == 3) {
@@ -660,6 +723,8 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.g = g;
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
+  P.discard = 0;   // measured neutral-to-slower on c2
+  if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.plane = pl.plane;
   P.n_fi = g.n_blk * (ws::kNCG + ws::kNIG);
   P.grid = sm_count;
@@ -690,5 +755,17 @@ extern "C" int wf_debug_ws_profile(unsigned long long* host, int n) {
   cudaError_t e = cudaMemcpyFromSymbol(host, wf::ws::g_wsprof, cnt * sizeof(unsigned long long));
   static unsigned long long zeros[1024 * wf::ws::kProfSlots] = {0};
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(wf::ws::g_wsprof, zeros, sizeof(zeros));
+  return e == cudaSuccess ? 0 : 4;
+}
+
+extern "C" int wf_debug_ws_trace(unsigned long long* host, int n_blocks, int reset) {
+  const int cnt = (n_blocks < wf::ws::kTraceBlocks ? n_blocks : wf::ws::kTraceBlocks) * 8;
+  cudaError_t e = cudaMemcpyFromSymbol(host, wf::ws::g_wstrace, cnt * sizeof(unsigned long long));
+  if (reset) {
+    static unsigned long long init[wf::ws::kTraceBlocks * 8];
+    for (int b = 0; b < wf::ws::kTraceBlocks; ++b)
+      for (int k = 0; k < 8; ++k) init[b * 8 + k] = (k % 2 == 0) ? ~0ull : 0ull;
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(wf::ws::g_wstrace, init, sizeof(init));
+  }
   return e == cudaSuccess ? 0 : 4;
 }

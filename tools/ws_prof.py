@@ -47,3 +47,20 @@ for it in range(3):
     for k, nm in zip(range(13, 19), ["G-prod", "G-issue", "G-epi", "FI-prod", "FI-work", "publisher"]):
         e = (a[:, k] - st) / 1e3
         print(f"   end {nm:10s} min {e.min():7.1f} med {np.median(e):7.1f} max {e.max():7.1f} us")
+
+# per-block event trace of the last step (ns): F start/end, G start/end, I start/end
+tr = (ctypes.c_ulonglong * (4096 * 8))()
+lib.wf_debug_ws_trace.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+lib.wf_debug_ws_trace(tr, 4096, 1)
+flush.zero_(); torch.cuda.synchronize()
+plan(xd); torch.cuda.synchronize()
+lib.wf_debug_ws_trace(tr, 4096, 1)
+nb = -(-(spec.batch * -(-spec.out_height // (t - 2)) * -(-spec.out_width // (t - 2))) // 128)
+a = np.array(tr[:nb * 8], dtype=np.float64).reshape(nb, 8)
+t0 = a[:, 0].min()
+a = (a - t0) / 1e3
+print("block  Fstart  Fend  Gstart  Gend  Istart  Iend   (us)   G-F  I-G")
+for b in list(range(0, nb, max(1, nb // 16))) + [nb - 1]:
+    r = a[b]
+    print(f"{b:5d} {r[0]:7.1f} {r[1]:6.1f} {r[2]:6.1f} {r[3]:6.1f} {r[4]:7.1f} {r[5]:6.1f}   {r[3]-r[1]:5.1f} {r[4]-r[3]:5.1f}")
+print(f"median Gend-Fend {np.median(a[:,3]-a[:,1]):.1f} us, Gstart-Fend {np.median(a[:,2]-a[:,1]):.1f}, Istart-Gend {np.median(a[:,4]-a[:,3]):.1f}, Fend-Fstart {np.median(a[:,1]-a[:,0]):.1f}, Iend-Istart {np.median(a[:,5]-a[:,4]):.1f}")
