@@ -679,13 +679,15 @@ static Plan plan(const Geo& g) {
   const int trows = ceil_div(kFT - 1, g.tiles_x) + 1;
   pl.plane = round_up(trows * kT * g.W, 32) + 16;
   if (static_cast<size_t>(kCPC) * pl.plane * 4 > kFISlot) return pl;
-  size_t budget = 150ull << 20;
+  // measured on c2 (tools/ws_time.py): rings of 300 MB (slightly past L2)
+  // with the I units 44 steps behind their F units are best (94 us)
+  size_t budget = 300ull << 20;
   if (const char* e = getenv("WF_WS_BUDGET_MB")) budget = static_cast<size_t>(atoi(e)) << 20;
   int slots = static_cast<int>(budget / (kUSlot + kMSlot));
   if (slots < 4) slots = 4;
   pl.NU = std::min(slots / 2, g.n_blk);
   pl.NM = std::min(slots - slots / 2, g.n_blk);
-  int lag = 24;
+  int lag = 44;
   if (const char* e = getenv("WF_WS_LAG")) lag = atoi(e);
   // deadlock freedom: some L1 with 1 <= L1 < NU (when F waits on G) and L2 - L1 < NM
   const int lmax = (pl.NU >= g.n_blk ? g.n_blk + pl.NM : pl.NU + pl.NM - 2);

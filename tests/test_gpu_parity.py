@@ -297,3 +297,30 @@ def test_randomized_sweep_like_reference_acceptance():
         worst = max(worst, err)
         assert err <= TOL[t], (i, t, spec, err)
     assert worst > 0.0
+
+
+@pytest.mark.parametrize("dims", [(3, 64, 64, 56, 56, 3, 1, 1),     # 588 tiles: a partial last block
+                                  (2, 64, 64, 28, 36, 3, 1, 1),     # non-square, 7 x 9 tiles per image
+                                  (5, 64, 64, 12, 8, 3, 1, 1),      # tiny images, several per F unit
+                                  (16, 64, 64, 56, 56, 3, 1, 1)])   # 25 blocks: ring reuse
+def test_warp_specialised_kernel(dims, monkeypatch):
+    """The warp-specialised fused kernel (F(4x4,3x3), C = C' = 64, W % 4 == 0,
+    pad 1 -- the c2 benchmark layer) against three-stage (bitwise), the
+    item-queue persistent kernel (WF_WS=0, bitwise) and FP64 direct.  Small
+    rings (WF_WS_BUDGET_MB) force slot reuse and the lagged dependencies."""
+    spec = wf.LayerSpec(*dims)
+    rng = np.random.default_rng(sum(dims))
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
+    s, _ = _run("three_stage", x, pack, spec, 6)
+    ref = O.direct_conv_f64(x, w, spec)
+    for budget in ("300", "12"):
+        monkeypatch.setenv("WF_WS_BUDGET_MB", budget)
+        f, _ = _run("fused", x, pack, spec, 6)
+        assert np.array_equal(f, s), (dims, budget)
+        assert O.max_rel_error(f, ref) <= TOL[6], (dims, budget)
+    monkeypatch.setenv("WF_WS", "0")
+    monkeypatch.setenv("WF_PERSIST_MIN_BLOCKS", "1")
+    q, _ = _run("fused", x, pack, spec, 6)
+    assert np.array_equal(q, s), dims
