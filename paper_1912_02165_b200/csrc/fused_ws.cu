@@ -37,6 +37,9 @@ constexpr int NT = 512;
 constexpr int kC = 64;                                   // C = C' = Cpad = Cppad
 constexpr int kT = 6;
 constexpr int kP = kT * kT;
+#ifndef WF_WS_FSCALAR
+#define WF_WS_FSCALAR 0   // measured: more instructions and spills than the f32x2 path
+#endif
 #ifndef WF_WS_GP
 #define WF_WS_GP 1
 #endif
@@ -309,6 +312,58 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       const int tl = wl * 8 + (lane & 7), q = lane >> 3;
       const int tile = t0 + tl;
       const bool live = tile < g.n_tile;
+#if WF_WS_FSCALAR
+      // scalar f32 arithmetic, one channel at a time: the two channels of the
+      // pair come from different 16-byte loads, and packing them into f32x2
+      // register pairs costs a move per operand (per element the same
+      // operations and rounding as forward_transform2<6>)
+      float wa[kT][kT], wb[kT][kT];
+      if (live) {
+        const int per_img = g.tiles_y * g.tiles_x;
+        const int bi = tile / per_img;
+        const int rem = tile - bi * per_img;
+        const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+        const int j = bi * g.tiles_y + ty - gr0;
+        const int x0 = tx * g.m - g.pad_lo;
+        const float* pa = reinterpret_cast<const float*>(src) + (2 * q) * P.plane + j * kT * g.W + x0;
+        const float* pb = pa + P.plane;
+        const bool lo_ok = x0 >= 0, hi_ok = x0 + kT <= g.W;
+#pragma unroll
+        for (int r = 0; r < kT; ++r) {
+          const float* ra = pa + r * g.W - 3;
+          const float* rb = pb + r * g.W - 3;
+          const float4 a0 = *reinterpret_cast<const float4*>(ra), a1 = *reinterpret_cast<const float4*>(ra + 4);
+          const float4 b0 = *reinterpret_cast<const float4*>(rb), b1 = *reinterpret_cast<const float4*>(rb + 4);
+          const float a5 = ra[8], b5 = rb[8];
+          wa[r][0] = lo_ok ? a0.w : 0.0f; wa[r][1] = a1.x; wa[r][2] = a1.y; wa[r][3] = a1.z; wa[r][4] = a1.w;
+          wa[r][5] = hi_ok ? a5 : 0.0f;
+          wb[r][0] = lo_ok ? b0.w : 0.0f; wb[r][1] = b1.x; wb[r][2] = b1.y; wb[r][3] = b1.z; wb[r][4] = b1.w;
+          wb[r][5] = hi_ok ? b5 : 0.0f;
+          bt6_line<ScalarOps>(wa[r][0], wa[r][1], wa[r][2], wa[r][3], wa[r][4], wa[r][5]);
+          bt6_line<ScalarOps>(wb[r][0], wb[r][1], wb[r][2], wb[r][3], wb[r][4], wb[r][5]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window consumed: slot free
+      if (live) {
+        const int row = tb0 + tl, c0 = cg * kCPC + 2 * q;
+        uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * kUSlot + (c0 >> 5) * kAHalf +
+                       (row >> 3) * 512 + ((c0 & 31) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2;
+#pragma unroll
+        for (int s = 0; s < kT; ++s) {
+          bt6_line<ScalarOps>(wa[0][s], wa[1][s], wa[2][s], wa[3][s], wa[4][s], wa[5][s]);
+          bt6_line<ScalarOps>(wb[0][s], wb[1][s], wb[2][s], wb[3][s], wb[4][s], wb[5][s]);
+#pragma unroll
+          for (int r = 0; r < kT; ++r) {
+            uint32_t hi, lo;
+            split_bf16x2(wa[r][s], wb[r][s], hi, lo);
+            uint8_t* p = dst + (r * kT + s) * kUPos;
+            *reinterpret_cast<uint32_t*>(p) = hi;
+            *reinterpret_cast<uint32_t*>(p + 2 * kAHalf) = lo;
+          }
+        }
+      }
+#else
       float2 w[kT][kT];
       if (live) {
         const int per_img = g.tiles_y * g.tiles_x;
@@ -362,6 +417,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           }
         }
       }
+#endif
     } else {
       // ---- I(b, sub): thread = (tile, c' pair); 36 staged float2 per thread
       const int tl = wtid & (kBlockTiles - 1), pr = wtid >> 7;
