@@ -78,7 +78,6 @@ struct Params {
   int NU, NM, L2;
   int passes;
   int discard;            // drop consumed U / M ring lines from L2 (WF_WS_DISCARD, default off)
-  int l2pol;              // L2 policies (WF_WS_L2POL bits): 1 input evict_first, 2 output evict_first, 4 rings evict_last
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
   int grid;
@@ -174,37 +173,6 @@ __device__ __forceinline__ int atom_acqrel_cta_smem(int* p, int v) {
 __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
-// L2 residency policies: the input and the output stream through once; the
-// U / M rings are what should stay in L2 (WF_WS_L2POL selects, see plan).
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
-                                              uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void st_hint_u32(void* p, uint32_t v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint_f2(void* p, float2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint_f4(void* p, float4 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w), "l"(pol)
-               : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -285,12 +253,8 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
         if (yb > ya) {
           const uint32_t bytes = static_cast<uint32_t>((yb - ya) * g.W * 4);
           mbar_add_tx(&sy.fi_full[slot], bytes);
-          if (P.l2pol & 1)
-            bulk_g2s_hint(dst + (ya - y0) * g.W, P.x + ((static_cast<size_t>(bi) * g.C + c) * g.H + ya) * g.W, bytes,
-                          &sy.fi_full[slot], policy_evict_first());
-          else
-            bulk_g2s(dst + (ya - y0) * g.W, P.x + ((static_cast<size_t>(bi) * g.C + c) * g.H + ya) * g.W, bytes,
-                     &sy.fi_full[slot]);
+          bulk_g2s(dst + (ya - y0) * g.W, P.x + ((static_cast<size_t>(bi) * g.C + c) * g.H + ya) * g.W, bytes,
+                   &sy.fi_full[slot]);
         }
         for (int r = 0; r < kT; ++r)
           if (r < ya - y0 || r >= yb - y0)
@@ -448,14 +412,8 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
             uint32_t hi, lo;
             split_bf16x2(w[r][s], hi, lo);
             uint8_t* p = dst + (r * kT + s) * kUPos;
-            if (P.l2pol & 4) {
-              const uint64_t pol = policy_evict_last();
-              st_hint_u32(p, hi, pol);
-              st_hint_u32(p + 2 * kAHalf, lo, pol);
-            } else {
-              *reinterpret_cast<uint32_t*>(p) = hi;
-              *reinterpret_cast<uint32_t*>(p + 2 * kAHalf) = lo;
-            }
+            *reinterpret_cast<uint32_t*>(p) = hi;
+            *reinterpret_cast<uint32_t*>(p + 2 * kAHalf) = lo;
           }
         }
       }
@@ -493,14 +451,8 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           float2 o[MO];
           at6_line<PairOps>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], o[0], o[1], o[2], o[3]);
           if (vec) {
-            if (P.l2pol & 2) {
-              const uint64_t pol = policy_evict_first();
-              st_hint_f4(ybase + r * g.Wo, make_float4(o[0].x, o[1].x, o[2].x, o[3].x), pol);
-              st_hint_f4(ybase + plane + r * g.Wo, make_float4(o[0].y, o[1].y, o[2].y, o[3].y), pol);
-            } else {
-              *reinterpret_cast<float4*>(ybase + r * g.Wo) = make_float4(o[0].x, o[1].x, o[2].x, o[3].x);
-              *reinterpret_cast<float4*>(ybase + plane + r * g.Wo) = make_float4(o[0].y, o[1].y, o[2].y, o[3].y);
-            }
+            *reinterpret_cast<float4*>(ybase + r * g.Wo) = make_float4(o[0].x, o[1].x, o[2].x, o[3].x);
+            *reinterpret_cast<float4*>(ybase + plane + r * g.Wo) = make_float4(o[0].y, o[1].y, o[2].y, o[3].y);
           } else if (oy + r < g.Ho) {
 #pragma unroll
             for (int c = 0; c < MO; ++c)
@@ -666,10 +618,7 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
         tmem_ld_wait();
         if (live) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (P.l2pol & 4) st_hint_f2(mrow + (c / 2 + i) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]), policy_evict_last());
-            else __stcg(mrow + (c / 2 + i) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]));
-          }
+          for (int i = 0; i < 8; ++i) __stcg(mrow + (c / 2 + i) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]));
         }
       }
       pf.add(kGEBusy, t0);
@@ -833,8 +782,6 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
   P.discard = 0;   // measured neutral-to-slower on c2
-  P.l2pol = 0;
-  if (const char* e = getenv("WF_WS_L2POL")) P.l2pol = atoi(e);
   if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.plane = pl.plane;
   P.n_fi = g.n_blk * (ws::kNCG + ws::kNIG);
