@@ -80,8 +80,6 @@ struct Params {
   int discard;            // drop consumed U / M ring lines from L2 (WF_WS_DISCARD, default off)
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
-  int dbg;                // tuning aid (WF_WS_DBG): 3 = no GEMM work (results invalid)
-  int dyn;                // 1: F/I units handed out by a global atomic counter (in queue order)
   int grid;
   int prof;
 };
@@ -132,12 +130,6 @@ struct Sync {
   // not get a full counter ring ahead of another (the F/I slot ring and the
   // TMEM buffer ring block it first), so each count is attributed to its unit.
   int fi_cnt[4], g_cnt[kNAcc];
-  // dynamic F/I queue (WF_WS_DYN): the producer takes unit indices from a
-  // global counter and passes them to the workers and the publisher through
-  // this ring (fi_made = units handed over, fi_pub = units published; the
-  // producer stays less than 8 ahead of the publisher); index -1 ends the queue
-  int fi_desc[8];
-  int fi_made, fi_pub;
   uint32_t tmem;
 };
 
@@ -222,32 +214,8 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
   const ProfT<PROF> pf(P.prof && lane == 0);
   FIWalker wk;
   wk.init(P);
-  int* head = P.counters + 3 * g.n_blk;               // dynamic queue head
-  int next = 0;
-  if (P.dyn && lane == 0) next = atomicAdd(head, 1);
   int it = 0;
-  for (int u = blockIdx.x;; ++it) {
-    if (P.dyn) {
-      // the index of the unit after this one is fetched now: its round trip
-      // overlaps this unit's dependency wait and copies
-      if (lane == 0) {
-        u = next;
-        if (u < P.n_fi) next = atomicAdd(head, 1);
-      }
-      u = __shfl_sync(0xffffffffu, u, 0);
-      if (u >= P.n_fi) {
-        if (lane == 0) {
-          while (ld_acquire_cta_smem(&sy.fi_pub) < it - 6) __nanosleep(32);
-          sy.fi_desc[it & 7] = -1;
-          red_release_cta_smem(&sy.fi_made, 1);
-          mbar_wait(&sy.fi_empty[it & 1], ((it >> 1) & 1) ^ 1);
-          mbar_arrive(&sy.fi_full[it & 1]);            // wakes the workers: end of queue
-        }
-        break;
-      }
-    } else if (u >= P.n_fi) {
-      break;
-    }
+  for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
     int kind, b, sub;
     wk.decode(P, u, kind, b, sub);
     const int slot = it & 1;
@@ -263,11 +231,6 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       pf.add(kFPDep, t0);
       t0 = pf.now();
       mbar_wait(&sy.fi_empty[slot], ((it >> 1) & 1) ^ 1);
-      if (P.dyn) {
-        while (ld_acquire_cta_smem(&sy.fi_pub) < it - 6) __nanosleep(32);   // descriptor ring
-        sy.fi_desc[it & 7] = u;
-        red_release_cta_smem(&sy.fi_made, 1);
-      }
       pf.add(kFPSlot, t0);
     }
     __syncwarp();
@@ -295,7 +258,8 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
         }
         for (int r = 0; r < kT; ++r)
           if (r < ya - y0 || r >= yb - y0)
-            for (int s2 = 0; s2 < g.W; ++s2) dst[r * g.W + s2] = 0.0f;
+            for (int s2 = 0; s2 < g.W; s2 += 4)          // W % 4 == 0: 16-byte aligned rows
+              *reinterpret_cast<float4*>(dst + r * g.W + s2) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
     } else {
       const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * kMSlot +
@@ -307,7 +271,6 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
-    if (!P.dyn) u += P.grid;
   }
   pf.end(kEndFP);
 }
@@ -322,17 +285,14 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
   FIWalker wk;
   wk.init(P);
   int it = 0;
-  for (int u = blockIdx.x;; ++it) {
-    if (!P.dyn && u >= P.n_fi) break;
+  for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
+    int kind, b, sub;
+    wk.decode(P, u, kind, b, sub);
     const int slot = it & 1;
     const uint8_t* src = smem + kOffFI + slot * kFISlot;
     long long t0 = pf.now();
     mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
     pf.add(kFWWait, t0);
-    if (P.dyn) u = sy.fi_desc[it & 7];
-    if (u < 0 || u >= P.n_fi) break;
-    int kind, b, sub;
-    wk.decode(P, u, kind, b, sub);
     t0 = pf.now();
     if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
     if (kind == 2 && P.discard) {
@@ -439,12 +399,18 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window consumed: slot free
-      if (live) {
+      {
         // columns: B^T down each column, then one column of positions
-        // (r, s), r = 0..5, split and stored (== forward_transform2<6>)
-        const int row = tb0 + tl, c0 = cg * kCPC + 2 * q;
+        // (r, s), r = 0..5, split (== forward_transform2<6>) and stored.
+        // Lanes q and q^1 (same tile, neighbouring channel pairs) swap
+        // halves so that the even one stores 4 channels of hi and the odd
+        // one 4 channels of lo: one 8-byte store per position instead of
+        // two 4-byte ones (a warp still writes whole core-matrix rows).
+        const bool odd = q & 1;
+        const int row = tb0 + tl, c0 = cg * kCPC + 2 * (q & ~1);
         uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * kUSlot + (c0 >> 5) * kAHalf +
-                       (row >> 3) * 512 + ((c0 & 31) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2;
+                       (row >> 3) * 512 + ((c0 & 31) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
+                       (odd ? 2 * kAHalf : 0);
 #pragma unroll
         for (int s = 0; s < kT; ++s) {
           bt6_line<PairOps>(w[0][s], w[1][s], w[2][s], w[3][s], w[4][s], w[5][s]);
@@ -452,9 +418,9 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           for (int r = 0; r < kT; ++r) {
             uint32_t hi, lo;
             split_bf16x2(w[r][s], hi, lo);
-            uint8_t* p = dst + (r * kT + s) * kUPos;
-            *reinterpret_cast<uint32_t*>(p) = hi;
-            *reinterpret_cast<uint32_t*>(p + 2 * kAHalf) = lo;
+            const uint32_t other = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 8);
+            if (live)
+              *reinterpret_cast<uint2*>(dst + (r * kT + s) * kUPos) = odd ? make_uint2(other, lo) : make_uint2(hi, other);
           }
         }
       }
@@ -507,7 +473,6 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     }
     __syncwarp();
     if (lane == 0) red_release_cta_smem(&sy.fi_cnt[it & 3], 1);
-    if (!P.dyn) u += P.grid;
     if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 1 : 5, false);
     pf.add(kind == 0 ? kFWF : kFWI, t0);
     pf.inc(kind == 0 ? kNF : kNI);
@@ -695,23 +660,15 @@ __device__ void publisher(const Params& P, Sync& sy, int n_g) {
   wk.init(P);
   int uf = blockIdx.x, kf = 0;        // next F/I unit of this CTA, its ordinal
   int vg = blockIdx.x, kg = 0;        // next G unit, its ordinal
-  for (;;) {
-    if (P.dyn) {
-      while (ld_acquire_cta_smem(&sy.fi_made) <= kf) __nanosleep(32);
-      uf = sy.fi_desc[kf & 7];
-      if (uf < 0) break;
-    } else if (uf >= P.n_fi) {
-      break;
-    }
+  while (uf < P.n_fi) {
     bool progress = false;
-    if (ld_acquire_cta_smem(&sy.fi_cnt[kf & 3]) >= 8 * ((kf >> 2) + 1)) {
+    if (uf < P.n_fi && ld_acquire_cta_smem(&sy.fi_cnt[kf & 3]) >= 8 * ((kf >> 2) + 1)) {
       int kind, b, sub;
       wk.decode(P, uf, kind, b, sub);
       const long long t0 = pf.now();
       red_release_gpu((kind == 0 ? doneF : doneI) + b, 1);
       pf.add(kPubFence, t0);
-      if (P.dyn) red_release_cta_smem(&sy.fi_pub, 1);
-      else uf += P.grid;
+      uf += P.grid;
       ++kf;
       progress = true;
     }
@@ -739,8 +696,6 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
       mbar_init(&sy.tempty[s], 4);
     }
     for (int i = 0; i < 4; ++i) sy.fi_cnt[i] = 0;
-    sy.fi_made = 0;
-    sy.fi_pub = 0;
     for (int i = 0; i < kNAcc; ++i) sy.g_cnt[i] = 0;
     for (int i = 0; i < kProfSlots; ++i) s_prof[i] = 0;
     if (PROF) g_wsprof[blockIdx.x * kProfSlots + kStart] = gtimer();
@@ -751,19 +706,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   __syncthreads();
   tc_fence_after();
   const int n_g = P.g.n_blk * kNGG;
-  if (P.dbg == 3) {
-    // tuning aid: no GEMM work, every G unit is published at once (results invalid)
-    if (warp == 0) {
-      if (lane_id() == 0)
-        for (int v = blockIdx.x; v < n_g; v += P.grid) red_release_gpu(P.counters + P.g.n_blk + v / kNGG, 1);
-    } else if (warp == 2) {
-      fi_producer<PROF>(P, smem, sy);
-    } else if (warp == 3) {
-      publisher<PROF>(P, sy, n_g);
-    } else if (warp >= 8) {
-      fi_workers<PROF>(P, smem, sy);
-    }
-  } else if (warp == 0) {
+  if (warp == 0) {
     if (lane_id() == 0) g_producer<PROF>(P, smem, sy, n_g);
   } else if (warp == 1) {
     g_issuer<PROF>(P, smem, sy, n_g);
@@ -815,7 +758,7 @@ static Plan plan(const Geo& g) {
   if (lag < 2) lag = 2;
   pl.L2 = lag;
   if (pl.NU < 2 && pl.NU < g.n_blk) return pl;
-  pl.counters_bytes = static_cast<size_t>(3 * g.n_blk + 2) * sizeof(int);   // + dynamic queue heads
+  pl.counters_bytes = static_cast<size_t>(3 * g.n_blk) * sizeof(int);
   pl.ok = true;
   return pl;
 }
@@ -849,10 +792,6 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.plane = pl.plane;
   P.n_fi = g.n_blk * (ws::kNCG + ws::kNIG);
-  P.dbg = 0;
-  if (const char* e = getenv("WF_WS_DBG")) P.dbg = atoi(e);
-  P.dyn = 0;
-  if (const char* e = getenv("WF_WS_DYN")) P.dyn = atoi(e);
   P.grid = sm_count;
   P.prof = 0;
   if (const char* e = getenv("WF_WS_PROF")) P.prof = atoi(e);
