@@ -37,9 +37,6 @@ constexpr int NT = 512;
 constexpr int kC = 64;                                   // C = C' = Cpad = Cppad
 constexpr int kT = 6;
 constexpr int kP = kT * kT;
-#ifndef WF_WS_FSCALAR
-#define WF_WS_FSCALAR 0   // measured: more instructions and spills than the f32x2 path
-#endif
 #ifndef WF_WS_GP
 #define WF_WS_GP 1
 #endif
@@ -59,9 +56,12 @@ constexpr uint32_t kBSlab = kC * kC * 2;                 // 8 KB: V hi or lo of 
 constexpr uint32_t kBBuf = 2 * kBSlab;                   // 16 KB
 constexpr size_t kUPos = 4 * kAHalf;                     // 32 KB: [hl][kb] half-K blocks
 constexpr size_t kUSlot = kP * kUPos;                    // 1.18 MB
-constexpr size_t kMPos = static_cast<size_t>(kC) * kBlockTiles * 4;   // 32 KB: [pair][tile][2]
+constexpr size_t kMPos = static_cast<size_t>(kC) * kBlockTiles * 4;   // 32 KB per position
 constexpr size_t kMSlot = kP * kMPos;
+// M ring slot layout: [I unit (c' group of 4)][position][c' pair (2)][tile][2]:
+// the products one I unit needs are one contiguous 72 KB range (one bulk copy)
 constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;    // 2 KB staged per position (I unit)
+constexpr uint32_t kMUnit = kP * kIPos;                  // 72 KB: the products of one I unit
 constexpr uint32_t kFISlot = 72 * 1024;                  // F staging or I staging
 constexpr uint32_t kOffB = kAStages * kAStage;           // 48 KB
 constexpr uint32_t kOffFI = kOffB + 2 * kBBuf;           // 80 KB
@@ -90,7 +90,7 @@ constexpr int kProfSlots = 32;
 __device__ unsigned long long g_wsprof[1024 * kProfSlots];
 enum ProfSlot {
   kGPDep, kGPStage, kGIFull, kGITempty, kGEWait, kGEBusy, kFPDep, kFPSlot, kFWWait, kFWF, kFWI, kPubFence,
-  kStart, kEndGP, kEndGI, kEndGE, kEndFP, kEndFW, kEndPub, kNF, kNI, kFWLoop
+  kStart, kEndGP, kEndGI, kEndGE, kEndFP, kEndFW, kEndPub, kNF, kNI, kFWLoop, kFPBusy
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -205,6 +205,32 @@ struct FIWalker {
   }
 };
 
+// Input staging of one F unit (64 tiles x 8 channels): every image row the
+// unit's windows touch is staged once per channel ("segments": the unit's
+// tile rows of one image, at most 3 or so images for small images), one bulk
+// copy per (channel, segment); rows outside the image are not staged, the
+// workers zero them.
+struct FGeo {
+  int gr0, bi0, ya0, rows0, nseg, rows_full, rows_last;
+  __device__ __host__ FGeo(const Geo& g, int t0, int tlast) {
+    const int gr1 = tlast / g.tiles_x;
+    gr0 = t0 / g.tiles_x;
+    bi0 = gr0 / g.tiles_y;
+    const int bi1 = gr1 / g.tiles_y;
+    const int ty0 = gr0 - bi0 * g.tiles_y, ty1 = gr1 - bi1 * g.tiles_y;
+    ya0 = ty0 * g.m - g.pad_lo > 0 ? ty0 * g.m - g.pad_lo : 0;
+    rows_full = min(g.H, (g.tiles_y - 1) * g.m - g.pad_lo + kT);
+    nseg = bi1 - bi0 + 1;
+    rows0 = (nseg == 1 ? min(g.H, ty1 * g.m - g.pad_lo + kT) : rows_full) - ya0;
+    rows_last = nseg == 1 ? 0 : min(g.H, ty1 * g.m - g.pad_lo + kT);
+  }
+  __device__ __host__ int rowoff(int k) const { return k == 0 ? 0 : rows0 + (k - 1) * rows_full; }
+  __device__ __host__ int rows(int k) const { return k == 0 ? rows0 : (k == nseg - 1 ? rows_last : rows_full); }
+  __device__ __host__ int total() const { return nseg == 1 ? rows0 : rows0 + (nseg - 2) * rows_full + rows_last; }
+  // staged row holding image row y of segment k
+  __device__ __host__ int srow(int k, int y) const { return k == 0 ? y - ya0 : rowoff(k) + y; }
+};
+
 // ------------------------------------------------------------ F/I producer
 template <bool PROF>
 __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
@@ -233,44 +259,39 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       mbar_wait(&sy.fi_empty[slot], ((it >> 1) & 1) ^ 1);
       pf.add(kFPSlot, t0);
     }
+    const long long tb = pf.now();
     __syncwarp();
     fence_proxy_async_smem();
     if (kind == 0) {
       const int part = sub / (kC / kCPC), cg = sub % (kC / kCPC);
       const int t0 = b * kBlockTiles + part * kFT;
       const int tlast = min(t0 + kFT, g.n_tile) - 1;
-      const int gr0 = t0 / g.tiles_x;
-      const int nrows = tlast >= t0 ? tlast / g.tiles_x - gr0 + 1 : 0;
       float* xs = reinterpret_cast<float*>(dstbase);
-      for (int cu = lane; cu < kCPC * nrows; cu += 32) {
-        const int j = cu % nrows, cl = cu / nrows;
-        const int gr = gr0 + j;
-        const int bi = gr / g.tiles_y, ty = gr - bi * g.tiles_y;
-        const int y0 = ty * g.m - g.pad_lo;
-        const int ya = max(y0, 0), yb = min(y0 + kT, g.H);
-        const int c = cg * kCPC + cl;
-        float* dst = xs + cl * P.plane + j * kT * g.W;
-        if (yb > ya) {
-          const uint32_t bytes = static_cast<uint32_t>((yb - ya) * g.W * 4);
-          mbar_add_tx(&sy.fi_full[slot], bytes);
-          bulk_g2s(dst + (ya - y0) * g.W, P.x + ((static_cast<size_t>(bi) * g.C + c) * g.H + ya) * g.W, bytes,
-                   &sy.fi_full[slot]);
+      if (tlast >= t0) {
+        const FGeo fg(g, t0, tlast);
+        if (lane == 0) mbar_add_tx(&sy.fi_full[slot], static_cast<uint32_t>(fg.total() * g.W * 4 * kCPC));
+        __syncwarp();
+        for (int cu = lane; cu < kCPC * fg.nseg; cu += 32) {
+          const int k = cu / kCPC, cl = cu - k * kCPC;
+          const int c = cg * kCPC + cl;
+          const int y0 = k == 0 ? fg.ya0 : 0;
+          const uint32_t bytes = static_cast<uint32_t>(fg.rows(k) * g.W * 4);
+          if (bytes)
+            bulk_g2s(xs + cl * P.plane + fg.rowoff(k) * g.W,
+                     P.x + ((static_cast<size_t>(fg.bi0 + k) * g.C + c) * g.H + y0) * g.W, bytes, &sy.fi_full[slot]);
         }
-        for (int r = 0; r < kT; ++r)
-          if (r < ya - y0 || r >= yb - y0)
-            for (int s2 = 0; s2 < g.W; s2 += 4)          // W % 4 == 0: 16-byte aligned rows
-              *reinterpret_cast<float4*>(dst + r * g.W + s2) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
     } else {
+      // the unit's products are one contiguous range: two 36 KB copies
       const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * kMSlot +
-                            static_cast<size_t>(2 * sub) * kBlockTiles * 8;
-      for (int p = lane; p < kP; p += 32) {
-        mbar_add_tx(&sy.fi_full[slot], kIPos);
-        bulk_g2s(dstbase + p * kIPos, msrc + p * kMPos, kIPos, &sy.fi_full[slot]);
-      }
+                            static_cast<size_t>(sub) * kMUnit;
+      if (lane == 0) mbar_add_tx(&sy.fi_full[slot], kMUnit);
+      __syncwarp();
+      if (lane < 2) bulk_g2s(dstbase + lane * (kMUnit / 2), msrc + lane * (kMUnit / 2), kMUnit / 2, &sy.fi_full[slot]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
+    pf.add(kFPBusy, tb);
   }
   pf.end(kEndFP);
 }
@@ -295,13 +316,6 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     pf.add(kFWWait, t0);
     t0 = pf.now();
     if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
-    if (kind == 2 && P.discard) {
-      // the unit's 36 x 2 KB of M are in smem now: 576 dead lines, ~2 per thread
-      const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * kMSlot +
-                            static_cast<size_t>(2 * sub) * kBlockTiles * 8;
-      for (int i = wtid; i < kP * (kIPos / 128); i += 256)
-        discard_l2(msrc + (i >> 4) * kMPos + (i & 15) * 128);
-    }
     if (kind == 0) {
       // ---- F(b, sub): thread = (tile tl, channel pair q); a warp = 8 tiles
       // (one core-matrix row group) x 4 pairs (one 8-channel k group), so
@@ -309,91 +323,44 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       const int part = sub / (kC / kCPC), cg = sub % (kC / kCPC);
       const int tb0 = part * kFT;
       const int t0 = b * kBlockTiles + tb0;
-      const int gr0 = t0 / g.tiles_x;
       const int tl = wl * 8 + (lane & 7), q = lane >> 3;
       const int tile = t0 + tl;
       const bool live = tile < g.n_tile;
-#if WF_WS_FSCALAR
-      // scalar f32 arithmetic, one channel at a time: the two channels of the
-      // pair come from different 16-byte loads, and packing them into f32x2
-      // register pairs costs a move per operand (per element the same
-      // operations and rounding as forward_transform2<6>)
-      float wa[kT][kT], wb[kT][kT];
-      if (live) {
-        const int per_img = g.tiles_y * g.tiles_x;
-        const int bi = tile / per_img;
-        const int rem = tile - bi * per_img;
-        const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
-        const int j = bi * g.tiles_y + ty - gr0;
-        const int x0 = tx * g.m - g.pad_lo;
-        const float* pa = reinterpret_cast<const float*>(src) + (2 * q) * P.plane + j * kT * g.W + x0;
-        const float* pb = pa + P.plane;
-        const bool lo_ok = x0 >= 0, hi_ok = x0 + kT <= g.W;
-#pragma unroll
-        for (int r = 0; r < kT; ++r) {
-          const float* ra = pa + r * g.W - 3;
-          const float* rb = pb + r * g.W - 3;
-          const float4 a0 = *reinterpret_cast<const float4*>(ra), a1 = *reinterpret_cast<const float4*>(ra + 4);
-          const float4 b0 = *reinterpret_cast<const float4*>(rb), b1 = *reinterpret_cast<const float4*>(rb + 4);
-          const float a5 = ra[8], b5 = rb[8];
-          wa[r][0] = lo_ok ? a0.w : 0.0f; wa[r][1] = a1.x; wa[r][2] = a1.y; wa[r][3] = a1.z; wa[r][4] = a1.w;
-          wa[r][5] = hi_ok ? a5 : 0.0f;
-          wb[r][0] = lo_ok ? b0.w : 0.0f; wb[r][1] = b1.x; wb[r][2] = b1.y; wb[r][3] = b1.z; wb[r][4] = b1.w;
-          wb[r][5] = hi_ok ? b5 : 0.0f;
-          bt6_line<ScalarOps>(wa[r][0], wa[r][1], wa[r][2], wa[r][3], wa[r][4], wa[r][5]);
-          bt6_line<ScalarOps>(wb[r][0], wb[r][1], wb[r][2], wb[r][3], wb[r][4], wb[r][5]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window consumed: slot free
-      if (live) {
-        const int row = tb0 + tl, c0 = cg * kCPC + 2 * q;
-        uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * kUSlot + (c0 >> 5) * kAHalf +
-                       (row >> 3) * 512 + ((c0 & 31) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2;
-#pragma unroll
-        for (int s = 0; s < kT; ++s) {
-          bt6_line<ScalarOps>(wa[0][s], wa[1][s], wa[2][s], wa[3][s], wa[4][s], wa[5][s]);
-          bt6_line<ScalarOps>(wb[0][s], wb[1][s], wb[2][s], wb[3][s], wb[4][s], wb[5][s]);
-#pragma unroll
-          for (int r = 0; r < kT; ++r) {
-            uint32_t hi, lo;
-            split_bf16x2(wa[r][s], wb[r][s], hi, lo);
-            uint8_t* p = dst + (r * kT + s) * kUPos;
-            *reinterpret_cast<uint32_t*>(p) = hi;
-            *reinterpret_cast<uint32_t*>(p + 2 * kAHalf) = lo;
-          }
-        }
-      }
-#else
       float2 w[kT][kT];
       if (live) {
+        const FGeo fg(g, t0, min(t0 + kFT, g.n_tile) - 1);
         const int per_img = g.tiles_y * g.tiles_x;
         const int bi = tile / per_img;
         const int rem = tile - bi * per_img;
         const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
-        const int j = bi * g.tiles_y + ty - gr0;
+        const int y0 = ty * g.m - g.pad_lo;
         const int x0 = tx * g.m - g.pad_lo;
-        const float* pa = reinterpret_cast<const float*>(src) + (2 * q) * P.plane + j * kT * g.W + x0;
+        const float* pa = reinterpret_cast<const float*>(src) + (2 * q) * P.plane + fg.srow(bi - fg.bi0, y0) * g.W + x0;
         const float* pb = pa + P.plane;
-        // window columns [x0, x0 + 6) with x0 = 4 tx - 1: two aligned 16-byte
-        // loads [x0 - 3, x0 + 5) plus one scalar per row, branch free; the
-        // image's left / right padding column is masked (the loads there read
-        // neighbouring staged data, inside the slot).  Each row is transformed
-        // (B^T along the row) as soon as it is loaded.
+        // window columns [x0, x0 + 6) with x0 = 4 tx - 1: one aligned 16-byte
+        // load [x0 + 1, x0 + 5) and two scalars per row, branch free; the
+        // image's padding columns and rows are zeros (their loads are
+        // predicated off or read neighbouring staged data inside the slot)
         const bool lo_ok = x0 >= 0, hi_ok = x0 + kT <= g.W;
 #pragma unroll
         for (int r = 0; r < kT; ++r) {
+          const bool rv = y0 + r >= 0 && y0 + r < g.H;
           const float* ra = pa + r * g.W - 3;
           const float* rb = pb + r * g.W - 3;
-          const float4 a0 = *reinterpret_cast<const float4*>(ra), a1 = *reinterpret_cast<const float4*>(ra + 4);
-          const float4 b0 = *reinterpret_cast<const float4*>(rb), b1 = *reinterpret_cast<const float4*>(rb + 4);
-          const float a5 = ra[8], b5 = rb[8];
-          w[r][0] = lo_ok ? make_float2(a0.w, b0.w) : make_float2(0.0f, 0.0f);
+          float4 a1 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), b1 = a1;
+          float a0 = 0.0f, b0 = 0.0f, a5 = 0.0f, b5 = 0.0f;
+          if (rv) {
+            a1 = *reinterpret_cast<const float4*>(ra + 4);
+            b1 = *reinterpret_cast<const float4*>(rb + 4);
+            if (lo_ok) { a0 = ra[3]; b0 = rb[3]; }
+            if (hi_ok) { a5 = ra[8]; b5 = rb[8]; }
+          }
+          w[r][0] = make_float2(a0, b0);
           w[r][1] = make_float2(a1.x, b1.x);
           w[r][2] = make_float2(a1.y, b1.y);
           w[r][3] = make_float2(a1.z, b1.z);
           w[r][4] = make_float2(a1.w, b1.w);
-          w[r][5] = hi_ok ? make_float2(a5, b5) : make_float2(0.0f, 0.0f);
+          w[r][5] = make_float2(a5, b5);
           bt6_line<PairOps>(w[r][0], w[r][1], w[r][2], w[r][3], w[r][4], w[r][5]);
         }
       }
@@ -424,7 +391,6 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           }
         }
       }
-#endif
     } else {
       // ---- I(b, sub): thread = (tile, c' pair); 36 staged float2 per thread
       const int tl = wtid & (kBlockTiles - 1), pr = wtid >> 7;
@@ -617,7 +583,8 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
       t0 = pf.now();
       tc_fence_after();
       const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (kGP * kC) + pl * kC;
-      float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * kGP + pl) * (kMPos / 4)) + row;
+      // pair k of position p: [k / 2][p][k % 2][tile][2] (see kMUnit)
+      float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * kGP + pl) * (kIPos / 4)) + row;
 #pragma unroll
       for (int c = 0; c < kC; c += 16) {
         float vv[16];
@@ -625,7 +592,10 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
         tmem_ld_wait();
         if (live) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) __stcg(mrow + (c / 2 + i) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]));
+          for (int i = 0; i < 8; ++i) {
+            const int k = c / 2 + i;
+            __stcg(mrow + (k >> 1) * (kMUnit / 8) + (k & 1) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]));
+          }
         }
       }
       pf.add(kGEBusy, t0);
@@ -739,8 +709,12 @@ static Plan plan(const Geo& g) {
   if (g.fft || g.T != kT || g.C != kC || g.Cp != kC || g.Cpad != kC || g.Cppad != kC) return pl;
   // the branch-free window loads assume pad_lo = 1 and 16-byte aligned rows (W % 4 == 0)
   if (g.W % 4 != 0 || g.m != 4 || g.pad_lo != 1 || g.W < 8) return pl;
-  const int trows = ceil_div(kFT - 1, g.tiles_x) + 1;
-  pl.plane = round_up(trows * kT * g.W, 32) + 16;
+  int max_rows = 0;                        // union staging: the largest unit
+  for (int t0 = 0; t0 < g.n_tile; t0 += kFT) {
+    const FGeo fg(g, t0, std::min(t0 + kFT, g.n_tile) - 1);
+    max_rows = std::max(max_rows, fg.total());
+  }
+  pl.plane = round_up(max_rows * g.W, 32) + 16;
   if (static_cast<size_t>(kCPC) * pl.plane * 4 > kFISlot) return pl;
   // measured on c2 (tools/ws_time.py): rings of 300 MB (slightly past L2)
   // with the I units 44 steps behind their F units are best (94 us)
