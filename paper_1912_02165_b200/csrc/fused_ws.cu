@@ -44,12 +44,13 @@ constexpr int kGP = WF_WS_GP;                            // positions per G unit
 constexpr int kNGG = kP / kGP;                           // G units per block
 constexpr int kNAcc = 512 / (kGP * kC);                  // TMEM accumulator buffers (units in flight)
 static_assert(kP % kGP == 0 && kNAcc >= 2, "G unit shape");
+static_assert(kGP == 1, "G units own one position (position-affine CTAs keep V resident)");
 constexpr int kCPC = 8;                                  // channels per F unit
 constexpr int kFT = 64;                                  // tiles per F unit
 constexpr int kNCG = (kBlockTiles / kFT) * (kC / kCPC);  // 16 F units per block
 constexpr int kIPairs = 2;                               // c' pairs per I unit
 constexpr int kNIG = kC / (2 * kIPairs);                 // 16 I units per block
-constexpr int kAStages = 3;
+constexpr int kAStages = 4;
 constexpr uint32_t kAHalf = kBlockTiles * 32 * 2;        // 8 KB: hi or lo, 128 rows x 32 k
 constexpr uint32_t kAStage = 2 * kAHalf;                 // 16 KB
 constexpr uint32_t kBSlab = kC * kC * 2;                 // 8 KB: V hi or lo of one position
@@ -63,8 +64,8 @@ constexpr size_t kMSlot = kP * kMPos;
 constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;    // 2 KB staged per position (I unit)
 constexpr uint32_t kMUnit = kP * kIPos;                  // 72 KB: the products of one I unit
 constexpr uint32_t kFISlot = 72 * 1024;                  // F staging or I staging
-constexpr uint32_t kOffB = kAStages * kAStage;           // 48 KB
-constexpr uint32_t kOffFI = kOffB + 2 * kBBuf;           // 80 KB
+constexpr uint32_t kOffB = kAStages * kAStage;           // 64 KB
+constexpr uint32_t kOffFI = kOffB + kBBuf;               // 80 KB (V of the CTA's position stays resident)
 constexpr uint32_t kSmem = kOffFI + 2 * kFISlot;         // 224 KB
 
 struct Params {
@@ -447,6 +448,19 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
   pf.end(kEndFW);
 }
 
+// G units of this CTA, in block order.  With one position per unit, CTA k
+// owns position k % 36 for the blocks b = k / 36, + grid / 36, ... -- its V
+// slab (16 KB) is loaded once and stays in shared memory (grid >= 36; the
+// grid % 36 last CTAs have no G work).
+struct GUnits {
+  int p, b0, step;
+  __device__ GUnits(const Params& P) {
+    step = P.grid / kP;
+    p = blockIdx.x % kP;
+    b0 = static_cast<int>(blockIdx.x) < step * kP ? blockIdx.x / kP : P.g.n_blk;
+  }
+};
+
 // -------------------------------------------------------------- G producer
 template <bool PROF>
 __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
@@ -454,9 +468,13 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   const int* doneF = P.counters;
   const int* doneI = P.counters + 2 * g.n_blk;
   const ProfT<PROF> pf(P.prof);
-  int a_it = 0, b_it = 0;
-  for (int v = blockIdx.x; v < n_g; v += P.grid) {
-    const int b = v / kNGG, gg = v - b * kNGG;
+  const GUnits gu(P);
+  if (gu.b0 < g.n_blk) {                                           // V of this CTA's position, once
+    mbar_expect_tx(&sy.b_full[0], kBBuf);
+    bulk_g2s(smem + kOffB, P.vpack + static_cast<size_t>(gu.p) * kBBuf, kBBuf, &sy.b_full[0]);
+  }
+  int a_it = 0;
+  for (int b = gu.b0; b < g.n_blk; b += gu.step) {
     long long t0 = pf.now();
     spin_until(doneF + b, kNCG);                                   // U complete
     if (b >= P.NM) spin_until(doneI + (b - P.NM), kNIG);           // M slot free
@@ -464,16 +482,8 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
     trace<PROF>(b, 2, true);
     fence_proxy_async_global();
     const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * kUSlot;
-    for (int pl = 0; pl < kGP; ++pl) {
-      const int p = gg * kGP + pl;
-      const int pb = b_it & 1;
-      long long t1 = pf.now();
-      mbar_wait(&sy.b_empty[pb], ((b_it >> 1) & 1) ^ 1);
-      pf.add(kGPStage, t1);
-      uint8_t* bdst = smem + kOffB + pb * kBBuf;
-      mbar_expect_tx(&sy.b_full[pb], kBBuf);
-      bulk_g2s(bdst, P.vpack + static_cast<size_t>(p) * kBBuf, kBBuf, &sy.b_full[pb]);
-      ++b_it;
+    {
+      const int p = gu.p;
       for (int kb = 0; kb < 2; ++kb) {
         const int st = a_it % kAStages;
         long long t2 = pf.now();
@@ -494,44 +504,40 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
 // ---------------------------------------------------------------- G issuer
 template <bool PROF>
 __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
-  // the whole warp runs the loop (its lanes drop the consumed U lines from
-  // L2); lane 0 issues the MMAs
+  // the whole warp runs the loop (its lanes may drop the consumed U lines
+  // from L2); lane 0 issues the MMAs
   const int lane = threadIdx.x & 31;
   const uint32_t idesc = idesc_bf16(kBlockTiles, kC);
   const ProfT<PROF> pf(P.prof);
-  int a_it = 0, b_it = 0, k = 0;
-  for (int v = blockIdx.x; v < n_g; v += P.grid, ++k) {
+  const GUnits gu(P);
+  if (gu.b0 < P.g.n_blk) mbar_wait(&sy.b_full[0], 0);            // the resident V slab
+  const uint32_t sb = smem_u32(smem + kOffB);
+  int a_it = 0, k = 0;
+  for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
     const int buf = k % kNAcc;
-    const int b = v / kNGG, gg = v - b * kNGG;
     const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * kUSlot;
     long long t0 = pf.now();
     mbar_wait(&sy.tempty[buf], ((k / kNAcc) & 1) ^ 1);
     pf.add(kGITempty, t0);
     tc_fence_after();
-    for (int pl = 0; pl < kGP; ++pl) {
-      const int pb = b_it & 1;
-      long long t1 = pf.now();
-      mbar_wait(&sy.b_full[pb], (b_it >> 1) & 1);
-      pf.add(kGIFull, t1);
-      const uint32_t sb = smem_u32(smem + kOffB + pb * kBBuf);
-      const uint32_t dcol = sy.tmem + buf * (kGP * kC) + pl * kC;
-      for (int kb = 0; kb < 2; ++kb) {
-        const int st = a_it % kAStages;
-        long long t2 = pf.now();
-        mbar_wait(&sy.a_full[st], (a_it / kAStages) & 1);
-        pf.add(kGIFull, t2);
-        tc_fence_after();
-        if (P.discard) {
-          // the stage's hi and lo half-K blocks (2 x 8 KB = 128 lines) are in smem now
-          const uint8_t* asrc = uslot + (gg * kGP + pl) * kUPos + kb * kAHalf;
+    const uint32_t dcol = sy.tmem + buf * kC;
+    for (int kb = 0; kb < 2; ++kb) {
+      const int st = a_it % kAStages;
+      long long t2 = pf.now();
+      mbar_wait(&sy.a_full[st], (a_it / kAStages) & 1);
+      pf.add(kGIFull, t2);
+      tc_fence_after();
+      if (P.discard) {
+        // the stage's hi and lo half-K blocks (2 x 8 KB = 128 lines) are in smem now
+        const uint8_t* asrc = uslot + gu.p * kUPos + kb * kAHalf;
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            discard_l2(asrc + (lane + 32 * i) * 128);
-            discard_l2(asrc + 2 * kAHalf + (lane + 32 * i) * 128);
-          }
+        for (int i = 0; i < 2; ++i) {
+          discard_l2(asrc + (lane + 32 * i) * 128);
+          discard_l2(asrc + 2 * kAHalf + (lane + 32 * i) * 128);
         }
-        __syncwarp();
-        if (lane == 0) {
+      }
+      __syncwarp();
+      if (lane == 0) {
         const uint32_t sa = smem_u32(smem + st * kAStage);
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
@@ -549,16 +555,10 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
           }
         }
         mma_commit(&sy.a_empty[st]);
-        }
-        __syncwarp();
-        ++a_it;
-      }
-      if (lane == 0) {
-        mma_commit(&sy.b_empty[pb]);
-        mma_commit(&sy.tfull[buf][pl]);
+        if (kb == 1) mma_commit(&sy.tfull[buf][0]);
       }
       __syncwarp();
-      ++b_it;
+      ++a_it;
     }
   }
   pf.end(kEndGI);
@@ -570,9 +570,10 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
   const int lane = threadIdx.x & 31, qd = (threadIdx.x >> 5) & 3;
   const int row = qd * 32 + lane;
   const ProfT<PROF> pf(P.prof && qd == 0 && lane == 0);
+  const GUnits gu(P);
+  const int gg = gu.p;
   int k = 0;
-  for (int v = blockIdx.x; v < n_g; v += P.grid, ++k) {
-    const int b = v / kNGG, gg = v - b * kNGG;
+  for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
     const int buf = k % kNAcc;
     const bool live = b * kBlockTiles + row < P.g.n_tile;
     float* mslot = P.mring + static_cast<size_t>(b % P.NM) * (kMSlot / 4);
@@ -724,7 +725,7 @@ static Plan plan(const Geo& g) {
   if (slots < 4) slots = 4;
   pl.NU = std::min(slots / 2, g.n_blk);
   pl.NM = std::min(slots - slots / 2, g.n_blk);
-  int lag = 44;
+  int lag = 32;
   if (const char* e = getenv("WF_WS_LAG")) lag = atoi(e);
   // deadlock freedom: some L1 with 1 <= L1 < NU (when F waits on G) and L2 - L1 < NM
   const int lmax = (pl.NU >= g.n_blk ? g.n_blk + pl.NM : pl.NU + pl.NM - 2);
@@ -741,6 +742,10 @@ static Plan plan(const Geo& g) {
 
 bool ws_fits(const Geo& g) {
   if (const char* e = getenv("WF_WS")) if (atoi(e) == 0) return false;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms < ws::kP) return false;          // position-affine G units need a CTA per position
   return ws::plan(g).ok;
 }
 
