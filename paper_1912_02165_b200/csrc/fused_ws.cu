@@ -78,6 +78,7 @@ struct Params {
   Geo g;
   int NU, NM, L2;
   int passes;
+  int dbg;                // tuning aid (WF_WS_DBG)
   int discard;            // drop consumed U / M ring lines from L2 (WF_WS_DISCARD, default off)
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
@@ -91,7 +92,7 @@ constexpr int kProfSlots = 32;
 __device__ unsigned long long g_wsprof[1024 * kProfSlots];
 enum ProfSlot {
   kGPDep, kGPStage, kGIFull, kGITempty, kGEWait, kGEBusy, kFPDep, kFPSlot, kFWWait, kFWF, kFWI, kPubFence,
-  kStart, kEndGP, kEndGI, kEndGE, kEndFP, kEndFW, kEndPub, kNF, kNI, kFWLoop, kFPBusy
+  kStart, kEndGP, kEndGI, kEndGE, kEndFP, kEndFW, kEndPub, kNF, kNI, kFWLoop, kFPBusy, kFPBusyI
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -261,8 +262,10 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       pf.add(kFPSlot, t0);
     }
     const long long tb = pf.now();
+    // (no proxy fence: the slot is only ever written by bulk copies; the
+    // workers' generic reads of its previous contents are ordered before
+    // these writes by the fi_empty barrier)
     __syncwarp();
-    fence_proxy_async_smem();
     if (kind == 0) {
       const int part = sub / (kC / kCPC), cg = sub % (kC / kCPC);
       const int t0 = b * kBlockTiles + part * kFT;
@@ -288,11 +291,14 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
                             static_cast<size_t>(sub) * kMUnit;
       if (lane == 0) mbar_add_tx(&sy.fi_full[slot], kMUnit);
       __syncwarp();
-      if (lane < 2) bulk_g2s(dstbase + lane * (kMUnit / 2), msrc + lane * (kMUnit / 2), kMUnit / 2, &sy.fi_full[slot]);
+      {
+        const int nc = P.dbg >= 10 ? P.dbg - 10 : 2;     // tuning aid: copies per I unit (1, 2, 4, 8)
+        if (lane < nc) bulk_g2s(dstbase + lane * (kMUnit / nc), msrc + lane * (kMUnit / nc), kMUnit / nc, &sy.fi_full[slot]);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
-    pf.add(kFPBusy, tb);
+    pf.add(kind == 0 ? kFPBusy : kFPBusyI, tb);
   }
   pf.end(kEndFP);
 }
@@ -767,6 +773,8 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.g = g;
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
+  P.dbg = 0;
+  if (const char* e = getenv("WF_WS_DBG")) P.dbg = atoi(e);
   P.discard = 0;   // measured neutral-to-slower on c2
   if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.plane = pl.plane;
