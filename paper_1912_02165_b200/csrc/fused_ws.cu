@@ -79,6 +79,7 @@ struct Params {
   int NU, NM, L2;
   int passes;
   int dbg;                // tuning aid (WF_WS_DBG)
+  int pf_ahead;           // F units whose input rows are prefetched into L2 this many units ahead (WF_WS_PF)
   int discard;            // drop consumed U / M ring lines from L2 (WF_WS_DISCARD, default off)
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
@@ -174,6 +175,10 @@ __device__ __forceinline__ int atom_acqrel_cta_smem(int* p, int v) {
 // neither cost a DRAM write-back nor push live ring lines out of L2.
 __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+// Pull a global range into L2 ahead of its bulk copy (no shared memory).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -298,6 +303,27 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
+    // the 2-slot ring hides one unit of copy latency; input rows come from
+    // HBM, so the rows of the unit PF_AHEAD units ahead are pulled into L2 now
+    if (P.pf_ahead > 0 && u + P.pf_ahead * P.grid < P.n_fi) {
+      int k2, b2, s2;
+      wk.decode(P, u + P.pf_ahead * P.grid, k2, b2, s2);
+      if (k2 == 0) {
+        const int part = s2 / (kC / kCPC), cg = s2 % (kC / kCPC);
+        const int t0 = b2 * kBlockTiles + part * kFT;
+        const int tlast = min(t0 + kFT, g.n_tile) - 1;
+        if (tlast >= t0) {
+          const FGeo fg(g, t0, tlast);
+          for (int cu = lane; cu < kCPC * fg.nseg; cu += 32) {
+            const int k = cu / kCPC, cl = cu - k * kCPC;
+            const uint32_t bytes = static_cast<uint32_t>(fg.rows(k) * g.W * 4);
+            if (bytes)
+              prefetch_l2(P.x + ((static_cast<size_t>(fg.bi0 + k) * g.C + cg * kCPC + cl) * g.H + (k == 0 ? fg.ya0 : 0)) * g.W,
+                          bytes);
+          }
+        }
+      }
+    }
     pf.add(kind == 0 ? kFPBusy : kFPBusyI, tb);
   }
   pf.end(kEndFP);
@@ -390,6 +416,10 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           bt6_line<PairOps>(w[0][s], w[1][s], w[2][s], w[3][s], w[4][s], w[5][s]);
 #pragma unroll
           for (int r = 0; r < kT; ++r) {
+            if (P.dbg == 1) {    // tuning aid: raw f32 pair stores, no split (results invalid)
+              if (live) *reinterpret_cast<float2*>(dst + (r * kT + s) * kUPos) = w[r][s];
+              continue;
+            }
             uint32_t hi, lo;
             split_bf16x2(w[r][s], hi, lo);
             const uint32_t other = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 8);
@@ -683,7 +713,19 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   __syncthreads();
   tc_fence_after();
   const int n_g = P.g.n_blk * kNGG;
-  if (warp == 0) {
+  if (P.dbg == 3) {
+    // tuning aid: no GEMM work, every G unit is published at once (results invalid)
+    if (warp == 0) {
+      if (lane_id() == 0)
+        for (int v = blockIdx.x; v < n_g; v += P.grid) red_release_gpu(P.counters + P.g.n_blk + v / kNGG, 1);
+    } else if (warp == 2) {
+      fi_producer<PROF>(P, smem, sy);
+    } else if (warp == 3) {
+      publisher<PROF>(P, sy, n_g);
+    } else if (warp >= 8) {
+      fi_workers<PROF>(P, smem, sy);
+    }
+  } else if (warp == 0) {
     if (lane_id() == 0) g_producer<PROF>(P, smem, sy, n_g);
   } else if (warp == 1) {
     g_issuer<PROF>(P, smem, sy, n_g);
@@ -773,6 +815,8 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.g = g;
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
+  P.pf_ahead = 0;   // measured neutral on c2
+  if (const char* e = getenv("WF_WS_PF")) P.pf_ahead = atoi(e);
   P.dbg = 0;
   if (const char* e = getenv("WF_WS_DBG")) P.dbg = atoi(e);
   P.discard = 0;   // measured neutral-to-slower on c2
