@@ -40,6 +40,9 @@ CONFIGS = {
     "c1": (1, 64, 64, 56, 4, "inv_sqrt", "normal"),
     # c5 (the sweep / scaling config) at its C = 64, 56x56 point: B = 256 per GPU
     "c5": (256, 64, 64, 56, 8, "he", "uniform"),
+    # tuning shapes (not bench lines): VGG-16 conv2_2 / conv3_x at B = 32
+    "vgg4": (32, 128, 128, 112, 6, "he", "normal"),
+    "vgg6": (32, 256, 256, 56, 6, "he", "normal"),
 }
 
 

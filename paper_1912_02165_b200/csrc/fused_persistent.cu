@@ -18,6 +18,7 @@
 // transformed tiles and products never make an HBM round trip, and all
 // three stages of different blocks run concurrently on different SMs with
 // no per-stage launch or tail.
+#include <algorithm>
 #include <cstdlib>
 #include <cuda_bf16.h>
 #include "common.cuh"
@@ -799,11 +800,16 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   if (const char* env = getenv("WF_L2_BUDGET_MB")) budget = static_cast<size_t>(atoi(env)) << 20;
   const int items_per_block = pl.n_cg + pl.n_gg + pl.n_ig;
   const int window = ceil_div(148 * pl.cps, items_per_block) + 1;
-  int lag = 32;
+  // the lag is a number of blocks; what matters is the work between a
+  // producer and its consumer, ~800 items (measured: c2 32 blocks of 33
+  // items, c5 (T = 8) 16-24 of 32, VGG 128->128@112 8-20 of 57 -- the old
+  // fixed 32 left that layer 822 us instead of 520), and the rings need
+  // slack beyond lag + window or the producers stall on ring slots
+  int lag = std::max(4, std::min(32, (800 + items_per_block / 2) / items_per_block));
   if (const char* env = getenv("WF_LAG")) lag = atoi(env);
   const int slots = static_cast<int>(budget / (pl.u_slot + pl.m_slot));
   if (slots < 4) return pl;
-  if (2 * (lag + window) > slots) lag = slots / 2 - window;
+  if (2 * (lag + window + 2) > slots) lag = slots / 2 - window - 2;
   if (lag < 1) lag = 1;
   int lag2 = lag;                          // inverse items trail the GEMM items by lag2 steps
   if (const char* env = getenv("WF_LAG2")) lag2 = atoi(env);
