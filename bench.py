@@ -41,8 +41,12 @@ CONFIGS = {
     # c5 (the sweep / scaling config) at its C = 64, 56x56 point: B = 256 per GPU
     "c5": (256, 64, 64, 56, 8, "he", "uniform"),
     # tuning shapes (not bench lines): VGG-16 conv2_2 / conv3_x at B = 32
+    "vgg1": (32, 3, 64, 224, 6, "he", "normal"),
+    "vgg3": (32, 64, 128, 112, 6, "he", "normal"),
     "vgg4": (32, 128, 128, 112, 6, "he", "normal"),
     "vgg6": (32, 256, 256, 56, 6, "he", "normal"),
+    "c5_32_112": (256, 32, 32, 112, 8, "he", "uniform"),
+    "c5_128_56": (256, 128, 128, 56, 8, "he", "uniform"),
 }
 
 
