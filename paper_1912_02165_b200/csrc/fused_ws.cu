@@ -34,6 +34,13 @@ namespace wf {
 namespace ws {
 
 constexpr int NT = 512;
+#ifndef WF_WS_REGS
+#define WF_WS_REGS 1
+#endif
+constexpr uint32_t kRegsLight = WF_WS_REGS ? 40 : 128;
+constexpr uint32_t kRegsEpi = WF_WS_REGS ? 64 : 128;
+constexpr uint32_t kRegsFI = WF_WS_REGS ? 200 : 128;
+static_assert(4 * 32 * kRegsLight + 4 * 32 * kRegsEpi + 8 * 32 * kRegsFI <= 65536, "register file");
 constexpr int kC = 64;                                   // C = C' = Cpad = Cppad
 constexpr int kT = 6;
 constexpr int kP = kT * kT;
@@ -179,6 +186,13 @@ __device__ __forceinline__ void discard_l2(const void* p) {
 // Pull a global range into L2 ahead of its bulk copy (no shared memory).
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// Register re-distribution between warpgroups (all 4 warps of a group run it).
+template <uint32_t N> __device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N> __device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -712,30 +726,38 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // 512 threads x 128 registers fill the register file at launch; the
+  // single-lane roles (warps 0-3) and the epilogue (4-7) hand registers to
+  // the transform warps (8-15): 4*32*40 + 4*32*64 + 8*32*200 <= 64K.  Each
+  // warpgroup re-sizes inside its own branch so ptxas allocates every
+  // role's code under its own limit.
   const int n_g = P.g.n_blk * kNGG;
-  if (P.dbg == 3) {
-    // tuning aid: no GEMM work, every G unit is published at once (results invalid)
-    if (warp == 0) {
-      if (lane_id() == 0)
-        for (int v = blockIdx.x; v < n_g; v += P.grid) red_release_gpu(P.counters + P.g.n_blk + v / kNGG, 1);
+  if (warp < 4) {
+    regs_dec<kRegsLight>();
+    if (P.dbg == 3) {
+      // tuning aid: no GEMM work, every G unit is published at once (results invalid)
+      if (warp == 0) {
+        if (lane_id() == 0)
+          for (int v = blockIdx.x; v < n_g; v += P.grid) red_release_gpu(P.counters + P.g.n_blk + v / kNGG, 1);
+      } else if (warp == 2) {
+        fi_producer<PROF>(P, smem, sy);
+      } else if (warp == 3) {
+        publisher<PROF>(P, sy, n_g);
+      }
+    } else if (warp == 0) {
+      if (lane_id() == 0) g_producer<PROF>(P, smem, sy, n_g);
+    } else if (warp == 1) {
+      g_issuer<PROF>(P, smem, sy, n_g);
     } else if (warp == 2) {
       fi_producer<PROF>(P, smem, sy);
-    } else if (warp == 3) {
+    } else {
       publisher<PROF>(P, sy, n_g);
-    } else if (warp >= 8) {
-      fi_workers<PROF>(P, smem, sy);
     }
-  } else if (warp == 0) {
-    if (lane_id() == 0) g_producer<PROF>(P, smem, sy, n_g);
-  } else if (warp == 1) {
-    g_issuer<PROF>(P, smem, sy, n_g);
-  } else if (warp == 2) {
-    fi_producer<PROF>(P, smem, sy);
-  } else if (warp == 3) {
-    publisher<PROF>(P, sy, n_g);
   } else if (warp < 8) {
-    g_epilogue<PROF>(P, sy, n_g);
+    regs_dec<kRegsEpi>();
+    if (P.dbg != 3) g_epilogue<PROF>(P, sy, n_g);
   } else {
+    regs_inc<kRegsFI>();
     fi_workers<PROF>(P, smem, sy);
   }
   tc_fence_before();
