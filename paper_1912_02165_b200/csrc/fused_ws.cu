@@ -100,7 +100,7 @@ constexpr int kProfSlots = 32;
 __device__ unsigned long long g_wsprof[1024 * kProfSlots];
 enum ProfSlot {
   kGPDep, kGPStage, kGIFull, kGITempty, kGEWait, kGEBusy, kFPDep, kFPSlot, kFWWait, kFWF, kFWI, kPubFence,
-  kStart, kEndGP, kEndGI, kEndGE, kEndFP, kEndFW, kEndPub, kNF, kNI, kFWLoop, kFPBusy, kFPBusyI
+  kStart, kEndGP, kEndGI, kEndGE, kEndFP, kEndFW, kEndPub, kNF, kNI, kFWLoop, kFPBusy, kFPBusyI, kFPTx, kFPCopy
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -290,10 +290,14 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       const int t0 = b * kBlockTiles + part * kFT;
       const int tlast = min(t0 + kFT, g.n_tile) - 1;
       float* xs = reinterpret_cast<float*>(dstbase);
-      if (tlast >= t0) {
+      // the single arrival carries the whole unit's byte count and comes
+      // first: the phase cannot complete before every copy has landed
+      // (copies that land earlier only drive the tx-count negative)
+      if (tlast < t0) {
+        if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
+      } else {
         const FGeo fg(g, t0, tlast);
-        if (lane == 0) mbar_add_tx(&sy.fi_full[slot], static_cast<uint32_t>(fg.total() * g.W * 4 * kCPC));
-        __syncwarp();
+        if (lane == 0) mbar_expect_tx(&sy.fi_full[slot], static_cast<uint32_t>(fg.total() * g.W * 4 * kCPC));
         for (int cu = lane; cu < kCPC * fg.nseg; cu += 32) {
           const int k = cu / kCPC, cl = cu - k * kCPC;
           const int c = cg * kCPC + cl;
@@ -308,15 +312,13 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       // the unit's products are one contiguous range: two 36 KB copies
       const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * kMSlot +
                             static_cast<size_t>(sub) * kMUnit;
-      if (lane == 0) mbar_add_tx(&sy.fi_full[slot], kMUnit);
-      __syncwarp();
-      {
-        const int nc = P.dbg >= 10 ? P.dbg - 10 : 2;     // tuning aid: copies per I unit (1, 2, 4, 8)
-        if (lane < nc) bulk_g2s(dstbase + lane * (kMUnit / nc), msrc + lane * (kMUnit / nc), kMUnit / nc, &sy.fi_full[slot]);
+      if (lane == 0) {
+        mbar_expect_tx(&sy.fi_full[slot], kMUnit);       // the arrival, with the byte count
+        bulk_g2s(dstbase, msrc, kMUnit / 2, &sy.fi_full[slot]);
+        bulk_g2s(dstbase + kMUnit / 2, msrc + kMUnit / 2, kMUnit / 2, &sy.fi_full[slot]);
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
     // the 2-slot ring hides one unit of copy latency; input rows come from
     // HBM, so the rows of the unit PF_AHEAD units ahead are pulled into L2 now
     if (P.pf_ahead > 0 && u + P.pf_ahead * P.grid < P.n_fi) {

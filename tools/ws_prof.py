@@ -26,7 +26,7 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 names = ["G-prod dep wait", "G-prod stage wait", "G-issue full wait", "G-issue tempty wait", "G-epi tfull wait",
          "G-epi busy", "FI-prod dep wait", "FI-prod slot wait", "FI-work full wait", "FI-work F busy",
          "FI-work I busy", "publish fence"]
-extra = {21: "FI-work loop total", 22: "FI-prod busy F (issue)", 23: "FI-prod busy I (issue)"}
+extra = {21: "FI-work loop total", 22: "FI-prod busy F (issue)", 23: "FI-prod busy I (issue)", 24: "FI-prod I: expect_tx", 25: "FI-prod I: copy issue"}
 clk = 1.9e3
 for it in range(3):
     flush.zero_()
