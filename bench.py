@@ -45,6 +45,7 @@ CONFIGS = {
     "vgg3": (32, 64, 128, 112, 6, "he", "normal"),
     "vgg4": (32, 128, 128, 112, 6, "he", "normal"),
     "vgg6": (32, 256, 256, 56, 6, "he", "normal"),
+    "vgg9": (32, 512, 512, 28, 6, "he", "normal"),
     "c5_32_112": (256, 32, 32, 112, 8, "he", "uniform"),
     "c5_128_56": (256, 128, 128, 56, 8, "he", "uniform"),
 }
