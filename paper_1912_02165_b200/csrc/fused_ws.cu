@@ -41,46 +41,57 @@ constexpr uint32_t kRegsLight = WF_WS_REGS ? 40 : 128;
 constexpr uint32_t kRegsEpi = WF_WS_REGS ? 64 : 128;
 constexpr uint32_t kRegsFI = WF_WS_REGS ? 200 : 128;
 static_assert(4 * 32 * kRegsLight + 4 * 32 * kRegsEpi + 8 * 32 * kRegsFI <= 65536, "register file");
-constexpr int kC = 64;                                   // C = C' = Cpad = Cppad
 constexpr int kT = 6;
 constexpr int kP = kT * kT;
 #ifndef WF_WS_GP
 #define WF_WS_GP 1
 #endif
 constexpr int kGP = WF_WS_GP;                            // positions per G unit
-constexpr int kNGG = kP / kGP;                           // G units per block
-constexpr int kNAcc = 512 / (kGP * kC);                  // TMEM accumulator buffers (units in flight)
-static_assert(kP % kGP == 0 && kNAcc >= 2, "G unit shape");
 static_assert(kGP == 1, "G units own one position (position-affine CTAs keep V resident)");
+constexpr int kN = 64;                                   // output channels per G unit (MMA N)
+constexpr int kNAcc = 512 / (kGP * kN);                  // TMEM accumulator buffers (units in flight)
 constexpr int kCPC = 8;                                  // channels per F unit
 constexpr int kFT = 64;                                  // tiles per F unit
-constexpr int kNCG = (kBlockTiles / kFT) * (kC / kCPC);  // 16 F units per block
 constexpr int kIPairs = 2;                               // c' pairs per I unit
-constexpr int kNIG = kC / (2 * kIPairs);                 // 16 I units per block
-constexpr int kAStages = 4;
 constexpr uint32_t kAHalf = kBlockTiles * 32 * 2;        // 8 KB: hi or lo, 128 rows x 32 k
-constexpr uint32_t kAStage = 2 * kAHalf;                 // 16 KB
-constexpr uint32_t kBSlab = kC * kC * 2;                 // 8 KB: V hi or lo of one position
-constexpr uint32_t kBBuf = 2 * kBSlab;                   // 16 KB
-constexpr size_t kUPos = 4 * kAHalf;                     // 32 KB: [hl][kb] half-K blocks
-constexpr size_t kUSlot = kP * kUPos;                    // 1.18 MB
-constexpr size_t kMPos = static_cast<size_t>(kC) * kBlockTiles * 4;   // 32 KB per position
-constexpr size_t kMSlot = kP * kMPos;
+constexpr uint32_t kAStage = 2 * kAHalf;                 // 16 KB: one 32-channel K block, hi + lo
+constexpr int kMaxAStages = 4;
 // M ring slot layout: [I unit (c' group of 4)][position][c' pair (2)][tile][2]:
 // the products one I unit needs are one contiguous 72 KB range (one bulk copy)
 constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;    // 2 KB staged per position (I unit)
 constexpr uint32_t kMUnit = kP * kIPos;                  // 72 KB: the products of one I unit
 constexpr uint32_t kFISlot = 72 * 1024;                  // F staging or I staging
-constexpr uint32_t kOffB = kAStages * kAStage;           // 64 KB
-constexpr uint32_t kOffFI = kOffB + kBBuf;               // 80 KB (V of the CTA's position stays resident)
-constexpr uint32_t kSmem = kOffFI + 2 * kFISlot;         // 224 KB
+
+// Channel shape: C input channels (GEMM K, 32-channel K blocks), CP output
+// channels (GEMM N, 64-wide G units).  Shared memory: A stages + the V slab
+// of the CTA's (position, c' group) + two 72 KB F/I slots <= 227 KB.
+template <int C_, int CP_>
+struct Shape {
+  static constexpr int C = C_, CP = CP_;
+  static constexpr int kKB = C / 32;                     // 32-channel K blocks
+  static constexpr int kNG = CP / kN;                    // c' groups (G units per position)
+  static constexpr int kNGG = kP * kNG;                  // G units per block
+  static constexpr int kNCG = (kBlockTiles / kFT) * (C / kCPC);   // F units per block
+  static constexpr int kNIG = CP / (2 * kIPairs);                 // I units per block
+  static constexpr int kAStages = C >= 128 ? 3 : 4;
+  static constexpr uint32_t kVHalf = kN * C * 2;         // V hi (or lo) of one (position, c' group)
+  static constexpr uint32_t kVGroup = 2 * kVHalf;
+  static constexpr size_t kUPos = 2 * kKB * kAHalf;      // U of one position: [hl][K block]
+  static constexpr size_t kUSlot = kP * kUPos;
+  static constexpr size_t kMPos = static_cast<size_t>(CP) * kBlockTiles * 4;
+  static constexpr size_t kMSlot = kP * kMPos;
+  static constexpr uint32_t kOffB = kAStages * kAStage;
+  static constexpr uint32_t kOffFI = kOffB + kVGroup;
+  static constexpr uint32_t kSmem = kOffFI + 2 * kFISlot;
+  static_assert(kSmem <= 227 * 1024 && kAStages <= kMaxAStages && C % 64 == 0 && CP % kN == 0, "shape");
+};
 
 struct Params {
   const float* x;
   float* y;
   const uint8_t* vpack;   // standard MMA pack: per position hi / lo slabs of 64 x 64 (kblock, kc = 64)
-  uint8_t* uring;         // NU slots x kUSlot
-  float* mring;           // NM slots x kMSlot
+  uint8_t* uring;         // NU slots x S::kUSlot
+  float* mring;           // NM slots x S::kMSlot
   int* counters;          // doneF, doneG, doneI (n_blk each)
   Geo g;
   int NU, NM, L2;
@@ -131,7 +142,7 @@ struct ProfT {
 };
 
 struct Sync {
-  uint64_t a_full[kAStages], a_empty[kAStages];
+  uint64_t a_full[kMaxAStages], a_empty[kMaxAStages];
   uint64_t b_full[2], b_empty[2];
   uint64_t tfull[kNAcc][kGP], tempty[kNAcc];
   uint64_t fi_full[2], fi_empty[2];
@@ -198,31 +209,31 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// The F/I queue: step s holds the kNCG F units of block s (s < n_blk) and
-// then the kNIG I units of block s - L2.  Closed-form decode (no state
+// The F/I queue: step s holds the S::kNCG F units of block s (s < n_blk) and
+// then the S::kNIG I units of block s - L2.  Closed-form decode (no state
 // carried across units: nothing to keep live through the transforms).
+template <class S>
 struct FIWalker {
   __device__ void init(const Params&) {}
   // -> kind (0 = F, 2 = I), block, sub
   __device__ void decode(const Params& P, int u, int& kind, int& b, int& sub) const {
     const int nb = P.g.n_blk, L = P.L2;
-    static_assert(kNCG == kNIG, "closed-form decode assumes equal F and I units per block");
-    constexpr int n = kNCG;
+    constexpr int nf = S::kNCG, ni = S::kNIG;
     if (L >= nb) {                       // all F steps come before the first I step
-      if (u < n * nb) { kind = 0; b = u / n; sub = u - b * n; }
-      else { kind = 2; b = (u - n * nb) / n; sub = (u - n * nb) - b * n; }
+      if (u < nf * nb) { kind = 0; b = u / nf; sub = u - b * nf; }
+      else { kind = 2; b = (u - nf * nb) / ni; sub = (u - nf * nb) - b * ni; }
       return;
     }
-    if (u < n * L) { kind = 0; b = u / n; sub = u - b * n; return; }
-    const int u2 = u - n * L;
-    if (u2 < 2 * n * (nb - L)) {         // steps L .. nb-1: F(s) then I(s - L)
-      const int s = u2 / (2 * n), k = u2 - s * 2 * n;
-      if (k < n) { kind = 0; b = L + s; sub = k; }
-      else { kind = 2; b = s; sub = k - n; }
+    if (u < nf * L) { kind = 0; b = u / nf; sub = u - b * nf; return; }
+    const int u2 = u - nf * L;
+    if (u2 < (nf + ni) * (nb - L)) {     // steps L .. nb-1: F(s) then I(s - L)
+      const int st = u2 / (nf + ni), k = u2 - st * (nf + ni);
+      if (k < nf) { kind = 0; b = L + st; sub = k; }
+      else { kind = 2; b = st; sub = k - nf; }
       return;
     }
-    const int u3 = u2 - 2 * n * (nb - L);  // steps nb ..: I only
-    kind = 2; b = nb - L + u3 / n; sub = u3 - (u3 / n) * n;
+    const int u3 = u2 - (nf + ni) * (nb - L);  // steps nb ..: I only
+    kind = 2; b = nb - L + u3 / ni; sub = u3 - (u3 / ni) * ni;
   }
 };
 
@@ -253,26 +264,26 @@ struct FGeo {
 };
 
 // ------------------------------------------------------------ F/I producer
-template <bool PROF>
+template <class S, bool PROF>
 __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
   const Geo& g = P.g;
   const int lane = threadIdx.x & 31;
   const int* doneG = P.counters + g.n_blk;
   const ProfT<PROF> pf(P.prof && lane == 0);
-  FIWalker wk;
+  FIWalker<S> wk;
   wk.init(P);
   int it = 0;
   for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
     int kind, b, sub;
     wk.decode(P, u, kind, b, sub);
     const int slot = it & 1;
-    uint8_t* dstbase = smem + kOffFI + slot * kFISlot;
+    uint8_t* dstbase = smem + S::kOffFI + slot * kFISlot;
     if (lane == 0) {
       long long t0 = pf.now();
       if (kind == 0) {
-        if (b >= P.NU) spin_until(doneG + (b - P.NU), kNGG);     // U slot free
+        if (b >= P.NU) spin_until(doneG + (b - P.NU), S::kNGG);     // U slot free
       } else {
-        spin_until(doneG + b, kNGG);                               // M complete
+        spin_until(doneG + b, S::kNGG);                               // M complete
         fence_proxy_async_global();
       }
       pf.add(kFPDep, t0);
@@ -286,7 +297,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     // these writes by the fi_empty barrier)
     __syncwarp();
     if (kind == 0) {
-      const int part = sub / (kC / kCPC), cg = sub % (kC / kCPC);
+      const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
       const int t0 = b * kBlockTiles + part * kFT;
       const int tlast = min(t0 + kFT, g.n_tile) - 1;
       float* xs = reinterpret_cast<float*>(dstbase);
@@ -310,7 +321,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       }
     } else {
       // the unit's products are one contiguous range: two 36 KB copies
-      const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * kMSlot +
+      const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * S::kMSlot +
                             static_cast<size_t>(sub) * kMUnit;
       if (lane == 0) {
         mbar_expect_tx(&sy.fi_full[slot], kMUnit);       // the arrival, with the byte count
@@ -325,7 +336,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       int k2, b2, s2;
       wk.decode(P, u + P.pf_ahead * P.grid, k2, b2, s2);
       if (k2 == 0) {
-        const int part = s2 / (kC / kCPC), cg = s2 % (kC / kCPC);
+        const int part = s2 / (S::C / kCPC), cg = s2 % (S::C / kCPC);
         const int t0 = b2 * kBlockTiles + part * kFT;
         const int tlast = min(t0 + kFT, g.n_tile) - 1;
         if (tlast >= t0) {
@@ -346,20 +357,20 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
 }
 
 // ------------------------------------------------------------- F/I workers
-template <bool PROF>
+template <class S, bool PROF>
 __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
   const Geo& g = P.g;
   const int wtid = threadIdx.x - 256, lane = threadIdx.x & 31, wl = wtid >> 5;
   const ProfT<PROF> pf(P.prof && wtid == 0);
   const long long tloop = pf.now();
-  FIWalker wk;
+  FIWalker<S> wk;
   wk.init(P);
   int it = 0;
   for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
     int kind, b, sub;
     wk.decode(P, u, kind, b, sub);
     const int slot = it & 1;
-    const uint8_t* src = smem + kOffFI + slot * kFISlot;
+    const uint8_t* src = smem + S::kOffFI + slot * kFISlot;
     long long t0 = pf.now();
     mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
     pf.add(kFWWait, t0);
@@ -369,7 +380,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       // ---- F(b, sub): thread = (tile tl, channel pair q); a warp = 8 tiles
       // (one core-matrix row group) x 4 pairs (one 8-channel k group), so
       // every store instruction writes one contiguous 128-byte core matrix
-      const int part = sub / (kC / kCPC), cg = sub % (kC / kCPC);
+      const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
       const int tb0 = part * kFT;
       const int t0 = b * kBlockTiles + tb0;
       const int tl = wl * 8 + (lane & 7), q = lane >> 3;
@@ -424,23 +435,23 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
         // two 4-byte ones (a warp still writes whole core-matrix rows).
         const bool odd = q & 1;
         const int row = tb0 + tl, c0 = cg * kCPC + 2 * (q & ~1);
-        uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * kUSlot + (c0 >> 5) * kAHalf +
+        uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 >> 5) * kAHalf +
                        (row >> 3) * 512 + ((c0 & 31) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
-                       (odd ? 2 * kAHalf : 0);
+                       (odd ? S::kKB * kAHalf : 0);
 #pragma unroll
         for (int s = 0; s < kT; ++s) {
           bt6_line<PairOps>(w[0][s], w[1][s], w[2][s], w[3][s], w[4][s], w[5][s]);
 #pragma unroll
           for (int r = 0; r < kT; ++r) {
             if (P.dbg == 1) {    // tuning aid: raw f32 pair stores, no split (results invalid)
-              if (live) *reinterpret_cast<float2*>(dst + (r * kT + s) * kUPos) = w[r][s];
+              if (live) *reinterpret_cast<float2*>(dst + (r * kT + s) * S::kUPos) = w[r][s];
               continue;
             }
             uint32_t hi, lo;
             split_bf16x2(w[r][s], hi, lo);
             const uint32_t other = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 8);
             if (live)
-              *reinterpret_cast<uint2*>(dst + (r * kT + s) * kUPos) = odd ? make_uint2(other, lo) : make_uint2(hi, other);
+              *reinterpret_cast<uint2*>(dst + (r * kT + s) * S::kUPos) = odd ? make_uint2(other, lo) : make_uint2(hi, other);
           }
         }
       }
@@ -500,52 +511,66 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
   pf.end(kEndFW);
 }
 
-// G units of this CTA, in block order.  With one position per unit, CTA k
-// owns position k % 36 for the blocks b = k / 36, + grid / 36, ... -- its V
-// slab (16 KB) is loaded once and stays in shared memory (grid >= 36; the
-// grid % 36 last CTAs have no G work).
+// G units of this CTA, in block order.  A G unit is one (position, group of
+// 64 output channels) of one block; CTA k owns the pair k % (36 * groups)
+// for the blocks b = k / (36 * groups), + grid / (36 * groups), ... -- its V
+// slab (64 x C, hi + lo) is loaded once and stays in shared memory (grid >=
+// 36 * groups; the remaining CTAs have no G work).
+template <class S>
 struct GUnits {
-  int p, b0, step;
+  int p, ng, b0, step;
   __device__ GUnits(const Params& P) {
-    step = P.grid / kP;
-    p = blockIdx.x % kP;
-    b0 = static_cast<int>(blockIdx.x) < step * kP ? blockIdx.x / kP : P.g.n_blk;
+    constexpr int combos = kP * S::kNG;                  // (position, c' group) pairs
+    step = P.grid / combos;
+    const int c = blockIdx.x % combos;
+    p = c % kP;
+    ng = c / kP;
+    b0 = static_cast<int>(blockIdx.x) < step * combos ? blockIdx.x / combos : P.g.n_blk;
   }
 };
 
 // -------------------------------------------------------------- G producer
-template <bool PROF>
+template <class S, bool PROF>
 __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   const Geo& g = P.g;
   const int* doneF = P.counters;
   const int* doneI = P.counters + 2 * g.n_blk;
   const ProfT<PROF> pf(P.prof);
-  const GUnits gu(P);
-  if (gu.b0 < g.n_blk) {                                           // V of this CTA's position, once
-    mbar_expect_tx(&sy.b_full[0], kBBuf);
-    bulk_g2s(smem + kOffB, P.vpack + static_cast<size_t>(gu.p) * kBBuf, kBBuf, &sy.b_full[0]);
+  const GUnits<S> gu(P);
+  if (gu.b0 < g.n_blk) {
+    // V of this CTA's (position, c' group), once: in the MMA pack (per
+    // position a hi and a lo slab of CP x C, K blocks of 64) the group's 64
+    // rows of one K block are 8 KB contiguous; smem holds [hl][K block of 64]
+    mbar_expect_tx(&sy.b_full[0], S::kVGroup);
+    const size_t slab = static_cast<size_t>(S::CP) * S::C * 2;
+    for (int hl = 0; hl < 2; ++hl)
+      for (int j = 0; j < S::C / 64; ++j)
+        bulk_g2s(smem + S::kOffB + (hl * (S::C / 64) + j) * 8192,
+                 P.vpack + (static_cast<size_t>(gu.p) * 2 + hl) * slab + static_cast<size_t>(j) * S::CP * 128 +
+                     static_cast<size_t>(gu.ng) * 8192,
+                 8192, &sy.b_full[0]);
   }
   int a_it = 0;
   for (int b = gu.b0; b < g.n_blk; b += gu.step) {
     long long t0 = pf.now();
-    spin_until(doneF + b, kNCG);                                   // U complete
-    if (b >= P.NM) spin_until(doneI + (b - P.NM), kNIG);           // M slot free
+    spin_until(doneF + b, S::kNCG);                                   // U complete
+    if (b >= P.NM) spin_until(doneI + (b - P.NM), S::kNIG);           // M slot free
     pf.add(kGPDep, t0);
     trace<PROF>(b, 2, true);
     fence_proxy_async_global();
-    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * kUSlot;
+    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot;
     {
       const int p = gu.p;
-      for (int kb = 0; kb < 2; ++kb) {
-        const int st = a_it % kAStages;
+      for (int kb = 0; kb < S::kKB; ++kb) {
+        const int st = a_it % S::kAStages;
         long long t2 = pf.now();
-        mbar_wait(&sy.a_empty[st], ((a_it / kAStages) & 1) ^ 1);
+        mbar_wait(&sy.a_empty[st], ((a_it / S::kAStages) & 1) ^ 1);
         pf.add(kGPStage, t2);
         uint8_t* adst = smem + st * kAStage;
         mbar_expect_tx(&sy.a_full[st], kAStage);
-        const uint8_t* asrc = uslot + p * kUPos + kb * kAHalf;
+        const uint8_t* asrc = uslot + p * S::kUPos + kb * kAHalf;
         bulk_g2s(adst, asrc, kAHalf, &sy.a_full[st]);                          // hi
-        bulk_g2s(adst + kAHalf, asrc + 2 * kAHalf, kAHalf, &sy.a_full[st]);    // lo
+        bulk_g2s(adst + kAHalf, asrc + S::kKB * kAHalf, kAHalf, &sy.a_full[st]);    // lo
         ++a_it;
       }
     }
@@ -554,38 +579,38 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
 }
 
 // ---------------------------------------------------------------- G issuer
-template <bool PROF>
+template <class S, bool PROF>
 __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   // the whole warp runs the loop (its lanes may drop the consumed U lines
   // from L2); lane 0 issues the MMAs
   const int lane = threadIdx.x & 31;
-  const uint32_t idesc = idesc_bf16(kBlockTiles, kC);
+  const uint32_t idesc = idesc_bf16(kBlockTiles, kN);
   const ProfT<PROF> pf(P.prof);
-  const GUnits gu(P);
+  const GUnits<S> gu(P);
   if (gu.b0 < P.g.n_blk) mbar_wait(&sy.b_full[0], 0);            // the resident V slab
-  const uint32_t sb = smem_u32(smem + kOffB);
+  const uint32_t sb = smem_u32(smem + S::kOffB);
   int a_it = 0, k = 0;
   for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
     const int buf = k % kNAcc;
-    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * kUSlot;
+    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot;
     long long t0 = pf.now();
     mbar_wait(&sy.tempty[buf], ((k / kNAcc) & 1) ^ 1);
     pf.add(kGITempty, t0);
     tc_fence_after();
-    const uint32_t dcol = sy.tmem + buf * kC;
-    for (int kb = 0; kb < 2; ++kb) {
-      const int st = a_it % kAStages;
+    const uint32_t dcol = sy.tmem + buf * kN;
+    for (int kb = 0; kb < S::kKB; ++kb) {
+      const int st = a_it % S::kAStages;
       long long t2 = pf.now();
-      mbar_wait(&sy.a_full[st], (a_it / kAStages) & 1);
+      mbar_wait(&sy.a_full[st], (a_it / S::kAStages) & 1);
       pf.add(kGIFull, t2);
       tc_fence_after();
       if (P.discard) {
         // the stage's hi and lo half-K blocks (2 x 8 KB = 128 lines) are in smem now
-        const uint8_t* asrc = uslot + gu.p * kUPos + kb * kAHalf;
+        const uint8_t* asrc = uslot + gu.p * S::kUPos + kb * kAHalf;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           discard_l2(asrc + (lane + 32 * i) * 128);
-          discard_l2(asrc + 2 * kAHalf + (lane + 32 * i) * 128);
+          discard_l2(asrc + S::kKB * kAHalf + (lane + 32 * i) * 128);
         }
       }
       __syncwarp();
@@ -595,8 +620,10 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
         for (int s = 0; s < 2; ++s) {
           const uint64_t ahi = smem_desc(sa + s * 256, 128, 512);
           const uint64_t alo = smem_desc(sa + kAHalf + s * 256, 128, 512);
-          const uint64_t bhi = smem_desc(sb + kb * 512 + s * 256, 128, 1024);
-          const uint64_t blo = smem_desc(sb + kBSlab + kb * 512 + s * 256, 128, 1024);
+          // V: [hl][K block of 64][64 rows x 64 k], 32-channel block kb at (kb/2, kb%2)
+          const uint32_t voff = (kb >> 1) * 8192 + (kb & 1) * 512 + s * 256;
+          const uint64_t bhi = smem_desc(sb + voff, 128, 1024);
+          const uint64_t blo = smem_desc(sb + S::kVHalf + voff, 128, 1024);
           const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
           if (P.passes > 1) {
             mma_bf16_ss(dcol, alo, bhi, idesc, first);
@@ -607,7 +634,7 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
           }
         }
         mma_commit(&sy.a_empty[st]);
-        if (kb == 1) mma_commit(&sy.tfull[buf][0]);
+        if (kb == S::kKB - 1) mma_commit(&sy.tfull[buf][0]);
       }
       __syncwarp();
       ++a_it;
@@ -617,36 +644,37 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
 }
 
 // -------------------------------------------------------------- G epilogue
-template <bool PROF>
+template <class S, bool PROF>
 __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
   const int lane = threadIdx.x & 31, qd = (threadIdx.x >> 5) & 3;
   const int row = qd * 32 + lane;
   const ProfT<PROF> pf(P.prof && qd == 0 && lane == 0);
-  const GUnits gu(P);
+  const GUnits<S> gu(P);
   const int gg = gu.p;
   int k = 0;
   for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
     const int buf = k % kNAcc;
     const bool live = b * kBlockTiles + row < P.g.n_tile;
-    float* mslot = P.mring + static_cast<size_t>(b % P.NM) * (kMSlot / 4);
+    float* mslot = P.mring + static_cast<size_t>(b % P.NM) * (S::kMSlot / 4);
     for (int pl = 0; pl < kGP; ++pl) {
       long long t0 = pf.now();
       mbar_wait(&sy.tfull[buf][pl], (k / kNAcc) & 1);
       pf.add(kGEWait, t0);
       t0 = pf.now();
       tc_fence_after();
-      const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (kGP * kC) + pl * kC;
-      // pair k of position p: [k / 2][p][k % 2][tile][2] (see kMUnit)
+      const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (kGP * kN) + pl * kN;
+      // pair k of position p: [k / 2][p][k % 2][tile][2] (see kMUnit); this
+      // unit's 64 outputs are the pairs 32 ng .. 32 ng + 31
       float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * kGP + pl) * (kIPos / 4)) + row;
 #pragma unroll
-      for (int c = 0; c < kC; c += 16) {
+      for (int c = 0; c < kN; c += 16) {
         float vv[16];
         tmem_ld16(taddr + c, vv);
         tmem_ld_wait();
         if (live) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int k = c / 2 + i;
+            const int k = gu.ng * (kN / 2) + c / 2 + i;
             __stcg(mrow + (k >> 1) * (kMUnit / 8) + (k & 1) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]));
           }
         }
@@ -672,14 +700,14 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
 }
 
 // --------------------------------------------------------------- publisher
-template <bool PROF>
+template <class S, bool PROF>
 __device__ void publisher(const Params& P, Sync& sy, int n_g) {
   if ((threadIdx.x & 31) != 0) return;
   const ProfT<PROF> pf(P.prof);
   int* doneF = P.counters;
   int* doneG = doneF + P.g.n_blk;
   int* doneI = doneG + P.g.n_blk;
-  FIWalker wk;
+  FIWalker<S> wk;
   wk.init(P);
   int uf = blockIdx.x, kf = 0;        // next F/I unit of this CTA, its ordinal
   int vg = blockIdx.x, kg = 0;        // next G unit, its ordinal
@@ -701,13 +729,13 @@ __device__ void publisher(const Params& P, Sync& sy, int n_g) {
   pf.end(kEndPub);
 }
 
-template <bool PROF>
+template <class S, bool PROF>
 __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Sync sy;
   const int tid = threadIdx.x, warp = tid >> 5;
   if (tid == 0) {
-    for (int s = 0; s < kAStages; ++s) { mbar_init(&sy.a_full[s], 1); mbar_init(&sy.a_empty[s], 1); }
+    for (int s = 0; s < S::kAStages; ++s) { mbar_init(&sy.a_full[s], 1); mbar_init(&sy.a_empty[s], 1); }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sy.b_full[s], 1);
       mbar_init(&sy.b_empty[s], 1);
@@ -733,34 +761,34 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   // the transform warps (8-15): 4*32*40 + 4*32*64 + 8*32*200 <= 64K.  Each
   // warpgroup re-sizes inside its own branch so ptxas allocates every
   // role's code under its own limit.
-  const int n_g = P.g.n_blk * kNGG;
+  const int n_g = P.g.n_blk * S::kNGG;
   if (warp < 4) {
     regs_dec<kRegsLight>();
     if (P.dbg == 3) {
       // tuning aid: no GEMM work, every G unit is published at once (results invalid)
       if (warp == 0) {
         if (lane_id() == 0)
-          for (int v = blockIdx.x; v < n_g; v += P.grid) red_release_gpu(P.counters + P.g.n_blk + v / kNGG, 1);
+          for (int v = blockIdx.x; v < n_g; v += P.grid) red_release_gpu(P.counters + P.g.n_blk + v / S::kNGG, 1);
       } else if (warp == 2) {
-        fi_producer<PROF>(P, smem, sy);
+        fi_producer<S, PROF>(P, smem, sy);
       } else if (warp == 3) {
-        publisher<PROF>(P, sy, n_g);
+        publisher<S, PROF>(P, sy, n_g);
       }
     } else if (warp == 0) {
-      if (lane_id() == 0) g_producer<PROF>(P, smem, sy, n_g);
+      if (lane_id() == 0) g_producer<S, PROF>(P, smem, sy, n_g);
     } else if (warp == 1) {
-      g_issuer<PROF>(P, smem, sy, n_g);
+      g_issuer<S, PROF>(P, smem, sy, n_g);
     } else if (warp == 2) {
-      fi_producer<PROF>(P, smem, sy);
+      fi_producer<S, PROF>(P, smem, sy);
     } else {
-      publisher<PROF>(P, sy, n_g);
+      publisher<S, PROF>(P, sy, n_g);
     }
   } else if (warp < 8) {
     regs_dec<kRegsEpi>();
-    if (P.dbg != 3) g_epilogue<PROF>(P, sy, n_g);
+    if (P.dbg != 3) g_epilogue<S, PROF>(P, sy, n_g);
   } else {
     regs_inc<kRegsFI>();
-    fi_workers<PROF>(P, smem, sy);
+    fi_workers<S, PROF>(P, smem, sy);
   }
   tc_fence_before();
   __syncthreads();
@@ -774,12 +802,12 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
 struct Plan {
   bool ok;
   int NU, NM, L2, plane;
-  size_t counters_bytes;
+  size_t counters_bytes, u_slot, m_slot;
 };
 
-static Plan plan(const Geo& g) {
+template <class S>
+static Plan plan_t(const Geo& g) {
   Plan pl = {};
-  if (g.fft || g.T != kT || g.C != kC || g.Cp != kC || g.Cpad != kC || g.Cppad != kC) return pl;
   // the branch-free window loads assume pad_lo = 1 and 16-byte aligned rows (W % 4 == 0)
   if (g.W % 4 != 0 || g.m != 4 || g.pad_lo != 1 || g.W < 8) return pl;
   int max_rows = 0;                        // union staging: the largest unit
@@ -790,10 +818,10 @@ static Plan plan(const Geo& g) {
   pl.plane = round_up(max_rows * g.W, 32) + 16;
   if (static_cast<size_t>(kCPC) * pl.plane * 4 > kFISlot) return pl;
   // measured on c2 (tools/ws_time.py): rings of 300 MB (slightly past L2)
-  // with the I units 44 steps behind their F units are best (94 us)
+  // with the I units 32 steps behind their F units are best (80 us)
   size_t budget = 300ull << 20;
   if (const char* e = getenv("WF_WS_BUDGET_MB")) budget = static_cast<size_t>(atoi(e)) << 20;
-  int slots = static_cast<int>(budget / (kUSlot + kMSlot));
+  int slots = static_cast<int>(budget / (S::kUSlot + S::kMSlot));
   if (slots < 4) slots = 4;
   pl.NU = std::min(slots / 2, g.n_blk);
   pl.NM = std::min(slots - slots / 2, g.n_blk);
@@ -806,25 +834,66 @@ static Plan plan(const Geo& g) {
   pl.L2 = lag;
   if (pl.NU < 2 && pl.NU < g.n_blk) return pl;
   pl.counters_bytes = static_cast<size_t>(3 * g.n_blk) * sizeof(int);
+  pl.u_slot = S::kUSlot;
+  pl.m_slot = S::kMSlot;
   pl.ok = true;
   return pl;
+}
+
+// Channel shapes with a kernel instance: C (= Cpad) in {64, 128}, C' (=
+// C'pad) in {64, 128, 256} -- every (position, c' group) pair gets a CTA of
+// its own (36 x C'/64 <= 148), and A stages + V + two F/I slots fit smem.
+template <class F>
+static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<64, 64>())) {
+  using R = decltype(f(Shape<64, 64>()));
+  if (g.fft || g.T != kT || g.C != g.Cpad || g.Cp != g.Cppad) return R();
+  switch (g.C * 1000 + g.Cp) {
+    case 64064: return f(Shape<64, 64>());
+    case 64128: return f(Shape<64, 128>());
+    case 64256: return f(Shape<64, 256>());
+    case 128064: return f(Shape<128, 64>());
+    case 128128: return f(Shape<128, 128>());
+    case 128256: return f(Shape<128, 256>());
+  }
+  return R();
+}
+
+static Plan plan(const Geo& g) {
+  return with_shape(g, [&](auto s) { return plan_t<decltype(s)>(g); });
+}
+
+template <class S>
+static cudaError_t launch_t(const Params& P, int sm_count, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fused_ws_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fused_ws_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  note_launch();
+  if (P.prof) fused_ws_kernel<S, true><<<sm_count, NT, S::kSmem, st>>>(P);
+  else fused_ws_kernel<S, false><<<sm_count, NT, S::kSmem, st>>>(P);
+  return cudaGetLastError();
 }
 
 }  // namespace ws
 
 bool ws_fits(const Geo& g) {
   if (const char* e = getenv("WF_WS")) if (atoi(e) == 0) return false;
+  const ws::Plan pl = ws::plan(g);
+  if (!pl.ok) return false;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (sms < ws::kP) return false;          // position-affine G units need a CTA per position
-  return ws::plan(g).ok;
+  return sms >= ws::kP * (g.Cp / ws::kN);   // a CTA per (position, c' group)
 }
 
 size_t ws_scratch_bytes(const Geo& g) {
   const ws::Plan pl = ws::plan(g);
   if (!pl.ok) return 0;
-  return round_up(static_cast<int>(pl.counters_bytes), 1024) + pl.NU * ws::kUSlot + pl.NM * ws::kMSlot;
+  return round_up(static_cast<int>(pl.counters_bytes), 1024) + pl.NU * pl.u_slot + pl.NM * pl.m_slot;
 }
 
 cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g, int passes,
@@ -835,7 +904,7 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.x = x; P.y = y; P.vpack = vpack;
   P.counters = reinterpret_cast<int*>(scratch);
   P.uring = scratch + round_up(static_cast<int>(pl.counters_bytes), 1024);
-  P.mring = reinterpret_cast<float*>(P.uring + pl.NU * ws::kUSlot);
+  P.mring = reinterpret_cast<float*>(P.uring + pl.NU * pl.u_slot);
   P.g = g;
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
@@ -846,25 +915,18 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.discard = 0;   // measured neutral-to-slower on c2
   if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.plane = pl.plane;
-  P.n_fi = g.n_blk * (ws::kNCG + ws::kNIG);
   P.grid = sm_count;
   P.prof = 0;
   if (const char* e = getenv("WF_WS_PROF")) P.prof = atoi(e);
   cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
   if (e != cudaSuccess) return e;
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(ws::fused_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws::kSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(ws::fused_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws::kSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  note_launch();
-  if (P.prof) ws::fused_ws_kernel<true><<<sm_count, ws::NT, ws::kSmem, st>>>(P);
-  else ws::fused_ws_kernel<false><<<sm_count, ws::NT, ws::kSmem, st>>>(P);
-  return cudaGetLastError();
+  return ws::with_shape(g, [&](auto s) {
+    using S = decltype(s);
+    P.n_fi = g.n_blk * (S::kNCG + S::kNIG);
+    return ws::launch_t<S>(P, sm_count, st);
+  });
 }
+
 
 }  // namespace wf
 

@@ -302,10 +302,16 @@ def test_randomized_sweep_like_reference_acceptance():
 @pytest.mark.parametrize("dims", [(3, 64, 64, 56, 56, 3, 1, 1),     # 588 tiles: a partial last block
                                   (2, 64, 64, 28, 36, 3, 1, 1),     # non-square, 7 x 9 tiles per image
                                   (5, 64, 64, 12, 8, 3, 1, 1),      # tiny images, several per F unit
-                                  (16, 64, 64, 56, 56, 3, 1, 1)])   # 25 blocks: ring reuse
+                                  (16, 64, 64, 56, 56, 3, 1, 1),    # 25 blocks: ring reuse
+                                  (2, 64, 128, 28, 24, 3, 1, 1),    # the other channel shapes
+                                  (2, 128, 64, 20, 28, 3, 1, 1),
+                                  (3, 128, 128, 28, 28, 3, 1, 1),
+                                  (2, 64, 256, 16, 20, 3, 1, 1),
+                                  (2, 128, 256, 24, 16, 3, 1, 1)])
 def test_warp_specialised_kernel(dims, monkeypatch):
-    """The warp-specialised fused kernel (F(4x4,3x3), C = C' = 64, W % 4 == 0,
-    pad 1 -- the c2 benchmark layer) against three-stage (bitwise), the
+    """The warp-specialised fused kernel (F(4x4,3x3), C in {64, 128}, C' in
+    {64, 128, 256}, W % 4 == 0, pad 1 -- the c2 benchmark layer and the
+    VGG 64/128-channel layers) against three-stage (bitwise), the
     item-queue persistent kernel (WF_WS=0, bitwise) and FP64 direct.  Small
     rings (WF_WS_BUDGET_MB) force slot reuse and the lagged dependencies."""
     spec = wf.LayerSpec(*dims)
