@@ -42,6 +42,7 @@ CONFIGS = {
     "c5": (256, 64, 64, 56, 8, "he", "uniform"),
     # tuning shapes (not bench lines): VGG-16 conv2_2 / conv3_x at B = 32
     "vgg1": (32, 3, 64, 224, 6, "he", "normal"),
+    "vgg2": (32, 64, 64, 224, 6, "he", "normal"),
     "vgg3": (32, 64, 128, 112, 6, "he", "normal"),
     "vgg4": (32, 128, 128, 112, 6, "he", "normal"),
     "vgg6": (32, 256, 256, 56, 6, "he", "normal"),

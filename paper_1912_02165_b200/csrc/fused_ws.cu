@@ -53,8 +53,6 @@ constexpr int kNAcc = 512 / (kGP * kN);                  // TMEM accumulator buf
 constexpr int kCPC = 8;                                  // channels per F unit
 constexpr int kFT = 64;                                  // tiles per F unit
 constexpr int kIPairs = 2;                               // c' pairs per I unit
-constexpr uint32_t kAHalf = kBlockTiles * 32 * 2;        // 8 KB: hi or lo, 128 rows x 32 k
-constexpr uint32_t kAStage = 2 * kAHalf;                 // 16 KB: one 32-channel K block, hi + lo
 constexpr int kMaxAStages = 4;
 // M ring slot layout: [I unit (c' group of 4)][position][c' pair (2)][tile][2]:
 // the products one I unit needs are one contiguous 72 KB range (one bulk copy)
@@ -67,8 +65,13 @@ constexpr uint32_t kFISlot = 72 * 1024;                  // F staging or I stagi
 // of the CTA's (position, c' group) + two 72 KB F/I slots <= 227 KB.
 template <int C_, int CP_>
 struct Shape {
-  static constexpr int C = C_, CP = CP_;
-  static constexpr int kKB = C / 32;                     // 32-channel K blocks
+  static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
+  static constexpr int kKBW = C < 32 ? C : 32;           // K block width (channels per A stage)
+  static constexpr int kKB = C / kKBW;                   // K blocks
+  static constexpr uint32_t kAHalf = kBlockTiles * kKBW * 2;   // hi or lo of one K block
+  static constexpr uint32_t kAStage = 2 * kAHalf;
+  static constexpr int kVKW = C < 64 ? C : 64;           // K block width of the MMA pack (kblock layout)
+  static constexpr uint32_t kVChunk = kN * kVKW * 2;     // one c' group's rows of one pack K block
   static constexpr int kNG = CP / kN;                    // c' groups (G units per position)
   static constexpr int kNGG = kP * kNG;                  // G units per block
   static constexpr int kNCG = (kBlockTiles / kFT) * (C / kCPC);   // F units per block
@@ -83,7 +86,7 @@ struct Shape {
   static constexpr uint32_t kOffB = kAStages * kAStage;
   static constexpr uint32_t kOffFI = kOffB + kVGroup;
   static constexpr uint32_t kSmem = kOffFI + 2 * kFISlot;
-  static_assert(kSmem <= 227 * 1024 && kAStages <= kMaxAStages && C % 64 == 0 && CP % kN == 0, "shape");
+  static_assert(kSmem <= 227 * 1024 && kAStages <= kMaxAStages && C % 16 == 0 && CP % kN == 0, "shape");
 };
 
 struct Params {
@@ -304,17 +307,19 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       // the single arrival carries the whole unit's byte count and comes
       // first: the phase cannot complete before every copy has landed
       // (copies that land earlier only drive the tx-count negative)
-      if (tlast < t0) {
+      // channels at or past C (K padding of a 16-channel layer) are not staged
+      const int real = min(max(g.C - cg * kCPC, 0), kCPC);
+      if (tlast < t0 || real == 0) {
         if (lane == 0) mbar_arrive(&sy.fi_full[slot]);
       } else {
         const FGeo fg(g, t0, tlast);
-        if (lane == 0) mbar_expect_tx(&sy.fi_full[slot], static_cast<uint32_t>(fg.total() * g.W * 4 * kCPC));
+        if (lane == 0) mbar_expect_tx(&sy.fi_full[slot], static_cast<uint32_t>(fg.total() * g.W * 4 * real));
         for (int cu = lane; cu < kCPC * fg.nseg; cu += 32) {
           const int k = cu / kCPC, cl = cu - k * kCPC;
           const int c = cg * kCPC + cl;
           const int y0 = k == 0 ? fg.ya0 : 0;
           const uint32_t bytes = static_cast<uint32_t>(fg.rows(k) * g.W * 4);
-          if (bytes)
+          if (bytes && cl < real)
             bulk_g2s(xs + cl * P.plane + fg.rowoff(k) * g.W,
                      P.x + ((static_cast<size_t>(fg.bi0 + k) * g.C + c) * g.H + y0) * g.W, bytes, &sy.fi_full[slot]);
         }
@@ -402,6 +407,9 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
         // image's padding columns and rows are zeros (their loads are
         // predicated off or read neighbouring staged data inside the slot)
         const bool lo_ok = x0 >= 0, hi_ok = x0 + kT <= g.W;
+        // K padding channels (only in 16-channel layers) are zeros, never loaded
+        const int c0 = cg * kCPC + 2 * q;
+        const bool ca = S::C >= 64 || c0 < g.C, cb = S::C >= 64 || c0 + 1 < g.C;
 #pragma unroll
         for (int r = 0; r < kT; ++r) {
           const bool rv = y0 + r >= 0 && y0 + r < g.H;
@@ -409,11 +417,15 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           const float* rb = pb + r * g.W - 3;
           float4 a1 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), b1 = a1;
           float a0 = 0.0f, b0 = 0.0f, a5 = 0.0f, b5 = 0.0f;
-          if (rv) {
+          if (rv && ca) {
             a1 = *reinterpret_cast<const float4*>(ra + 4);
+            if (lo_ok) a0 = ra[3];
+            if (hi_ok) a5 = ra[8];
+          }
+          if (rv && cb) {
             b1 = *reinterpret_cast<const float4*>(rb + 4);
-            if (lo_ok) { a0 = ra[3]; b0 = rb[3]; }
-            if (hi_ok) { a5 = ra[8]; b5 = rb[8]; }
+            if (lo_ok) b0 = rb[3];
+            if (hi_ok) b5 = rb[8];
           }
           w[r][0] = make_float2(a0, b0);
           w[r][1] = make_float2(a1.x, b1.x);
@@ -435,9 +447,9 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
         // two 4-byte ones (a warp still writes whole core-matrix rows).
         const bool odd = q & 1;
         const int row = tb0 + tl, c0 = cg * kCPC + 2 * (q & ~1);
-        uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 >> 5) * kAHalf +
-                       (row >> 3) * 512 + ((c0 & 31) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
-                       (odd ? S::kKB * kAHalf : 0);
+        uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 / S::kKBW) * S::kAHalf +
+                       (row >> 3) * (16 * S::kKBW) + ((c0 % S::kKBW) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
+                       (odd ? S::kKB * S::kAHalf : 0);
 #pragma unroll
         for (int s = 0; s < kT; ++s) {
           bt6_line<PairOps>(w[0][s], w[1][s], w[2][s], w[3][s], w[4][s], w[5][s]);
@@ -544,11 +556,11 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
     mbar_expect_tx(&sy.b_full[0], S::kVGroup);
     const size_t slab = static_cast<size_t>(S::CP) * S::C * 2;
     for (int hl = 0; hl < 2; ++hl)
-      for (int j = 0; j < S::C / 64; ++j)
-        bulk_g2s(smem + S::kOffB + (hl * (S::C / 64) + j) * 8192,
-                 P.vpack + (static_cast<size_t>(gu.p) * 2 + hl) * slab + static_cast<size_t>(j) * S::CP * 128 +
-                     static_cast<size_t>(gu.ng) * 8192,
-                 8192, &sy.b_full[0]);
+      for (int j = 0; j < S::C / S::kVKW; ++j)
+        bulk_g2s(smem + S::kOffB + (hl * (S::C / S::kVKW) + j) * S::kVChunk,
+                 P.vpack + (static_cast<size_t>(gu.p) * 2 + hl) * slab +
+                     static_cast<size_t>(j) * S::CP * S::kVKW * 2 + static_cast<size_t>(gu.ng) * S::kVChunk,
+                 S::kVChunk, &sy.b_full[0]);
   }
   int a_it = 0;
   for (int b = gu.b0; b < g.n_blk; b += gu.step) {
@@ -566,11 +578,11 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
         long long t2 = pf.now();
         mbar_wait(&sy.a_empty[st], ((a_it / S::kAStages) & 1) ^ 1);
         pf.add(kGPStage, t2);
-        uint8_t* adst = smem + st * kAStage;
-        mbar_expect_tx(&sy.a_full[st], kAStage);
-        const uint8_t* asrc = uslot + p * S::kUPos + kb * kAHalf;
-        bulk_g2s(adst, asrc, kAHalf, &sy.a_full[st]);                          // hi
-        bulk_g2s(adst + kAHalf, asrc + S::kKB * kAHalf, kAHalf, &sy.a_full[st]);    // lo
+        uint8_t* adst = smem + st * S::kAStage;
+        mbar_expect_tx(&sy.a_full[st], S::kAStage);
+        const uint8_t* asrc = uslot + p * S::kUPos + kb * S::kAHalf;
+        bulk_g2s(adst, asrc, S::kAHalf, &sy.a_full[st]);                          // hi
+        bulk_g2s(adst + S::kAHalf, asrc + S::kKB * S::kAHalf, S::kAHalf, &sy.a_full[st]);    // lo
         ++a_it;
       }
     }
@@ -606,24 +618,25 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
       tc_fence_after();
       if (P.discard) {
         // the stage's hi and lo half-K blocks (2 x 8 KB = 128 lines) are in smem now
-        const uint8_t* asrc = uslot + gu.p * S::kUPos + kb * kAHalf;
+        const uint8_t* asrc = uslot + gu.p * S::kUPos + kb * S::kAHalf;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           discard_l2(asrc + (lane + 32 * i) * 128);
-          discard_l2(asrc + S::kKB * kAHalf + (lane + 32 * i) * 128);
+          discard_l2(asrc + S::kKB * S::kAHalf + (lane + 32 * i) * 128);
         }
       }
       __syncwarp();
       if (lane == 0) {
-        const uint32_t sa = smem_u32(smem + st * kAStage);
+        const uint32_t sa = smem_u32(smem + st * S::kAStage);
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const uint64_t ahi = smem_desc(sa + s * 256, 128, 512);
-          const uint64_t alo = smem_desc(sa + kAHalf + s * 256, 128, 512);
-          // V: [hl][K block of 64][64 rows x 64 k], 32-channel block kb at (kb/2, kb%2)
-          const uint32_t voff = (kb >> 1) * 8192 + (kb & 1) * 512 + s * 256;
-          const uint64_t bhi = smem_desc(sb + voff, 128, 1024);
-          const uint64_t blo = smem_desc(sb + S::kVHalf + voff, 128, 1024);
+        for (int s = 0; s < S::kKBW / 16; ++s) {
+          const uint64_t ahi = smem_desc(sa + s * 256, 128, 16 * S::kKBW);
+          const uint64_t alo = smem_desc(sa + S::kAHalf + s * 256, 128, 16 * S::kKBW);
+          // V: [hl][pack K block][64 rows x kVKW k]; channel k0 of this K step
+          const int k0 = kb * S::kKBW + s * 16;
+          const uint32_t voff = (k0 / S::kVKW) * S::kVChunk + ((k0 % S::kVKW) >> 3) * 128;
+          const uint64_t bhi = smem_desc(sb + voff, 128, 16 * S::kVKW);
+          const uint64_t blo = smem_desc(sb + S::kVHalf + voff, 128, 16 * S::kVKW);
           const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
           if (P.passes > 1) {
             mma_bf16_ss(dcol, alo, bhi, idesc, first);
@@ -840,14 +853,17 @@ static Plan plan_t(const Geo& g) {
   return pl;
 }
 
-// Channel shapes with a kernel instance: C (= Cpad) in {64, 128}, C' (=
-// C'pad) in {64, 128, 256} -- every (position, c' group) pair gets a CTA of
+// Channel shapes with a kernel instance: Cpad in {64, 128} (= C) and 16
+// (C <= 16), C' (= C'pad) in {64, 128, 256} -- every (position, c' group) pair gets a CTA of
 // its own (36 x C'/64 <= 148), and A stages + V + two F/I slots fit smem.
 template <class F>
 static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<64, 64>())) {
   using R = decltype(f(Shape<64, 64>()));
-  if (g.fft || g.T != kT || g.C != g.Cpad || g.Cp != g.Cppad) return R();
-  switch (g.C * 1000 + g.Cp) {
+  // C = Cpad except for the 16-channel instance, which zero-pads C <= 16
+  // (VGG's RGB layer); C' = C'pad
+  if (g.fft || g.T != kT || g.Cp != g.Cppad || (g.C != g.Cpad && g.Cpad != 16)) return R();
+  switch (g.Cpad * 1000 + g.Cp) {
+    case 16064: return f(Shape<16, 64>());
     case 64064: return f(Shape<64, 64>());
     case 64128: return f(Shape<64, 128>());
     case 64256: return f(Shape<64, 256>());

@@ -307,7 +307,9 @@ def test_randomized_sweep_like_reference_acceptance():
                                   (2, 128, 64, 20, 28, 3, 1, 1),
                                   (3, 128, 128, 28, 28, 3, 1, 1),
                                   (2, 64, 256, 16, 20, 3, 1, 1),
-                                  (2, 128, 256, 24, 16, 3, 1, 1)])
+                                  (2, 128, 256, 24, 16, 3, 1, 1),
+                                  (2, 3, 64, 40, 44, 3, 1, 1),      # RGB input: 16-channel K padding
+                                  (2, 16, 64, 16, 24, 3, 1, 1)])
 def test_warp_specialised_kernel(dims, monkeypatch):
     """The warp-specialised fused kernel (F(4x4,3x3), C in {64, 128}, C' in
     {64, 128, 256}, W % 4 == 0, pad 1 -- the c2 benchmark layer and the
