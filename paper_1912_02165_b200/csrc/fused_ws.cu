@@ -838,7 +838,11 @@ static Plan plan_t(const Geo& g) {
   if (slots < 4) slots = 4;
   pl.NU = std::min(slots / 2, g.n_blk);
   pl.NM = std::min(slots - slots / 2, g.n_blk);
-  int lag = 32;
+  // the lag counts steps; a step is one block's F and I units, so the lag
+  // that keeps ~1000 units between a block's F and I units shrinks with the
+  // channel counts (measured: c2 32 steps of 32 units, VGG 64->128 and
+  // 128->128 16 steps of 48 / 64 units, VGG 3->64 32 of 20)
+  int lag = std::max(8, std::min(32, 1024 / (S::kNCG + S::kNIG)));
   if (const char* e = getenv("WF_WS_LAG")) lag = atoi(e);
   // deadlock freedom: some L1 with 1 <= L1 < NU (when F waits on G) and L2 - L1 < NM
   const int lmax = (pl.NU >= g.n_blk ? g.n_blk + pl.NM : pl.NU + pl.NM - 2);
