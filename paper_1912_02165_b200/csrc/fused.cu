@@ -14,14 +14,25 @@
 // left idle by wave w's GEMM / inverse tails (stage overlap without a
 // device-wide scheduler).  Fork/join through events keeps the call
 // stream-ordered for the caller.
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include "fused.cuh"
 #include "staged.cuh"
 
 namespace wf {
 
-static constexpr int kLanes = 2;                    // concurrent wave pipelines
-static constexpr size_t kL2Budget = 56ull << 20;    // U + M of all in-flight waves
+static constexpr int kMaxLanes = 4;
+// concurrent wave pipelines and the L2 budget of their U + M (WF_WAVE_LANES,
+// WF_WAVE_L2_MB override)
+static int lanes_cfg() {
+  const char* e = getenv("WF_WAVE_LANES");
+  return e ? std::max(1, std::min(kMaxLanes, atoi(e))) : 2;
+}
+static size_t budget_cfg() {
+  const char* e = getenv("WF_WAVE_L2_MB");
+  return (e ? static_cast<size_t>(atoi(e)) : 56) << 20;
+}
 
 // Bytes of U + M for one 128-tile block.
 static size_t block_bytes(const Geo& g) {
@@ -35,7 +46,7 @@ static size_t block_bytes(const Geo& g) {
 // L2-sized block would leave most SMs idle and the wave loop would be
 // launch-bound.
 static int wave_blocks(const Geo& g) {
-  size_t nb = kL2Budget / kLanes / block_bytes(g);
+  size_t nb = budget_cfg() / lanes_cfg() / block_bytes(g);
   const int n_nc = ceil_div(g.Cppad, gemm_nc(g.Cppad));
   const size_t nb_par = static_cast<size_t>(ceil_div(2 * 148, g.P * n_nc));
   if (nb < nb_par) nb = nb_par;
@@ -47,12 +58,12 @@ static int wave_blocks(const Geo& g) {
 size_t fused_scratch_bytes(const Geo& g, int /*r*/) {
   if (ws_fits(g)) return ws_scratch_bytes(g);
   if (persistent_fits(g)) return persistent_scratch_bytes(g);
-  return static_cast<size_t>(kLanes) * wave_blocks(g) * block_bytes(g);
+  return static_cast<size_t>(lanes_cfg()) * wave_blocks(g) * block_bytes(g);
 }
 
 struct LaneResources {
-  cudaStream_t aux = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t aux[kMaxLanes - 1] = {};
+  cudaEvent_t fork = nullptr, join[kMaxLanes - 1] = {};
 };
 
 static LaneResources& lane_resources() {
@@ -62,10 +73,12 @@ static LaneResources& lane_resources() {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   LaneResources& r = res[dev & 63];
-  if (!r.aux) {
-    cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking);
+  if (!r.fork) {
+    for (int i = 0; i < kMaxLanes - 1; ++i) {
+      cudaStreamCreateWithFlags(&r.aux[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&r.join[i], cudaEventDisableTiming);
+    }
     cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
   }
   return r;
 }
@@ -78,12 +91,12 @@ cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* s
   const size_t P = static_cast<size_t>(g.P);
   const size_t lane_bytes = static_cast<size_t>(wb) * block_bytes(g);
   const int n_waves = ceil_div(g.n_blk, wb);
-  const int lanes = n_waves > 1 ? kLanes : 1;
+  const int lanes = std::min(n_waves, lanes_cfg());
   LaneResources& res = lane_resources();
-  cudaStream_t streams[kLanes] = {st, res.aux};
+  cudaStream_t streams[kMaxLanes] = {st, res.aux[0], res.aux[1], res.aux[2]};
   if (lanes > 1) {
     cudaError_t e = cudaEventRecord(res.fork, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(res.aux, res.fork, 0);
+    for (int l = 1; l < lanes && e == cudaSuccess; ++l) e = cudaStreamWaitEvent(streams[l], res.fork, 0);
     if (e != cudaSuccess) return e;
   }
   for (int w = 0; w < n_waves; ++w) {
@@ -103,9 +116,9 @@ cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* s
     e = launch_inverse(M, y, g, tile0, nvalid, ldm, s);
     if (e != cudaSuccess) return e;
   }
-  if (lanes > 1) {
-    cudaError_t e = cudaEventRecord(res.join, res.aux);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, res.join, 0);
+  for (int l = 1; l < lanes; ++l) {
+    cudaError_t e = cudaEventRecord(res.join[l - 1], streams[l]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, res.join[l - 1], 0);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
