@@ -99,9 +99,7 @@ struct Params {
   Geo g;
   int NU, NM, L2;
   int passes;
-  int dbg;                // tuning aid (WF_WS_DBG)
-  int pf_ahead;           // F units whose input rows are prefetched into L2 this many units ahead (WF_WS_PF)
-  int discard;            // drop consumed U / M ring lines from L2 (WF_WS_DISCARD, default off)
+  int dbg;                // tuning aid (WF_WS_DBG=3: no GEMM work, results invalid)
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
   int grid;
@@ -190,16 +188,6 @@ __device__ __forceinline__ int atom_acqrel_cta_smem(int* p, int v) {
   int old;
   asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
   return old;
-}
-// Invalidate one 128-byte L2 line without write-back: ring data that its
-// single consumer has copied into shared memory is dead, so it should
-// neither cost a DRAM write-back nor push live ring lines out of L2.
-__device__ __forceinline__ void discard_l2(const void* p) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
-// Pull a global range into L2 ahead of its bulk copy (no shared memory).
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 // Register re-distribution between warpgroups (all 4 warps of a group run it).
 template <uint32_t N> __device__ __forceinline__ void regs_dec() {
@@ -335,27 +323,6 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       }
     }
     __syncwarp();
-    // the 2-slot ring hides one unit of copy latency; input rows come from
-    // HBM, so the rows of the unit PF_AHEAD units ahead are pulled into L2 now
-    if (P.pf_ahead > 0 && u + P.pf_ahead * P.grid < P.n_fi) {
-      int k2, b2, s2;
-      wk.decode(P, u + P.pf_ahead * P.grid, k2, b2, s2);
-      if (k2 == 0) {
-        const int part = s2 / (S::C / kCPC), cg = s2 % (S::C / kCPC);
-        const int t0 = b2 * kBlockTiles + part * kFT;
-        const int tlast = min(t0 + kFT, g.n_tile) - 1;
-        if (tlast >= t0) {
-          const FGeo fg(g, t0, tlast);
-          for (int cu = lane; cu < kCPC * fg.nseg; cu += 32) {
-            const int k = cu / kCPC, cl = cu - k * kCPC;
-            const uint32_t bytes = static_cast<uint32_t>(fg.rows(k) * g.W * 4);
-            if (bytes)
-              prefetch_l2(P.x + ((static_cast<size_t>(fg.bi0 + k) * g.C + cg * kCPC + cl) * g.H + (k == 0 ? fg.ya0 : 0)) * g.W,
-                          bytes);
-          }
-        }
-      }
-    }
     pf.add(kind == 0 ? kFPBusy : kFPBusyI, tb);
   }
   pf.end(kEndFP);
@@ -455,10 +422,6 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           bt6_line<PairOps>(w[0][s], w[1][s], w[2][s], w[3][s], w[4][s], w[5][s]);
 #pragma unroll
           for (int r = 0; r < kT; ++r) {
-            if (P.dbg == 1) {    // tuning aid: raw f32 pair stores, no split (results invalid)
-              if (live) *reinterpret_cast<float2*>(dst + (r * kT + s) * S::kUPos) = w[r][s];
-              continue;
-            }
             uint32_t hi, lo;
             split_bf16x2(w[r][s], hi, lo);
             const uint32_t other = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 8);
@@ -593,8 +556,7 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
 // ---------------------------------------------------------------- G issuer
 template <class S, bool PROF>
 __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
-  // the whole warp runs the loop (its lanes may drop the consumed U lines
-  // from L2); lane 0 issues the MMAs
+  // the whole warp runs the loop; lane 0 issues the MMAs
   const int lane = threadIdx.x & 31;
   const uint32_t idesc = idesc_bf16(kBlockTiles, kN);
   const ProfT<PROF> pf(P.prof);
@@ -604,7 +566,6 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   int a_it = 0, k = 0;
   for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
     const int buf = k % kNAcc;
-    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot;
     long long t0 = pf.now();
     mbar_wait(&sy.tempty[buf], ((k / kNAcc) & 1) ^ 1);
     pf.add(kGITempty, t0);
@@ -616,15 +577,6 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
       mbar_wait(&sy.a_full[st], (a_it / S::kAStages) & 1);
       pf.add(kGIFull, t2);
       tc_fence_after();
-      if (P.discard) {
-        // the stage's hi and lo half-K blocks (2 x 8 KB = 128 lines) are in smem now
-        const uint8_t* asrc = uslot + gu.p * S::kUPos + kb * S::kAHalf;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          discard_l2(asrc + (lane + 32 * i) * 128);
-          discard_l2(asrc + S::kKB * S::kAHalf + (lane + 32 * i) * 128);
-        }
-      }
       __syncwarp();
       if (lane == 0) {
         const uint32_t sa = smem_u32(smem + st * S::kAStage);
@@ -928,12 +880,8 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.g = g;
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
-  P.pf_ahead = 0;   // measured neutral on c2
-  if (const char* e = getenv("WF_WS_PF")) P.pf_ahead = atoi(e);
   P.dbg = 0;
   if (const char* e = getenv("WF_WS_DBG")) P.dbg = atoi(e);
-  P.discard = 0;   // measured neutral-to-slower on c2
-  if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.plane = pl.plane;
   P.grid = sm_count;
   P.prof = 0;
