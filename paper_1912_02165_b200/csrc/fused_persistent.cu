@@ -759,7 +759,10 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   pl.cpc = cpc;
   pl.ftiles = pl.nt / (pl.cpc / 2);        // ftiles x cpc/2 pairs = nt threads
   if (pl.ftiles > kBlockTiles) return pl;
-  if (g.Cpad % pl.cpc != 0 || g.Cppad > 128) return pl;
+  // up to C' = 256 (one CTA per SM, two GEMM stages; measured VGG 256->256@56
+  // 332 -> 313 us against the L2 waves); WF_PERSIST_MAX_CP overrides
+  const int max_cppad = getenv("WF_PERSIST_MAX_CP") ? atoi(getenv("WF_PERSIST_MAX_CP")) : 256;
+  if (g.Cpad % pl.cpc != 0 || g.Cppad > max_cppad) return pl;
   pl.gp = (512 / pl.cps) / g.Cppad;
   if (pl.gp > 8) pl.gp = 8;
   if (const char* env = getenv("WF_GP")) pl.gp = std::max(1, std::min(pl.gp, atoi(env)));
@@ -782,7 +785,11 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   pl.f_max_rows = pl.cpc * pl.trows * g.T;
   pl.f_desc_off = round_up(pl.cpc * pl.plane * 4, 16);
   const size_t f_smem = pl.f_desc_off + static_cast<size_t>(pl.f_max_rows) * 12;
-  const size_t g_smem = pl.stages * (2 * kBlockTiles * kKBlock * 2 + 2 * static_cast<size_t>(g.Cppad) * kKBlock * 2);
+  size_t g_smem = pl.stages * (2 * kBlockTiles * kKBlock * 2 + 2 * static_cast<size_t>(g.Cppad) * kKBlock * 2);
+  if (pl.cps == 1 && g_smem > 200u * 1024) {           // wide C': two stages
+    pl.stages = 2;
+    g_smem = pl.stages * (2 * kBlockTiles * kKBlock * 2 + 2 * static_cast<size_t>(g.Cppad) * kKBlock * 2);
+  }
   pl.smem = f_smem > g_smem ? f_smem : g_smem;
   if (pl.smem > (pl.cps == 2 ? 108u : 200u) * 1024) return pl;
   pl.u_slot = static_cast<size_t>(g.T) * g.T * 2 * kBlockTiles * g.Cpad * 2;

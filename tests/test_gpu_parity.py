@@ -264,7 +264,8 @@ def test_persistent_kernel_forced_on_small_layers(t, monkeypatch):
     dataflow kernel (WF_PERSIST_MIN_BLOCKS=1) and check it on ragged shapes:
     bitwise equal to three-stage, within tolerance of FP64."""
     monkeypatch.setenv("WF_PERSIST_MIN_BLOCKS", "1")
-    for dims in [(2, 20, 24, 13, 11, 3, 1, 0), (3, 64, 64, 30, 28, 3, 1, 1), (1, 130, 40, 17, 20, 3, 0, 1)]:
+    for dims in [(2, 20, 24, 13, 11, 3, 1, 0), (3, 64, 64, 30, 28, 3, 1, 1), (1, 130, 40, 17, 20, 3, 0, 1),
+                 (1, 256, 256, 12, 16, 3, 1, 1)]:
         spec = wf.LayerSpec(*dims)
         rng = np.random.default_rng(t)
         x = rng.standard_normal(spec.input_dims()).astype(np.float32)
