@@ -99,6 +99,7 @@ struct Params {
   Geo g;
   int NU, NM, L2;
   int passes;
+  int discard;            // drop consumed U / M ring lines from L2 (WF_WS_DISCARD)
   int dbg;                // tuning aid (WF_WS_DBG=3: no GEMM work, results invalid)
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
@@ -189,6 +190,12 @@ __device__ __forceinline__ int atom_acqrel_cta_smem(int* p, int v) {
   asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
   return old;
 }
+// Invalidate one 128-byte L2 line without write-back: ring data whose single
+// consumer has copied it into shared memory is dead, so it should neither
+// cost a DRAM write-back nor push live ring lines out of L2.
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 // Register re-distribution between warpgroups (all 4 warps of a group run it).
 template <uint32_t N> __device__ __forceinline__ void regs_dec() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
@@ -263,6 +270,10 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
   const ProfT<PROF> pf(P.prof && lane == 0);
   FIWalker<S> wk;
   wk.init(P);
+  // products staged into each slot by an I unit (their L2 lines are dropped
+  // once the workers have released the slot: they have no other reader)
+  const uint8_t* staged_m0 = nullptr;   // slot 0
+  const uint8_t* staged_m1 = nullptr;   // slot 1
   int it = 0;
   for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
     int kind, b, sub;
@@ -282,12 +293,20 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       mbar_wait(&sy.fi_empty[slot], ((it >> 1) & 1) ^ 1);
       pf.add(kFPSlot, t0);
     }
+    if (P.discard) {
+      const uint8_t* dead = slot ? staged_m1 : staged_m0;
+      __syncwarp();
+      if (dead)
+        for (int i = lane; i < static_cast<int>(kMUnit / 128); i += 32) discard_l2(dead + static_cast<size_t>(i) * 128);
+    }
     const long long tb = pf.now();
     // (no proxy fence: the slot is only ever written by bulk copies; the
     // workers' generic reads of its previous contents are ordered before
     // these writes by the fi_empty barrier)
     __syncwarp();
     if (kind == 0) {
+      if (slot) staged_m1 = nullptr;
+      else staged_m0 = nullptr;
       const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
       const int t0 = b * kBlockTiles + part * kFT;
       const int tlast = min(t0 + kFT, g.n_tile) - 1;
@@ -316,6 +335,8 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       // the unit's products are one contiguous range: two 36 KB copies
       const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * S::kMSlot +
                             static_cast<size_t>(sub) * kMUnit;
+      if (slot) staged_m1 = msrc;
+      else staged_m0 = msrc;
       if (lane == 0) {
         mbar_expect_tx(&sy.fi_full[slot], kMUnit);       // the arrival, with the byte count
         bulk_g2s(dstbase, msrc, kMUnit / 2, &sy.fi_full[slot]);
@@ -348,6 +369,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     pf.add(kFWWait, t0);
     t0 = pf.now();
     if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
+
     if (kind == 0) {
       // ---- F(b, sub): thread = (tile tl, channel pair q); a warp = 8 tiles
       // (one core-matrix row group) x 4 pairs (one 8-channel k group), so
@@ -566,6 +588,7 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   int a_it = 0, k = 0;
   for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
     const int buf = k % kNAcc;
+    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + gu.p * S::kUPos;
     long long t0 = pf.now();
     mbar_wait(&sy.tempty[buf], ((k / kNAcc) & 1) ^ 1);
     pf.add(kGITempty, t0);
@@ -577,6 +600,12 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
       mbar_wait(&sy.a_full[st], (a_it / S::kAStages) & 1);
       pf.add(kGIFull, t2);
       tc_fence_after();
+      if (P.discard && S::kNG == 1) {
+        // this K block of U (hi and lo) is in smem and nobody else reads it
+        // (one G unit per position when C' = 64)
+        for (int i = lane; i < 2 * static_cast<int>(S::kAHalf / 128); i += 32)
+          discard_l2(uslot + kb * S::kAHalf + (i & 1) * S::kKB * S::kAHalf + (i >> 1) * 128);
+      }
       __syncwarp();
       if (lane == 0) {
         const uint32_t sa = smem_u32(smem + st * S::kAStage);
@@ -880,6 +909,11 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.g = g;
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
+  // consumed U / M ring lines are dropped from L2 (discard.global.L2): c2
+  // DRAM traffic 282 -> 94 MB (dead ring lines are no longer written back)
+  // for ~1 us; WF_WS_DISCARD=0 turns it off
+  P.discard = 1;
+  if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.dbg = 0;
   if (const char* e = getenv("WF_WS_DBG")) P.dbg = atoi(e);
   P.plane = pl.plane;
