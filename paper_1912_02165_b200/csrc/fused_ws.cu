@@ -99,7 +99,7 @@ struct Params {
   Geo g;
   int NU, NM, L2;
   int passes;
-  int discard;            // drop consumed U / M ring lines from L2 (WF_WS_DISCARD)
+  int discard;            // drop consumed ring lines from L2 (WF_WS_DISCARD bits: 1 U, 2 M)
   int dbg;                // tuning aid (WF_WS_DBG=3: no GEMM work, results invalid)
   int plane;              // floats per staged channel of an F unit
   int n_fi;               // F/I queue length
@@ -270,10 +270,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
   const ProfT<PROF> pf(P.prof && lane == 0);
   FIWalker<S> wk;
   wk.init(P);
-  // products staged into each slot by an I unit (their L2 lines are dropped
-  // once the workers have released the slot: they have no other reader)
-  const uint8_t* staged_m0 = nullptr;   // slot 0
-  const uint8_t* staged_m1 = nullptr;   // slot 1
+
   int it = 0;
   for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
     int kind, b, sub;
@@ -293,20 +290,13 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       mbar_wait(&sy.fi_empty[slot], ((it >> 1) & 1) ^ 1);
       pf.add(kFPSlot, t0);
     }
-    if (P.discard) {
-      const uint8_t* dead = slot ? staged_m1 : staged_m0;
-      __syncwarp();
-      if (dead)
-        for (int i = lane; i < static_cast<int>(kMUnit / 128); i += 32) discard_l2(dead + static_cast<size_t>(i) * 128);
-    }
+
     const long long tb = pf.now();
     // (no proxy fence: the slot is only ever written by bulk copies; the
     // workers' generic reads of its previous contents are ordered before
     // these writes by the fi_empty barrier)
     __syncwarp();
     if (kind == 0) {
-      if (slot) staged_m1 = nullptr;
-      else staged_m0 = nullptr;
       const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
       const int t0 = b * kBlockTiles + part * kFT;
       const int tlast = min(t0 + kFT, g.n_tile) - 1;
@@ -335,8 +325,6 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       // the unit's products are one contiguous range: two 36 KB copies
       const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * S::kMSlot +
                             static_cast<size_t>(sub) * kMUnit;
-      if (slot) staged_m1 = msrc;
-      else staged_m0 = msrc;
       if (lane == 0) {
         mbar_expect_tx(&sy.fi_full[slot], kMUnit);       // the arrival, with the byte count
         bulk_g2s(dstbase, msrc, kMUnit / 2, &sy.fi_full[slot]);
@@ -588,7 +576,6 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   int a_it = 0, k = 0;
   for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
     const int buf = k % kNAcc;
-    const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + gu.p * S::kUPos;
     long long t0 = pf.now();
     mbar_wait(&sy.tempty[buf], ((k / kNAcc) & 1) ^ 1);
     pf.add(kGITempty, t0);
@@ -600,12 +587,6 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
       mbar_wait(&sy.a_full[st], (a_it / S::kAStages) & 1);
       pf.add(kGIFull, t2);
       tc_fence_after();
-      if (P.discard && S::kNG == 1) {
-        // this K block of U (hi and lo) is in smem and nobody else reads it
-        // (one G unit per position when C' = 64)
-        for (int i = lane; i < 2 * static_cast<int>(S::kAHalf / 128); i += 32)
-          discard_l2(uslot + kb * S::kAHalf + (i & 1) * S::kKB * S::kAHalf + (i >> 1) * 128);
-      }
       __syncwarp();
       if (lane == 0) {
         const uint32_t sa = smem_u32(smem + st * S::kAStage);
@@ -676,6 +657,14 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
       pf.add(kGEBusy, t0);
     }
     tc_fence_before();
+    if ((P.discard & 1) && S::kNG == 1) {
+      // the unit's U (one position, read by this unit only when C' = 64) is
+      // dead: drop its L2 lines before the unit is published (publishing
+      // lets the next F units of the ring slot write it again)
+      const uint8_t* u = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + gg * S::kUPos;
+      constexpr int lines = static_cast<int>(S::kUPos / 128);
+      for (int i = qd * 32 + lane; i < lines; i += 128) discard_l2(u + static_cast<size_t>(i) * 128);
+    }
     __syncwarp();
     if (lane == 0) {
       // the last of the 4 epilogue warps to finish publishes the unit (counted
@@ -696,30 +685,35 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
 // --------------------------------------------------------------- publisher
 template <class S, bool PROF>
 __device__ void publisher(const Params& P, Sync& sy, int n_g) {
-  if ((threadIdx.x & 31) != 0) return;
-  const ProfT<PROF> pf(P.prof);
+  // lane 0 polls and publishes; for I units the whole warp first drops the
+  // unit's products from L2 (dead once staged; dropped before the release
+  // that lets G units of a later block write the ring slot again)
+  const int lane = threadIdx.x & 31;
+  const ProfT<PROF> pf(P.prof && lane == 0);
   int* doneF = P.counters;
-  int* doneG = doneF + P.g.n_blk;
-  int* doneI = doneG + P.g.n_blk;
+  int* doneI = doneF + 2 * P.g.n_blk;
   FIWalker<S> wk;
   wk.init(P);
-  int uf = blockIdx.x, kf = 0;        // next F/I unit of this CTA, its ordinal
-  int vg = blockIdx.x, kg = 0;        // next G unit, its ordinal
-  while (uf < P.n_fi) {
-    bool progress = false;
-    if (uf < P.n_fi && ld_acquire_cta_smem(&sy.fi_cnt[kf & 3]) >= 8 * ((kf >> 2) + 1)) {
-      int kind, b, sub;
-      wk.decode(P, uf, kind, b, sub);
+  int kf = 0;
+  for (int uf = blockIdx.x; uf < P.n_fi; uf += P.grid, ++kf) {
+    if (lane == 0)
+      while (ld_acquire_cta_smem(&sy.fi_cnt[kf & 3]) < 8 * ((kf >> 2) + 1)) __nanosleep(32);
+    __syncwarp();
+    int kind, b, sub;
+    wk.decode(P, uf, kind, b, sub);
+    if (kind == 2 && (P.discard & 2)) {
+      const uint8_t* m = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * S::kMSlot +
+                         static_cast<size_t>(sub) * kMUnit;
+      for (int i = lane; i < static_cast<int>(kMUnit / 128); i += 32) discard_l2(m + static_cast<size_t>(i) * 128);
+      __syncwarp();
+    }
+    if (lane == 0) {
       const long long t0 = pf.now();
       red_release_gpu((kind == 0 ? doneF : doneI) + b, 1);
       pf.add(kPubFence, t0);
-      uf += P.grid;
-      ++kf;
-      progress = true;
     }
-    (void)vg; (void)kg; (void)doneG;
-    if (!progress) __nanosleep(32);
   }
+  (void)n_g;
   pf.end(kEndPub);
 }
 
@@ -909,9 +903,11 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.g = g;
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
-  // consumed U / M ring lines are dropped from L2 (discard.global.L2): c2
-  // DRAM traffic 282 -> 94 MB (dead ring lines are no longer written back)
-  // for ~1 us; WF_WS_DISCARD=0 turns it off
+  // consumed ring lines dropped from L2 (discard.global.L2) instead of being
+  // written back dead (measured on c2, ncu DRAM bytes / time): none 281 MB;
+  // U only (by the epilogue warps, default) 175 MB at the same time; M only
+  // (by the publisher) 212 MB, same time; both 99 MB but +2-4 us (the M
+  // discards delay the I publishes)
   P.discard = 1;
   if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.dbg = 0;
