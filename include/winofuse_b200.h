@@ -88,6 +88,17 @@ int wf_conv_fused(const float* x, const void* mma_pack, float* y, void* scratch,
                   size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
                   int precision, int r, void* stream);
 
+/* wf_conv_fused for a caller that owns `scratch` for this one layer (a
+ * planned layer, engines.LayerPlan): with WF_FUSED_COUNTERS_CLEAN the caller
+ * asserts that the scratch's dependency counters are zero -- it zeroed the
+ * scratch once and only calls this layer's fused engine on it -- and the
+ * per-call counter reset is skipped (the kernel leaves them zero again).
+ * Same results as wf_conv_fused. */
+#define WF_FUSED_COUNTERS_CLEAN 1
+int wf_conv_fused_planned(const float* x, const void* mma_pack, float* y, void* scratch,
+                          size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
+                          int precision, int flags, void* stream);
+
 /* conv_direct (winofuse/engines.py:213-231, kernels.py:22-49): 7-loop
  * cross-correlation with float64 accumulation, one f32 store. */
 int wf_conv_direct(const float* x, const float* w, float* y, const wf_layer* layer, void* stream);

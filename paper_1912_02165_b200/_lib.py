@@ -50,6 +50,7 @@ SIGNATURES = {
     "wf_conv_three_stage": (_i, [_fp, _vp, _fp, _vp, _sz, _LP, _i, _i, _i, _vp]),
     "wf_fused_scratch_bytes": (_sz, [_LP, _i, _i, _i]),
     "wf_conv_fused": (_i, [_fp, _vp, _fp, _vp, _sz, _LP, _i, _i, _i, _i, _vp]),
+    "wf_conv_fused_planned": (_i, [_fp, _vp, _fp, _vp, _sz, _LP, _i, _i, _i, _i, _vp]),
     "wf_conv_direct": (_i, [_fp, _fp, _fp, _LP, _vp]),
     "wf_forward_tiles": (_i, [_fp, _fp, _LP, _i, _i, _i, _i, _i, _vp]),
     "wf_multiply_positions": (_i, [_fp, _fp, _fp, _i, _i, _i, _i, _i, _vp]),

@@ -346,8 +346,25 @@ size_t wf_fused_scratch_bytes(const wf_layer* layer, int tile, int transform, in
   return fused_scratch_bytes(g, r);
 }
 
+static int conv_fused_impl(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
+                           const wf_layer* layer, int tile, int transform, int precision, int r, bool clean,
+                           void* stream);
+
 int wf_conv_fused(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
                   const wf_layer* layer, int tile, int transform, int precision, int r, void* stream) {
+  return conv_fused_impl(x, mma_pack, y, scratch, scratch_bytes, layer, tile, transform, precision, r, false, stream);
+}
+
+int wf_conv_fused_planned(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
+                          const wf_layer* layer, int tile, int transform, int precision, int flags, void* stream) {
+  if (flags & ~WF_FUSED_COUNTERS_CLEAN) return fail(WF_ERR_PARAM, "flags %d", flags);
+  return conv_fused_impl(x, mma_pack, y, scratch, scratch_bytes, layer, tile, transform, precision, 0,
+                         (flags & WF_FUSED_COUNTERS_CLEAN) != 0, stream);
+}
+
+static int conv_fused_impl(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
+                           const wf_layer* layer, int tile, int transform, int precision, int r, bool clean,
+                           void* stream) {
   Geo g;
   int rc = make_geo(layer, tile, transform, g);
   if (rc != WF_OK) return rc;
@@ -358,7 +375,7 @@ int wf_conv_fused(const float* x, const void* mma_pack, float* y, void* scratch,
   if (need && (!scratch || scratch_bytes < need))
     return fail(WF_ERR_SCRATCH, "scratch %zu < %zu bytes", scratch_bytes, need);
   cudaError_t e = run_fused(x, static_cast<const uint8_t*>(mma_pack), y, static_cast<uint8_t*>(scratch), g,
-                            precision == WF_PREC_3XBF16 ? 3 : 1, r, sm_count(), static_cast<cudaStream_t>(stream));
+                            precision == WF_PREC_3XBF16 ? 3 : 1, r, sm_count(), static_cast<cudaStream_t>(stream), clean);
   return e == cudaSuccess ? WF_OK : cuda_fail(e, "fused");
 }
 

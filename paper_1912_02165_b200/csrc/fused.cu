@@ -83,9 +83,37 @@ static LaneResources& lane_resources() {
   return r;
 }
 
+// Scratch buffers whose last fused launch was a warp-specialised kernel of
+// the same geometry (which leaves its counters zero).  A caller that owns its
+// scratch (counters_clean) skips the counter reset only when this says the
+// previous launch on that scratch left them clean -- a different kernel or
+// layer in between (environment overrides, shared scratch) forces a reset.
+struct CleanScratch {
+  const void* ptr;
+  size_t key;
+};
+static bool scratch_clean_then_mark(const void* ptr, size_t key, bool clean_after) {
+  static CleanScratch slots[64] = {};
+  static int next = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  bool was = false;
+  int hit = -1;
+  for (int i = 0; i < 64; ++i)
+    if (slots[i].ptr == ptr) { hit = i; was = slots[i].key == key; break; }
+  if (hit < 0) { hit = next; next = (next + 1) % 64; }
+  slots[hit].ptr = ptr;
+  slots[hit].key = clean_after ? key : 0;
+  return was;
+}
+
 cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
-                      int passes, int /*r*/, int sm_count, cudaStream_t st) {
-  if (ws_fits(g)) return run_fused_ws(x, vpack, y, scratch, g, passes, sm_count, st);
+                      int passes, int /*r*/, int sm_count, cudaStream_t st, bool counters_clean) {
+  const bool ws = ws_fits(g);
+  // geometry key of the warp-specialised launch (its counters' extent)
+  const size_t key = ws ? (static_cast<size_t>(g.n_blk) << 20) ^ (static_cast<size_t>(g.C) << 10) ^ g.Cp ^ 1 : 0;
+  const bool clean = counters_clean && scratch_clean_then_mark(scratch, key, ws) && ws;
+  if (ws) return run_fused_ws(x, vpack, y, scratch, g, passes, sm_count, st, clean);
   if (persistent_fits(g)) return run_fused_persistent(x, vpack, y, scratch, g, passes, sm_count, st);
   const int wb = wave_blocks(g);
   const size_t P = static_cast<size_t>(g.P);

@@ -16,9 +16,11 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
 // Warp-specialised persistent kernel (fused_ws.cu): F(4x4,3x3), C = C' = 64.
 bool ws_fits(const Geo& g);
 size_t ws_scratch_bytes(const Geo& g);
+// counters_clean: the scratch's counters are known to be zero (the kernel
+// leaves them zero when it finishes), so the memset is skipped
 cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g, int passes,
-                         int sm_count, cudaStream_t st);
+                         int sm_count, cudaStream_t st, bool counters_clean = false);
 cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
-                      int passes, int r, int sm_count, cudaStream_t st);
+                      int passes, int r, int sm_count, cudaStream_t st, bool counters_clean = false);
 
 }  // namespace wf

@@ -784,6 +784,22 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
     tc_fence_after();
     tmem_dealloc<512>(sy.tmem);
   }
+  // The last CTA to finish zeroes the dependency counters, so a caller that
+  // owns this scratch can skip the memset before the next launch
+  // (wf_conv_fused_planned).  Every CTA finished all its counter accesses
+  // before its release increment; the last one acquires them all.
+  {
+    __shared__ int last;
+    int* done = P.counters + 3 * P.g.n_blk;
+    if (tid == 0) {
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(done) : "memory");
+      last = old == P.grid - 1;
+    }
+    __syncthreads();
+    if (last)
+      for (int i = tid; i <= 3 * P.g.n_blk; i += NT) P.counters[i] = 0;
+  }
   if (PROF && tid < kProfSlots && (tid < kStart || tid > kEndPub)) g_wsprof[blockIdx.x * kProfSlots + tid] += s_prof[tid];
 }
 
@@ -825,7 +841,7 @@ static Plan plan_t(const Geo& g) {
   if (lag < 2) lag = 2;
   pl.L2 = lag;
   if (pl.NU < 2 && pl.NU < g.n_blk) return pl;
-  pl.counters_bytes = static_cast<size_t>(3 * g.n_blk) * sizeof(int);
+  pl.counters_bytes = static_cast<size_t>(3 * g.n_blk + 1) * sizeof(int);   // + finished-CTA count
   pl.u_slot = S::kUSlot;
   pl.m_slot = S::kMSlot;
   pl.ok = true;
@@ -892,7 +908,7 @@ size_t ws_scratch_bytes(const Geo& g) {
 }
 
 cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g, int passes,
-                         int sm_count, cudaStream_t st) {
+                         int sm_count, cudaStream_t st, bool counters_clean) {
   const ws::Plan pl = ws::plan(g);
   if (!pl.ok) return cudaErrorInvalidValue;
   ws::Params P;
@@ -916,8 +932,10 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.grid = sm_count;
   P.prof = 0;
   if (const char* e = getenv("WF_WS_PROF")) P.prof = atoi(e);
-  cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
-  if (e != cudaSuccess) return e;
+  if (!counters_clean) {
+    cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
+    if (e != cudaSuccess) return e;
+  }
   return ws::with_shape(g, [&](auto s) {
     using S = decltype(s);
     P.n_fi = g.n_blk * (S::kNCG + S::kNIG);

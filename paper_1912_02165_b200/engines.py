@@ -418,8 +418,13 @@ class LayerPlan:
             self.nbytes = int(self.lib.wf_three_stage_scratch_bytes(self.layer, cfg.tile, self.tf))
         if scratch is not None and scratch.numel() >= self.nbytes:
             self.scratch = scratch                    # shared with other plans on the same stream
+            self.flags = 0
         else:
+            # private scratch: the warp-specialised kernel leaves its
+            # dependency counters zero, so repeated calls skip the per-call
+            # reset (wf_conv_fused_planned, WF_FUSED_COUNTERS_CLEAN)
             self.scratch = _dev.torch.empty(max(self.nbytes, 16), dtype=_dev.torch.uint8, device=self.dev)
+            self.flags = 1
         self.vpack = self.pack.device_mma(self.dev)
         self.out = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=self.dev)
 
@@ -428,8 +433,9 @@ class LayerPlan:
         y = self.out if out is None else out
         stream = _dev.stream_ptr(self.dev)
         if self.cfg.kind == "fused":
-            rc = self.lib.wf_conv_fused(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y), _dev.ptr(self.scratch),
-                                        self.nbytes, self.layer, self.cfg.tile, self.tf, self.prec, 0, stream)
+            rc = self.lib.wf_conv_fused_planned(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y),
+                                                _dev.ptr(self.scratch), self.nbytes, self.layer, self.cfg.tile,
+                                                self.tf, self.prec, self.flags, stream)
         else:
             rc = self.lib.wf_conv_three_stage(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y),
                                               _dev.ptr(self.scratch), self.nbytes, self.layer, self.cfg.tile,

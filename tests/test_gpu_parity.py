@@ -333,3 +333,29 @@ def test_warp_specialised_kernel(dims, monkeypatch):
     monkeypatch.setenv("WF_PERSIST_MIN_BLOCKS", "1")
     q, _ = _run("fused", x, pack, spec, 6)
     assert np.array_equal(q, s), dims
+
+
+def test_planned_layer_skips_counter_reset_safely(monkeypatch):
+    """LayerPlan calls wf_conv_fused_planned: the warp-specialised kernel
+    leaves its dependency counters zero and repeated calls skip the reset;
+    switching the kernel under the same scratch (WF_WS=0 between calls)
+    must force the reset again.  Every call stays bitwise equal."""
+    import torch
+    spec = wf.LayerSpec(4, 64, 64, 56, 56, 3, 1, 1)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
+    ref, _ = _run("three_stage", x, pack, spec, 6)
+    dev = torch.device("cuda", 0)
+    # planned under WF_WS=0: the item-queue kernel's scratch is the larger one
+    monkeypatch.setenv("WF_WS", "0")
+    plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=6, device=dev))
+    xd = torch.from_numpy(x).to(dev)
+    for env in (None, None, None, "0", None, "0", "0", None, None):
+        if env is None:
+            monkeypatch.delenv("WF_WS", raising=False)
+        else:
+            monkeypatch.setenv("WF_WS", env)
+        y = plan(xd).cpu().numpy()
+        assert np.array_equal(y, ref), env
