@@ -41,8 +41,6 @@ constexpr uint32_t kRegsLight = WF_WS_REGS ? 40 : 128;
 constexpr uint32_t kRegsEpi = WF_WS_REGS ? 64 : 128;
 constexpr uint32_t kRegsFI = WF_WS_REGS ? 200 : 128;
 static_assert(4 * 32 * kRegsLight + 4 * 32 * kRegsEpi + 8 * 32 * kRegsFI <= 65536, "register file");
-constexpr int kT = 6;
-constexpr int kP = kT * kT;
 #ifndef WF_WS_GP
 #define WF_WS_GP 1
 #endif
@@ -50,22 +48,27 @@ constexpr int kGP = WF_WS_GP;                            // positions per G unit
 static_assert(kGP == 1, "G units own one position (position-affine CTAs keep V resident)");
 constexpr int kN = 64;                                   // output channels per G unit (MMA N)
 constexpr int kNAcc = 512 / (kGP * kN);                  // TMEM accumulator buffers (units in flight)
-constexpr int kCPC = 8;                                  // channels per F unit
 constexpr int kFT = 64;                                  // tiles per F unit
-constexpr int kIPairs = 2;                               // c' pairs per I unit
 constexpr int kMaxAStages = 4;
-// M ring slot layout: [I unit (c' group of 4)][position][c' pair (2)][tile][2]:
-// the products one I unit needs are one contiguous 72 KB range (one bulk copy)
-constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;    // 2 KB staged per position (I unit)
-constexpr uint32_t kMUnit = kP * kIPos;                  // 72 KB: the products of one I unit
 constexpr uint32_t kFISlot = 72 * 1024;                  // F staging or I staging
 
-// Channel shape: C input channels (GEMM K, 32-channel K blocks), CP output
-// channels (GEMM N, 64-wide G units).  Shared memory: A stages + the V slab
-// of the CTA's (position, c' group) + two 72 KB F/I slots <= 227 KB.
-template <int C_, int CP_>
+// Layer shape: window T (6: F(4x4,3x3), 8: F(6x6,3x3)), C input channels
+// (GEMM K, 32-channel K blocks), CP output channels (GEMM N, 64-wide G
+// units).  Shared memory: A stages + the V slab of the CTA's (position, c'
+// group) + two 72 KB F/I slots <= 227 KB.
+template <int T_, int C_, int CP_>
 struct Shape {
+  static constexpr int kT = T_, kP = T_ * T_;
   static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
+  // F unit: 64 tiles x kCPC channels (thread = tile x channel pair for T = 6,
+  // tile x channel for T = 8, whose larger windows halve the channels staged)
+  static constexpr int kCPC = T_ == 6 ? 8 : 4;
+  // I unit: kIPairs c' pairs.  M ring slot layout: [I unit][position][c' pair
+  // in unit][tile][2]: the products one I unit needs are one contiguous
+  // range (72 KB for T = 6, 64 KB for T = 8) -- one bulk copy
+  static constexpr int kIPairs = T_ == 6 ? 2 : 1;
+  static constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;
+  static constexpr uint32_t kMUnit = kP * kIPos;
   static constexpr int kKBW = C < 32 ? C : 32;           // K block width (channels per A stage)
   static constexpr int kKB = C / kKBW;                   // K blocks
   static constexpr uint32_t kAHalf = kBlockTiles * kKBW * 2;   // hi or lo of one K block
@@ -87,6 +90,7 @@ struct Shape {
   static constexpr uint32_t kOffFI = kOffB + kVGroup;
   static constexpr uint32_t kSmem = kOffFI + 2 * kFISlot;
   static_assert(kSmem <= 227 * 1024 && kAStages <= kMaxAStages && C % 16 == 0 && CP % kN == 0, "shape");
+  static_assert((T_ == 6 || T_ == 8) && kMUnit <= kFISlot, "window");
 };
 
 struct Params {
@@ -249,10 +253,10 @@ struct FGeo {
     const int bi1 = gr1 / g.tiles_y;
     const int ty0 = gr0 - bi0 * g.tiles_y, ty1 = gr1 - bi1 * g.tiles_y;
     ya0 = ty0 * g.m - g.pad_lo > 0 ? ty0 * g.m - g.pad_lo : 0;
-    rows_full = min(g.H, (g.tiles_y - 1) * g.m - g.pad_lo + kT);
+    rows_full = min(g.H, (g.tiles_y - 1) * g.m - g.pad_lo + g.T);
     nseg = bi1 - bi0 + 1;
-    rows0 = (nseg == 1 ? min(g.H, ty1 * g.m - g.pad_lo + kT) : rows_full) - ya0;
-    rows_last = nseg == 1 ? 0 : min(g.H, ty1 * g.m - g.pad_lo + kT);
+    rows0 = (nseg == 1 ? min(g.H, ty1 * g.m - g.pad_lo + g.T) : rows_full) - ya0;
+    rows_last = nseg == 1 ? 0 : min(g.H, ty1 * g.m - g.pad_lo + g.T);
   }
   __device__ __host__ int rowoff(int k) const { return k == 0 ? 0 : rows0 + (k - 1) * rows_full; }
   __device__ __host__ int rows(int k) const { return k == 0 ? rows0 : (k == nseg - 1 ? rows_last : rows_full); }
@@ -297,6 +301,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     // these writes by the fi_empty barrier)
     __syncwarp();
     if (kind == 0) {
+      constexpr int kCPC = S::kCPC;
       const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
       const int t0 = b * kBlockTiles + part * kFT;
       const int tlast = min(t0 + kFT, g.n_tile) - 1;
@@ -322,13 +327,14 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
         }
       }
     } else {
-      // the unit's products are one contiguous range: two 36 KB copies
+      // the unit's products are one contiguous range: two copies
       const uint8_t* msrc = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * S::kMSlot +
-                            static_cast<size_t>(sub) * kMUnit;
+                            static_cast<size_t>(sub) * S::kMUnit;
       if (lane == 0) {
-        mbar_expect_tx(&sy.fi_full[slot], kMUnit);       // the arrival, with the byte count
-        bulk_g2s(dstbase, msrc, kMUnit / 2, &sy.fi_full[slot]);
-        bulk_g2s(dstbase + kMUnit / 2, msrc + kMUnit / 2, kMUnit / 2, &sy.fi_full[slot]);
+        constexpr uint32_t half = S::kMUnit / 2;
+        mbar_expect_tx(&sy.fi_full[slot], S::kMUnit);    // the arrival, with the byte count
+        bulk_g2s(dstbase, msrc, half, &sy.fi_full[slot]);
+        bulk_g2s(dstbase + half, msrc + half, half, &sy.fi_full[slot]);
       }
     }
     __syncwarp();
@@ -338,12 +344,137 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
 }
 
 // ------------------------------------------------------------- F/I workers
+// F(6x6,3x3) units (T = 8).  The transforms are the generic ones every other
+// path of the library uses for T = 8 (common.cuh forward_transform<8>,
+// inverse_transform<8>), so the results stay bitwise equal to them.
+//
+// F(b, sub): thread = (tile tl, channel cq); a warp = 8 tiles x 4 channels
+// (half of an 8-channel core-matrix k group).  Lanes cq and cq ^ 1 swap
+// values so that the even one stores the hi and the odd one the lo bf16 of
+// both channels: one 4-byte store per position.
+template <class S>
+__device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Sync& sy, int slot, int b, int sub,
+                                        int wl, int lane) {
+  static_assert(S::kT == 8 && S::kCPC == 4, "T = 8 F unit");
+  const Geo& g = P.g;
+  constexpr int kCPC = S::kCPC;
+  const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
+  const int tb0 = part * kFT;
+  const int t0 = b * kBlockTiles + tb0;
+  const int tl = wl * 8 + (lane & 7), cq = lane >> 3;
+  const int tile = t0 + tl;
+  const bool live = tile < g.n_tile;
+  float x[8][8];
+  if (live) {
+    const FGeo fg(g, t0, min(t0 + kFT, g.n_tile) - 1);
+    const int per_img = g.tiles_y * g.tiles_x;
+    const int bi = tile / per_img;
+    const int rem = tile - bi * per_img;
+    const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+    const int y0 = ty * g.m - g.pad_lo;
+    const int x0 = tx * g.m - g.pad_lo;
+    const float* pa = reinterpret_cast<const float*>(src) + cq * P.plane + fg.srow(bi - fg.bi0, y0) * g.W + x0;
+    // window columns [x0, x0 + 8), x0 = 6 tx - 1: three 8-byte loads
+    // [x0 + 1, x0 + 7) and two scalars per row.  W is even, so every pair
+    // lies wholly inside or wholly outside the image; the padding columns
+    // and rows are zeros (their loads are predicated off)
+    const bool v0 = x0 >= 0, v3 = x0 + 3 < g.W, v5 = x0 + 5 < g.W, v7 = x0 + 7 < g.W;
+    const bool cv = S::C >= 64 || cg * kCPC + cq < g.C;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float* ra = pa + r * g.W;
+      float a0 = 0.0f, a7 = 0.0f;
+      float2 p1 = make_float2(0.0f, 0.0f), p3 = p1, p5 = p1;
+      if (cv && y0 + r >= 0 && y0 + r < g.H) {
+        if (v0) a0 = ra[0];
+        p1 = *reinterpret_cast<const float2*>(ra + 1);
+        if (v3) p3 = *reinterpret_cast<const float2*>(ra + 3);
+        if (v5) p5 = *reinterpret_cast<const float2*>(ra + 5);
+        if (v7) a7 = ra[7];
+      }
+      x[r][0] = a0;
+      x[r][1] = p1.x; x[r][2] = p1.y;
+      x[r][3] = p3.x; x[r][4] = p3.y;
+      x[r][5] = p5.x; x[r][6] = p5.y;
+      x[r][7] = a7;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) x[r][c] = 0.0f;
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window consumed: slot free
+  float u[8][8];
+  forward_transform<8>(x, u);
+  const bool odd = cq & 1;
+  const int row = tb0 + tl, c0 = cg * kCPC + (cq & ~1);
+  uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 / S::kKBW) * S::kAHalf +
+                 (row >> 3) * (16 * S::kKBW) + ((c0 % S::kKBW) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
+                 (odd ? S::kKB * S::kAHalf : 0);
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const float other = __shfl_xor_sync(0xffffffffu, u[r][s], 8);
+      uint32_t hi, lo;
+      split_bf16x2(odd ? other : u[r][s], odd ? u[r][s] : other, hi, lo);
+      if (live) *reinterpret_cast<uint32_t*>(dst + (r * 8 + s) * S::kUPos) = odd ? lo : hi;
+    }
+}
+
+// I(b, sub), T = 8: thread = (tile, c' of the unit's pair); 64 staged
+// products per thread, inverse transform, clipped 6 x 6 output block.
+template <class S>
+__device__ __forceinline__ void i_unit8(const Params& P, const uint8_t* src, Sync& sy, int slot, int b, int sub,
+                                        int wtid, int lane) {
+  static_assert(S::kT == 8 && S::kIPairs == 1, "T = 8 I unit");
+  const Geo& g = P.g;
+  const int tl = wtid & (kBlockTiles - 1), cq = wtid >> 7;
+  const int tile = b * kBlockTiles + tl;
+  const float* ms = reinterpret_cast<const float*>(src) + tl * 2 + cq;
+  float mm[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) mm[r][s] = ms[(r * 8 + s) * (S::kIPos / 4)];
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
+  float out[6][6];
+  inverse_transform<8>(mm, out);
+  if (tile < g.n_tile) {
+    const int per_img = g.tiles_y * g.tiles_x;
+    const int bi = tile / per_img;
+    const int rem = tile - bi * per_img;
+    const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+    const int oy = ty * 6, ox = tx * 6;
+    const bool vec = oy + 6 <= g.Ho && ox + 6 <= g.Wo && (g.Wo & 1) == 0;
+    const int cp = 2 * sub + cq;
+    float* ybase = P.y + ((static_cast<size_t>(bi) * g.Cp + cp) * g.Ho + oy) * g.Wo + ox;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      if (vec) {
+#pragma unroll
+        for (int c = 0; c < 6; c += 2)
+          *reinterpret_cast<float2*>(ybase + r * g.Wo + c) = make_float2(out[r][c], out[r][c + 1]);
+      } else if (oy + r < g.Ho) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          if (ox + c < g.Wo) ybase[r * g.Wo + c] = out[r][c];
+      }
+    }
+  }
+}
+
 template <class S, bool PROF>
 __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
   const Geo& g = P.g;
   const int wtid = threadIdx.x - 256, lane = threadIdx.x & 31, wl = wtid >> 5;
   const ProfT<PROF> pf(P.prof && wtid == 0);
   const long long tloop = pf.now();
+  constexpr int kT = S::kT, kCPC = S::kCPC;
+  constexpr uint32_t kIPos = S::kIPos;
   FIWalker<S> wk;
   wk.init(P);
   int it = 0;
@@ -358,7 +489,10 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     t0 = pf.now();
     if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
 
-    if (kind == 0) {
+    if constexpr (S::kT == 8) {
+      if (kind == 0) f_unit8<S>(P, src, sy, slot, b, sub, wl, lane);
+      else i_unit8<S>(P, src, sy, slot, b, sub, wtid, lane);
+    } else if (kind == 0) {
       // ---- F(b, sub): thread = (tile tl, channel pair q); a warp = 8 tiles
       // (one core-matrix row group) x 4 pairs (one 8-channel k group), so
       // every store instruction writes one contiguous 128-byte core matrix
@@ -505,11 +639,11 @@ template <class S>
 struct GUnits {
   int p, ng, b0, step;
   __device__ GUnits(const Params& P) {
-    constexpr int combos = kP * S::kNG;                  // (position, c' group) pairs
+    constexpr int combos = S::kP * S::kNG;               // (position, c' group) pairs
     step = P.grid / combos;
     const int c = blockIdx.x % combos;
-    p = c % kP;
-    ng = c / kP;
+    p = c % S::kP;
+    ng = c / S::kP;
     b0 = static_cast<int>(blockIdx.x) < step * combos ? blockIdx.x / combos : P.g.n_blk;
   }
 };
@@ -638,9 +772,9 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
       t0 = pf.now();
       tc_fence_after();
       const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (kGP * kN) + pl * kN;
-      // pair k of position p: [k / 2][p][k % 2][tile][2] (see kMUnit); this
-      // unit's 64 outputs are the pairs 32 ng .. 32 ng + 31
-      float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * kGP + pl) * (kIPos / 4)) + row;
+      // pair k of position p: [k / kIPairs][p][k % kIPairs][tile][2] (see
+      // Shape::kMUnit); this unit's 64 outputs are the pairs 32 ng .. 32 ng + 31
+      float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * kGP + pl) * (S::kIPos / 4)) + row;
 #pragma unroll
       for (int c = 0; c < kN; c += 16) {
         float vv[16];
@@ -650,7 +784,8 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int k = gu.ng * (kN / 2) + c / 2 + i;
-            __stcg(mrow + (k >> 1) * (kMUnit / 8) + (k & 1) * kBlockTiles, make_float2(vv[2 * i], vv[2 * i + 1]));
+            __stcg(mrow + (k / S::kIPairs) * (S::kMUnit / 8) + (k % S::kIPairs) * kBlockTiles,
+                   make_float2(vv[2 * i], vv[2 * i + 1]));
           }
         }
       }
@@ -703,8 +838,8 @@ __device__ void publisher(const Params& P, Sync& sy, int n_g) {
     wk.decode(P, uf, kind, b, sub);
     if (kind == 2 && (P.discard & 2)) {
       const uint8_t* m = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * S::kMSlot +
-                         static_cast<size_t>(sub) * kMUnit;
-      for (int i = lane; i < static_cast<int>(kMUnit / 128); i += 32) discard_l2(m + static_cast<size_t>(i) * 128);
+                         static_cast<size_t>(sub) * S::kMUnit;
+      for (int i = lane; i < static_cast<int>(S::kMUnit / 128); i += 32) discard_l2(m + static_cast<size_t>(i) * 128);
       __syncwarp();
     }
     if (lane == 0) {
@@ -812,15 +947,16 @@ struct Plan {
 template <class S>
 static Plan plan_t(const Geo& g) {
   Plan pl = {};
-  // the branch-free window loads assume pad_lo = 1 and 16-byte aligned rows (W % 4 == 0)
-  if (g.W % 4 != 0 || g.m != 4 || g.pad_lo != 1 || g.W < 8) return pl;
+  // the bulk-copied input rows must be 16-byte aligned (W % 4 == 0); the
+  // branch-free window loads assume pad_lo = 1
+  if (g.W % 4 != 0 || g.m != S::kT - 2 || g.pad_lo != 1 || g.W < 8) return pl;
   int max_rows = 0;                        // union staging: the largest unit
   for (int t0 = 0; t0 < g.n_tile; t0 += kFT) {
     const FGeo fg(g, t0, std::min(t0 + kFT, g.n_tile) - 1);
     max_rows = std::max(max_rows, fg.total());
   }
   pl.plane = round_up(max_rows * g.W, 32) + 16;
-  if (static_cast<size_t>(kCPC) * pl.plane * 4 > kFISlot) return pl;
+  if (static_cast<size_t>(S::kCPC) * pl.plane * 4 > kFISlot) return pl;
   // measured on c2 (tools/ws_time.py): rings of 300 MB (slightly past L2)
   // with the I units 32 steps behind their F units are best (80 us)
   size_t budget = 300ull << 20;
@@ -848,23 +984,27 @@ static Plan plan_t(const Geo& g) {
   return pl;
 }
 
-// Channel shapes with a kernel instance: Cpad in {64, 128} (= C) and 16
-// (C <= 16), C' (= C'pad) in {64, 128, 256} -- every (position, c' group) pair gets a CTA of
-// its own (36 x C'/64 <= 148), and A stages + V + two F/I slots fit smem.
+// Shapes with a kernel instance: T = 6 with Cpad in {64, 128} (= C) and 16
+// (C <= 16), C' (= C'pad) in {64, 128, 256}; T = 8 with C = C' in {64, 128}
+// -- every (position, c' group) pair gets a CTA of its own (T^2 x C'/64 <=
+// 148), and A stages + V + two F/I slots fit smem.
 template <class F>
-static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<64, 64>())) {
-  using R = decltype(f(Shape<64, 64>()));
+static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
+  using R = decltype(f(Shape<6, 64, 64>()));
   // C = Cpad except for the 16-channel instance, which zero-pads C <= 16
   // (VGG's RGB layer); C' = C'pad
-  if (g.fft || g.T != kT || g.Cp != g.Cppad || (g.C != g.Cpad && g.Cpad != 16)) return R();
-  switch (g.Cpad * 1000 + g.Cp) {
-    case 16064: return f(Shape<16, 64>());
-    case 64064: return f(Shape<64, 64>());
-    case 64128: return f(Shape<64, 128>());
-    case 64256: return f(Shape<64, 256>());
-    case 128064: return f(Shape<128, 64>());
-    case 128128: return f(Shape<128, 128>());
-    case 128256: return f(Shape<128, 256>());
+  if (g.fft || g.Cp != g.Cppad || (g.C != g.Cpad && g.Cpad != 16)) return R();
+  switch (g.T * 1000000 + g.Cpad * 1000 + g.Cp) {
+    case 6016064: return f(Shape<6, 16, 64>());
+    case 6064064: return f(Shape<6, 64, 64>());
+    case 6064128: return f(Shape<6, 64, 128>());
+    case 6064256: return f(Shape<6, 64, 256>());
+    case 6128064: return f(Shape<6, 128, 64>());
+    case 6128128: return f(Shape<6, 128, 128>());
+    case 6128256: return f(Shape<6, 128, 256>());
+    // F(6x6,3x3): the c5 sweep's 64- and 128-channel layers (64 x C'/64 <= 148)
+    case 8064064: return f(Shape<8, 64, 64>());
+    case 8128128: return f(Shape<8, 128, 128>());
   }
   return R();
 }
@@ -898,7 +1038,7 @@ bool ws_fits(const Geo& g) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms >= ws::kP * (g.Cp / ws::kN);   // a CTA per (position, c' group)
+  return sms >= g.P * (g.Cp / ws::kN);   // a CTA per (position, c' group)
 }
 
 size_t ws_scratch_bytes(const Geo& g) {

@@ -317,22 +317,40 @@ def test_warp_specialised_kernel(dims, monkeypatch):
     VGG 64/128-channel layers) against three-stage (bitwise), the
     item-queue persistent kernel (WF_WS=0, bitwise) and FP64 direct.  Small
     rings (WF_WS_BUDGET_MB) force slot reuse and the lagged dependencies."""
+    _check_ws(dims, 6, monkeypatch)
+
+
+def _check_ws(dims, t, monkeypatch):
     spec = wf.LayerSpec(*dims)
     rng = np.random.default_rng(sum(dims))
     x = rng.standard_normal(spec.input_dims()).astype(np.float32)
     w = _he(rng, spec)
-    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
-    s, _ = _run("three_stage", x, pack, spec, 6)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
+    s, _ = _run("three_stage", x, pack, spec, t)
     ref = O.direct_conv_f64(x, w, spec)
     for budget in ("300", "12"):
         monkeypatch.setenv("WF_WS_BUDGET_MB", budget)
-        f, _ = _run("fused", x, pack, spec, 6)
+        f, _ = _run("fused", x, pack, spec, t)
         assert np.array_equal(f, s), (dims, budget)
-        assert O.max_rel_error(f, ref) <= TOL[6], (dims, budget)
+        assert O.max_rel_error(f, ref) <= TOL[t], (dims, budget)
     monkeypatch.setenv("WF_WS", "0")
     monkeypatch.setenv("WF_PERSIST_MIN_BLOCKS", "1")
-    q, _ = _run("fused", x, pack, spec, 6)
+    q, _ = _run("fused", x, pack, spec, t)
     assert np.array_equal(q, s), dims
+
+
+@pytest.mark.parametrize("dims", [(2, 64, 64, 28, 28, 3, 1, 1),     # 5 x 5 tiles: several images per F unit
+                                  (3, 64, 64, 56, 56, 3, 1, 1),
+                                  (2, 64, 64, 27, 32, 3, 1, 1),     # partial bottom / right windows (3 pad columns)
+                                  (8, 64, 64, 56, 56, 3, 1, 1),     # 7 blocks: ring reuse at 12 MB
+                                  (2, 128, 128, 28, 28, 3, 1, 1),
+                                  (1, 128, 128, 112, 112, 3, 1, 1)])
+def test_warp_specialised_kernel_f6(dims, monkeypatch):
+    """The warp-specialised fused kernel for F(6x6,3x3) (T = 8, C = C' in
+    {64, 128}: the c5 sweep's wide layers) -- thread per (tile, channel)
+    transforms, 4-channel F units, 2-channel I units -- against three-stage
+    and the item-queue kernel (bitwise) and FP64 direct."""
+    _check_ws(dims, 8, monkeypatch)
 
 
 def test_planned_layer_skips_counter_reset_safely(monkeypatch):
