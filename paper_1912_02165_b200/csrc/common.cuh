@@ -277,6 +277,91 @@ __device__ __forceinline__ void inverse_transform2<6>(const float2 (&mm)[6][6], 
   inverse6<PairOps>(mm, y);
 }
 
+// ------------------------------------------------------------------------
+// F(6x6, 3x3) (T = 8) specialisations, factored the same way (26 adds/FMAs
+// instead of 44 for B^T, 20 instead of 38 for A^T), coefficients of the
+// reference basis (basis_tables.cuh: bt<8>, at<8>).
+// u = B^T x for one line of 8 (in place):
+//   u0 = x0 - 21/4 x2 + 21/4 x4 - x6                 = (x0 - x6) + 21/4 (x4 - x2)
+//   u1, u2 = a1 +- b1, a1 = x2 + x6 - 17/4 x4,       b1 = x1 + x5 - 17/4 x3
+//   u3, u4 = a3 +- b3, a3 = x2 / 4 - 5/4 x4 + x6,    b3 = x1 / 2 - 5/2 x3 + 2 x5
+//   u5, u6 = a5 +- b5, a5 = 4 x2 - 5 x4 + x6,        b5 = 2 x1 - 5/2 x3 + x5 / 2
+//   u7 = x1 - 21/4 x3 + 21/4 x5 - x7                 = (x1 - x7) + 21/4 (x5 - x3)
+template <class O, class V>
+__device__ __forceinline__ void bt8_line(V& x0, V& x1, V& x2, V& x3, V& x4, V& x5, V& x6, V& x7) {
+  const V a1 = O::fma(-4.25f, x4, O::add(x2, x6)), b1 = O::fma(-4.25f, x3, O::add(x1, x5));
+  const V a3 = O::fma(0.25f, x2, O::fma(-1.25f, x4, x6)), b3 = O::fma(0.5f, x1, O::fma(-2.5f, x3, O::add(x5, x5)));
+  const V a5 = O::fma(4.0f, x2, O::fma(-5.0f, x4, x6)), b5 = O::fma(0.5f, x5, O::fma(-2.5f, x3, O::add(x1, x1)));
+  const V u0 = O::fma(5.25f, O::sub(x4, x2), O::sub(x0, x6));
+  const V u7 = O::fma(5.25f, O::sub(x5, x3), O::sub(x1, x7));
+  x0 = u0;
+  x1 = O::add(a1, b1);
+  x2 = O::sub(a1, b1);
+  x3 = O::add(a3, b3);
+  x4 = O::sub(a3, b3);
+  x5 = O::add(a5, b5);
+  x6 = O::sub(a5, b5);
+  x7 = u7;
+}
+// y = A^T m for one line of 8 -> 6, with s = m1 + m2, d = m1 - m2 (and 34, 56):
+//   y0 = m0 + s12 + s34 + s56
+//   y1 = d12 +  2 d34 + d56 / 2      y2 = s12 +  4 s34 + s56 / 4
+//   y3 = d12 +  8 d34 + d56 / 8      y4 = s12 + 16 s34 + s56 / 16
+//   y5 = d12 + 32 d34 + d56 / 32 - m7
+template <class O, class V>
+__device__ __forceinline__ void at8_line(V m0, V m1, V m2, V m3, V m4, V m5, V m6, V m7, V& y0, V& y1, V& y2, V& y3,
+                                         V& y4, V& y5) {
+  const V s12 = O::add(m1, m2), d12 = O::sub(m1, m2);
+  const V s34 = O::add(m3, m4), d34 = O::sub(m3, m4);
+  const V s56 = O::add(m5, m6), d56 = O::sub(m5, m6);
+  y0 = O::add(O::add(O::add(m0, s12), s34), s56);
+  y1 = O::fma(2.0f, d34, O::fma(0.5f, d56, d12));
+  y2 = O::fma(4.0f, s34, O::fma(0.25f, s56, s12));
+  y3 = O::fma(8.0f, d34, O::fma(0.125f, d56, d12));
+  y4 = O::fma(16.0f, s34, O::fma(0.0625f, s56, s12));
+  y5 = O::fma(32.0f, d34, O::fma(0.03125f, d56, O::sub(d12, m7)));
+}
+// Order as for T = 6: rows, then columns (forward); columns, then rows (inverse).
+template <class O, class V>
+__device__ __forceinline__ void forward8(const V (&x)[8][8], V (&u)[8][8]) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) u[r][s] = x[r][s];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) bt8_line<O>(u[r][0], u[r][1], u[r][2], u[r][3], u[r][4], u[r][5], u[r][6], u[r][7]);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) bt8_line<O>(u[0][s], u[1][s], u[2][s], u[3][s], u[4][s], u[5][s], u[6][s], u[7][s]);
+}
+template <class O, class V>
+__device__ __forceinline__ void inverse8(const V (&mm)[8][8], V (&y)[6][6]) {
+  V t[6][8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    at8_line<O>(mm[0][s], mm[1][s], mm[2][s], mm[3][s], mm[4][s], mm[5][s], mm[6][s], mm[7][s], t[0][s], t[1][s],
+                t[2][s], t[3][s], t[4][s], t[5][s]);
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+    at8_line<O>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], t[r][6], t[r][7], y[r][0], y[r][1], y[r][2],
+                y[r][3], y[r][4], y[r][5]);
+}
+template <>
+__device__ __forceinline__ void forward_transform<8>(const float (&x)[8][8], float (&u)[8][8]) {
+  forward8<ScalarOps>(x, u);
+}
+template <>
+__device__ __forceinline__ void forward_transform2<8>(const float2 (&x)[8][8], float2 (&u)[8][8]) {
+  forward8<PairOps>(x, u);
+}
+template <>
+__device__ __forceinline__ void inverse_transform<8>(const float (&mm)[8][8], float (&y)[6][6]) {
+  inverse8<ScalarOps>(mm, y);
+}
+template <>
+__device__ __forceinline__ void inverse_transform2<8>(const float2 (&mm)[8][8], float2 (&y)[6][6]) {
+  inverse8<PairOps>(mm, y);
+}
+
 // Zero-filled T x T input window for one (tile, channel) (reference
 // kernels.py:73-86: origin (ty*m - pad_lo, tx*m - pad_lo), implicit padding).
 template <int T>

@@ -344,9 +344,10 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
 }
 
 // ------------------------------------------------------------- F/I workers
-// F(6x6,3x3) units (T = 8).  The transforms are the generic ones every other
-// path of the library uses for T = 8 (common.cuh forward_transform<8>,
-// inverse_transform<8>), so the results stay bitwise equal to them.
+// F(6x6,3x3) units (T = 8).  Per element the operations of forward8 /
+// inverse8 (common.cuh), which every other path of the library uses for
+// T = 8, so the results stay bitwise equal to them; rows are transformed as
+// they are loaded and positions stored one column at a time.
 //
 // F(b, sub): thread = (tile tl, channel cq); a warp = 8 tiles x 4 channels
 // (half of an 8-channel core-matrix k group).  Lanes cq and cq ^ 1 swap
@@ -397,6 +398,7 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
       x[r][3] = p3.x; x[r][4] = p3.y;
       x[r][5] = p5.x; x[r][6] = p5.y;
       x[r][7] = a7;
+      bt8_line<ScalarOps>(x[r][0], x[r][1], x[r][2], x[r][3], x[r][4], x[r][5], x[r][6], x[r][7]);
     }
   } else {
 #pragma unroll
@@ -406,22 +408,22 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window consumed: slot free
-  float u[8][8];
-  forward_transform<8>(x, u);
   const bool odd = cq & 1;
   const int row = tb0 + tl, c0 = cg * kCPC + (cq & ~1);
   uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 / S::kKBW) * S::kAHalf +
                  (row >> 3) * (16 * S::kKBW) + ((c0 % S::kKBW) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
                  (odd ? S::kKB * S::kAHalf : 0);
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
+  for (int s = 0; s < 8; ++s) {
+    bt8_line<ScalarOps>(x[0][s], x[1][s], x[2][s], x[3][s], x[4][s], x[5][s], x[6][s], x[7][s]);
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const float other = __shfl_xor_sync(0xffffffffu, u[r][s], 8);
+    for (int r = 0; r < 8; ++r) {
+      const float other = __shfl_xor_sync(0xffffffffu, x[r][s], 8);
       uint32_t hi, lo;
-      split_bf16x2(odd ? other : u[r][s], odd ? u[r][s] : other, hi, lo);
+      split_bf16x2(odd ? other : x[r][s], odd ? x[r][s] : other, hi, lo);
       if (live) *reinterpret_cast<uint32_t*>(dst + (r * 8 + s) * S::kUPos) = odd ? lo : hi;
     }
+  }
 }
 
 // I(b, sub), T = 8: thread = (tile, c' of the unit's pair); 64 staged
@@ -434,15 +436,18 @@ __device__ __forceinline__ void i_unit8(const Params& P, const uint8_t* src, Syn
   const int tl = wtid & (kBlockTiles - 1), cq = wtid >> 7;
   const int tile = b * kBlockTiles + tl;
   const float* ms = reinterpret_cast<const float*>(src) + tl * 2 + cq;
-  float mm[8][8];
+  // column pass (A^T down each column) as the products are read
+  float t[6][8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
+  for (int s = 0; s < 8; ++s) {
+    float m[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) mm[r][s] = ms[(r * 8 + s) * (S::kIPos / 4)];
+    for (int r = 0; r < 8; ++r) m[r] = ms[(r * 8 + s) * (S::kIPos / 4)];
+    at8_line<ScalarOps>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], t[0][s], t[1][s], t[2][s], t[3][s], t[4][s],
+                        t[5][s]);
+  }
   __syncwarp();
   if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
-  float out[6][6];
-  inverse_transform<8>(mm, out);
   if (tile < g.n_tile) {
     const int per_img = g.tiles_y * g.tiles_x;
     const int bi = tile / per_img;
@@ -454,14 +459,17 @@ __device__ __forceinline__ void i_unit8(const Params& P, const uint8_t* src, Syn
     float* ybase = P.y + ((static_cast<size_t>(bi) * g.Cp + cp) * g.Ho + oy) * g.Wo + ox;
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
+      float out[6];
+      at8_line<ScalarOps>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], t[r][6], t[r][7], out[0], out[1], out[2],
+                          out[3], out[4], out[5]);
       if (vec) {
 #pragma unroll
         for (int c = 0; c < 6; c += 2)
-          *reinterpret_cast<float2*>(ybase + r * g.Wo + c) = make_float2(out[r][c], out[r][c + 1]);
+          *reinterpret_cast<float2*>(ybase + r * g.Wo + c) = make_float2(out[c], out[c + 1]);
       } else if (oy + r < g.Ho) {
 #pragma unroll
         for (int c = 0; c < 6; ++c)
-          if (ox + c < g.Wo) ybase[r * g.Wo + c] = out[r][c];
+          if (ox + c < g.Wo) ybase[r * g.Wo + c] = out[c];
       }
     }
   }
