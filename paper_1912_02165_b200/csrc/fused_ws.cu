@@ -46,8 +46,7 @@ static_assert(4 * 32 * kRegsLight + 4 * 32 * kRegsEpi + 8 * 32 * kRegsFI <= 6553
 #endif
 constexpr int kGP = WF_WS_GP;                            // positions per G unit
 static_assert(kGP == 1, "G units own one position (position-affine CTAs keep V resident)");
-constexpr int kN = 64;                                   // output channels per G unit (MMA N)
-constexpr int kNAcc = 512 / (kGP * kN);                  // TMEM accumulator buffers (units in flight)
+constexpr int kNAcc = 8;                                 // TMEM accumulator buffers (units in flight)
 constexpr int kFT = 64;                                  // tiles per F unit
 constexpr int kMaxAStages = 4;
 constexpr uint32_t kFISlot = 72 * 1024;                  // F staging or I staging
@@ -60,6 +59,8 @@ template <int T_, int C_, int CP_>
 struct Shape {
   static constexpr int kT = T_, kP = T_ * T_;
   static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
+  static constexpr int kN = CP < 64 ? CP : 64;           // output channels per G unit (MMA N)
+  static constexpr int kTmemCols = kNAcc * kGP * kN;     // 128, 256 or 512
   // F unit: 64 tiles x kCPC channels (thread = tile x channel pair for T = 6,
   // tile x channel for T = 8, whose larger windows halve the channels staged)
   static constexpr int kCPC = T_ == 6 ? 8 : 4;
@@ -408,20 +409,32 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window consumed: slot free
-  const bool odd = cq & 1;
-  const int row = tb0 + tl, c0 = cg * kCPC + (cq & ~1);
+  // Two positions (r, s), (r + 1, s) at a time, a 4-lane transpose of the
+  // tile's bf16 halves (lanes cq = 0..3 hold channels c0 + cq): after it,
+  // lane cq stores 4 channels of [hi, lo][cq & 1] of position r + (cq >> 1)
+  // as one 8-byte store.
+  const int row = tb0 + tl, c0 = cg * kCPC;
   uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 / S::kKBW) * S::kAHalf +
                  (row >> 3) * (16 * S::kKBW) + ((c0 % S::kKBW) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
-                 (odd ? S::kKB * S::kAHalf : 0);
+                 (cq & 1) * (S::kKB * S::kAHalf) + (cq >> 1) * 8 * S::kUPos;
+  const bool odd = cq & 1, upper = cq & 2;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     bt8_line<ScalarOps>(x[0][s], x[1][s], x[2][s], x[3][s], x[4][s], x[5][s], x[6][s], x[7][s]);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const float other = __shfl_xor_sync(0xffffffffu, x[r][s], 8);
-      uint32_t hi, lo;
-      split_bf16x2(odd ? other : x[r][s], odd ? x[r][s] : other, hi, lo);
-      if (live) *reinterpret_cast<uint32_t*>(dst + (r * 8 + s) * S::kUPos) = odd ? lo : hi;
+    for (int r = 0; r < 8; r += 2) {
+      uint32_t hi, lo;                                    // (position r, position r + 1) of channel c0 + cq
+      split_bf16x2(x[r][s], x[r + 1][s], hi, lo);
+      // step 1 (lanes cq ^ 1): the even lane gathers the hi halves of its
+      // channel pair, the odd one the lo halves: A = position r, B = r + 1
+      const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 8);
+      const uint32_t mine = odd ? lo : hi;
+      const uint32_t lo_ch = odd ? got : mine, hi_ch = odd ? mine : got;
+      const uint32_t A = __byte_perm(lo_ch, hi_ch, 0x5410), B = __byte_perm(lo_ch, hi_ch, 0x7632);
+      // step 2 (lanes cq ^ 2): channels c0 + 2, c0 + 3 join c0, c0 + 1
+      const uint32_t got2 = __shfl_xor_sync(0xffffffffu, upper ? A : B, 16);
+      if (live)
+        *reinterpret_cast<uint2*>(dst + (r * 8 + s) * S::kUPos) = upper ? make_uint2(got2, B) : make_uint2(A, got2);
     }
   }
 }
@@ -710,6 +723,7 @@ template <class S, bool PROF>
 __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   // the whole warp runs the loop; lane 0 issues the MMAs
   const int lane = threadIdx.x & 31;
+  constexpr int kN = S::kN;
   const uint32_t idesc = idesc_bf16(kBlockTiles, kN);
   const ProfT<PROF> pf(P.prof);
   const GUnits<S> gu(P);
@@ -768,6 +782,7 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
   const ProfT<PROF> pf(P.prof && qd == 0 && lane == 0);
   const GUnits<S> gu(P);
   const int gg = gu.p;
+  constexpr int kN = S::kN;
   int k = 0;
   for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
     const int buf = k % kNAcc;
@@ -883,7 +898,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
     if (PROF) g_wsprof[blockIdx.x * kProfSlots + kStart] = gtimer();
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<512>(&sy.tmem);
+  if (warp == 1) tmem_alloc<S::kTmemCols>(&sy.tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -925,7 +940,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(sy.tmem);
+    tmem_dealloc<S::kTmemCols>(sy.tmem);
   }
   // The last CTA to finish zeroes the dependency counters, so a caller that
   // owns this scratch can skip the memset before the next launch
@@ -1010,7 +1025,10 @@ static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
     case 6128064: return f(Shape<6, 128, 64>());
     case 6128128: return f(Shape<6, 128, 128>());
     case 6128256: return f(Shape<6, 128, 256>());
-    // F(6x6,3x3): the c5 sweep's 64- and 128-channel layers (64 x C'/64 <= 148)
+    // F(6x6,3x3): the c5 sweep's layers (64 x C'/64 <= 148); C' < 64 runs
+    // G units of N = C'
+    case 8016016: return f(Shape<8, 16, 16>());
+    case 8032032: return f(Shape<8, 32, 32>());
     case 8064064: return f(Shape<8, 64, 64>());
     case 8128128: return f(Shape<8, 128, 128>());
   }
@@ -1046,7 +1064,8 @@ bool ws_fits(const Geo& g) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms >= g.P * (g.Cp / ws::kN);   // a CTA per (position, c' group)
+  // a CTA per (position, c' group)
+  return ws::with_shape(g, [&](auto s) { return sms >= decltype(s)::kP * decltype(s)::kNG; });
 }
 
 size_t ws_scratch_bytes(const Geo& g) {
@@ -1072,7 +1091,7 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   // U only (by the epilogue warps, default) 175 MB at the same time; M only
   // (by the publisher) 212 MB, same time; both 99 MB but +2-4 us (the M
   // discards delay the I publishes)
-  P.discard = 1;
+  P.discard = g.T == 6 ? 1 : 0;   // T = 8 (measured on c5): 2-3% faster without
   if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
   P.dbg = 0;
   if (const char* e = getenv("WF_WS_DBG")) P.dbg = atoi(e);

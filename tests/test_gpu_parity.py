@@ -344,10 +344,13 @@ def _check_ws(dims, t, monkeypatch):
                                   (2, 64, 64, 27, 32, 3, 1, 1),     # partial bottom / right windows (3 pad columns)
                                   (8, 64, 64, 56, 56, 3, 1, 1),     # 7 blocks: ring reuse at 12 MB
                                   (2, 128, 128, 28, 28, 3, 1, 1),
-                                  (1, 128, 128, 112, 112, 3, 1, 1)])
+                                  (1, 128, 128, 112, 112, 3, 1, 1),
+                                  (3, 16, 16, 28, 28, 3, 1, 1),     # C' < 64: G units of N = C'
+                                  (2, 32, 32, 56, 56, 3, 1, 1),
+                                  (8, 16, 16, 56, 56, 3, 1, 1)])
 def test_warp_specialised_kernel_f6(dims, monkeypatch):
     """The warp-specialised fused kernel for F(6x6,3x3) (T = 8, C = C' in
-    {64, 128}: the c5 sweep's wide layers) -- thread per (tile, channel)
+    {16, 32, 64, 128}: the c5 sweep's layers) -- thread per (tile, channel)
     transforms, 4-channel F units, 2-channel I units -- against three-stage
     and the item-queue kernel (bitwise) and FP64 direct."""
     _check_ws(dims, 8, monkeypatch)
