@@ -47,9 +47,7 @@ static_assert(4 * 32 * kRegsLight + 4 * 32 * kRegsEpi + 8 * 32 * kRegsFI <= 6553
 constexpr int kGP = WF_WS_GP;                            // positions per G unit
 static_assert(kGP == 1, "G units own one position (position-affine CTAs keep V resident)");
 constexpr int kNAcc = 8;                                 // TMEM accumulator buffers (units in flight)
-constexpr int kFT = 64;                                  // tiles per F unit
 constexpr int kMaxAStages = 4;
-constexpr uint32_t kFISlot = 72 * 1024;                  // F staging or I staging
 
 // Layer shape: window T (6: F(4x4,3x3), 8: F(6x6,3x3)), C input channels
 // (GEMM K, 32-channel K blocks), CP output channels (GEMM N, 64-wide G
@@ -61,9 +59,14 @@ struct Shape {
   static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
   static constexpr int kN = CP < 64 ? CP : 64;           // output channels per G unit (MMA N)
   static constexpr int kTmemCols = kNAcc * kGP * kN;     // 128, 256 or 512
-  // F unit: 64 tiles x kCPC channels (thread = tile x channel pair for T = 6,
-  // tile x channel for T = 8, whose larger windows halve the channels staged)
-  static constexpr int kCPC = T_ == 6 ? 8 : 4;
+  // F unit: kFT tiles x 8 channels (one core-matrix k group, so that a
+  // warp's U stores fill whole 32-byte sectors): 64 tiles with a thread per
+  // (tile, channel pair) for T = 6, 32 tiles with a thread per (tile,
+  // channel) for T = 8, whose larger windows need more staging per tile
+  static constexpr int kCPC = 8;
+  static constexpr int kFT = T_ == 6 ? 64 : 32;
+  // F staging or I staging slot (two of them)
+  static constexpr uint32_t kFISlot = (T_ == 6 ? 72 : 73) * 1024;
   // I unit: kIPairs c' pairs.  M ring slot layout: [I unit][position][c' pair
   // in unit][tile][2]: the products one I unit needs are one contiguous
   // range (72 KB for T = 6, 64 KB for T = 8) -- one bulk copy
@@ -281,7 +284,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     int kind, b, sub;
     wk.decode(P, u, kind, b, sub);
     const int slot = it & 1;
-    uint8_t* dstbase = smem + S::kOffFI + slot * kFISlot;
+    uint8_t* dstbase = smem + S::kOffFI + slot * S::kFISlot;
     if (lane == 0) {
       long long t0 = pf.now();
       if (kind == 0) {
@@ -304,8 +307,8 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     if (kind == 0) {
       constexpr int kCPC = S::kCPC;
       const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
-      const int t0 = b * kBlockTiles + part * kFT;
-      const int tlast = min(t0 + kFT, g.n_tile) - 1;
+      const int t0 = b * kBlockTiles + part * S::kFT;
+      const int tlast = min(t0 + S::kFT, g.n_tile) - 1;
       float* xs = reinterpret_cast<float*>(dstbase);
       // the single arrival carries the whole unit's byte count and comes
       // first: the phase cannot complete before every copy has landed
@@ -350,20 +353,20 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
 // T = 8, so the results stay bitwise equal to them; rows are transformed as
 // they are loaded and positions stored one column at a time.
 //
-// F(b, sub): thread = (tile tl, channel cq); a warp = 8 tiles x 4 channels
-// (half of an 8-channel core-matrix k group).  Lanes cq and cq ^ 1 swap
-// values so that the even one stores the hi and the odd one the lo bf16 of
-// both channels: one 4-byte store per position.
+// F(b, sub): thread = (tile tl, channel cl); a warp = 4 tiles x 8 channels
+// (half of the rows of a core matrix), so that a warp writes 64 contiguous
+// bytes of each core matrix it stores to.
 template <class S>
 __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Sync& sy, int slot, int b, int sub,
                                         int wl, int lane) {
-  static_assert(S::kT == 8 && S::kCPC == 4, "T = 8 F unit");
+  static_assert(S::kT == 8 && S::kCPC == 8, "T = 8 F unit");
   const Geo& g = P.g;
   constexpr int kCPC = S::kCPC;
   const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
+  constexpr int kFT = S::kFT;
   const int tb0 = part * kFT;
   const int t0 = b * kBlockTiles + tb0;
-  const int tl = wl * 8 + (lane & 7), cq = lane >> 3;
+  const int tl = wl * 4 + (lane & 3), cl = lane >> 2, cq = cl & 3;
   const int tile = t0 + tl;
   const bool live = tile < g.n_tile;
   float x[8][8];
@@ -375,13 +378,13 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
     const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
     const int y0 = ty * g.m - g.pad_lo;
     const int x0 = tx * g.m - g.pad_lo;
-    const float* pa = reinterpret_cast<const float*>(src) + cq * P.plane + fg.srow(bi - fg.bi0, y0) * g.W + x0;
+    const float* pa = reinterpret_cast<const float*>(src) + cl * P.plane + fg.srow(bi - fg.bi0, y0) * g.W + x0;
     // window columns [x0, x0 + 8), x0 = 6 tx - 1: three 8-byte loads
     // [x0 + 1, x0 + 7) and two scalars per row.  W is even, so every pair
     // lies wholly inside or wholly outside the image; the padding columns
     // and rows are zeros (their loads are predicated off)
     const bool v0 = x0 >= 0, v3 = x0 + 3 < g.W, v5 = x0 + 5 < g.W, v7 = x0 + 7 < g.W;
-    const bool cv = S::C >= 64 || cg * kCPC + cq < g.C;
+    const bool cv = S::C >= 64 || cg * kCPC + cl < g.C;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const float* ra = pa + r * g.W;
@@ -410,10 +413,10 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
   __syncwarp();
   if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);     // window consumed: slot free
   // Two positions (r, s), (r + 1, s) at a time, a 4-lane transpose of the
-  // tile's bf16 halves (lanes cq = 0..3 hold channels c0 + cq): after it,
-  // lane cq stores 4 channels of [hi, lo][cq & 1] of position r + (cq >> 1)
-  // as one 8-byte store.
-  const int row = tb0 + tl, c0 = cg * kCPC;
+  // bf16 halves of channels c0 .. c0 + 3 of a tile (lanes cq = 0..3 hold
+  // channel c0 + cq, c0 = 8 cg or 8 cg + 4): after it, lane cq stores the 4
+  // channels of [hi, lo][cq & 1] of position r + (cq >> 1) as one 8-byte store.
+  const int row = tb0 + tl, c0 = cg * kCPC + (cl & 4);
   uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 / S::kKBW) * S::kAHalf +
                  (row >> 3) * (16 * S::kKBW) + ((c0 % S::kKBW) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
                  (cq & 1) * (S::kKB * S::kAHalf) + (cq >> 1) * 8 * S::kUPos;
@@ -427,12 +430,12 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
       split_bf16x2(x[r][s], x[r + 1][s], hi, lo);
       // step 1 (lanes cq ^ 1): the even lane gathers the hi halves of its
       // channel pair, the odd one the lo halves: A = position r, B = r + 1
-      const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 8);
+      const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 4);
       const uint32_t mine = odd ? lo : hi;
       const uint32_t lo_ch = odd ? got : mine, hi_ch = odd ? mine : got;
       const uint32_t A = __byte_perm(lo_ch, hi_ch, 0x5410), B = __byte_perm(lo_ch, hi_ch, 0x7632);
       // step 2 (lanes cq ^ 2): channels c0 + 2, c0 + 3 join c0, c0 + 1
-      const uint32_t got2 = __shfl_xor_sync(0xffffffffu, upper ? A : B, 16);
+      const uint32_t got2 = __shfl_xor_sync(0xffffffffu, upper ? A : B, 8);
       if (live)
         *reinterpret_cast<uint2*>(dst + (r * 8 + s) * S::kUPos) = upper ? make_uint2(got2, B) : make_uint2(A, got2);
     }
@@ -503,7 +506,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     int kind, b, sub;
     wk.decode(P, u, kind, b, sub);
     const int slot = it & 1;
-    const uint8_t* src = smem + S::kOffFI + slot * kFISlot;
+    const uint8_t* src = smem + S::kOffFI + slot * S::kFISlot;
     long long t0 = pf.now();
     mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
     pf.add(kFWWait, t0);
@@ -518,6 +521,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       // (one core-matrix row group) x 4 pairs (one 8-channel k group), so
       // every store instruction writes one contiguous 128-byte core matrix
       const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
+      constexpr int kFT = S::kFT;
       const int tb0 = part * kFT;
       const int t0 = b * kBlockTiles + tb0;
       const int tl = wl * 8 + (lane & 7), q = lane >> 3;
@@ -974,12 +978,12 @@ static Plan plan_t(const Geo& g) {
   // branch-free window loads assume pad_lo = 1
   if (g.W % 4 != 0 || g.m != S::kT - 2 || g.pad_lo != 1 || g.W < 8) return pl;
   int max_rows = 0;                        // union staging: the largest unit
-  for (int t0 = 0; t0 < g.n_tile; t0 += kFT) {
-    const FGeo fg(g, t0, std::min(t0 + kFT, g.n_tile) - 1);
+  for (int t0 = 0; t0 < g.n_tile; t0 += S::kFT) {
+    const FGeo fg(g, t0, std::min(t0 + S::kFT, g.n_tile) - 1);
     max_rows = std::max(max_rows, fg.total());
   }
   pl.plane = round_up(max_rows * g.W, 32) + 16;
-  if (static_cast<size_t>(S::kCPC) * pl.plane * 4 > kFISlot) return pl;
+  if (static_cast<size_t>(S::kCPC) * pl.plane * 4 > S::kFISlot) return pl;
   // measured on c2 (tools/ws_time.py): rings of 300 MB (slightly past L2)
   // with the I units 32 steps behind their F units are best (80 us)
   size_t budget = 300ull << 20;
