@@ -66,11 +66,12 @@ struct Shape {
   static constexpr int kCPC = 8;
   static constexpr int kFT = T_ == 6 ? 64 : 32;
   // F staging or I staging slot (two of them)
-  static constexpr uint32_t kFISlot = (T_ == 6 ? 72 : 73) * 1024;
+  // (C = 256, T = 6: 48 KB, room for the 64 KB V slab; 2-channel I units)
+  static constexpr uint32_t kFISlot = (T_ == 6 ? (C_ >= 256 ? 48 : 72) : 73) * 1024;
   // I unit: kIPairs c' pairs.  M ring slot layout: [I unit][position][c' pair
   // in unit][tile][2]: the products one I unit needs are one contiguous
   // range (72 KB for T = 6, 64 KB for T = 8) -- one bulk copy
-  static constexpr int kIPairs = T_ == 6 ? 2 : 1;
+  static constexpr int kIPairs = (T_ == 6 && C_ < 256) ? 2 : 1;
   static constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;
   static constexpr uint32_t kMUnit = kP * kIPos;
   static constexpr int kKBW = C < 32 ? C : 32;           // K block width (channels per A stage)
@@ -442,6 +443,51 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
   }
 }
 
+// I(b, sub), T = 6 with 2-channel I units (C = 256): thread = (tile, c');
+// per element the operations of inverse6 (== the f32x2 path of the wider
+// I units).
+template <class S>
+__device__ __forceinline__ void i_unit6s(const Params& P, const uint8_t* src, Sync& sy, int slot, int b, int sub,
+                                         int wtid, int lane) {
+  static_assert(S::kT == 6 && S::kIPairs == 1, "T = 6 scalar I unit");
+  const Geo& g = P.g;
+  const int tl = wtid & (kBlockTiles - 1), cq = wtid >> 7;
+  const int tile = b * kBlockTiles + tl;
+  const float* ms = reinterpret_cast<const float*>(src) + tl * 2 + cq;
+  float t[4][6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    float m[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) m[r] = ms[(r * 6 + s) * (S::kIPos / 4)];
+    at6_line<ScalarOps>(m[0], m[1], m[2], m[3], m[4], m[5], t[0][s], t[1][s], t[2][s], t[3][s]);
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
+  if (tile < g.n_tile) {
+    const int per_img = g.tiles_y * g.tiles_x;
+    const int bi = tile / per_img;
+    const int rem = tile - bi * per_img;
+    const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+    const int oy = ty * 4, ox = tx * 4;
+    const bool vec = oy + 4 <= g.Ho && ox + 4 <= g.Wo && (g.Wo & 3) == 0;
+    const int cp = 2 * sub + cq;
+    float* ybase = P.y + ((static_cast<size_t>(bi) * g.Cp + cp) * g.Ho + oy) * g.Wo + ox;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float o[4];
+      at6_line<ScalarOps>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], o[0], o[1], o[2], o[3]);
+      if (vec) {
+        *reinterpret_cast<float4*>(ybase + r * g.Wo) = make_float4(o[0], o[1], o[2], o[3]);
+      } else if (oy + r < g.Ho) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (ox + c < g.Wo) ybase[r * g.Wo + c] = o[c];
+      }
+    }
+  }
+}
+
 // I(b, sub), T = 8: thread = (tile, c' of the unit's pair); 64 staged
 // products per thread, inverse transform, clipped 6 x 6 output block.
 template <class S>
@@ -599,6 +645,8 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           }
         }
       }
+    } else if constexpr (S::kIPairs == 1) {
+      i_unit6s<S>(P, src, sy, slot, b, sub, wtid, lane);
     } else {
       // ---- I(b, sub): thread = (tile, c' pair); 36 staged float2 per thread
       const int tl = wtid & (kBlockTiles - 1), pr = wtid >> 7;
@@ -993,10 +1041,12 @@ static Plan plan_t(const Geo& g) {
   pl.NU = std::min(slots / 2, g.n_blk);
   pl.NM = std::min(slots - slots / 2, g.n_blk);
   // the lag counts steps; a step is one block's F and I units, so the lag
-  // that keeps ~1000 units between a block's F and I units shrinks with the
-  // channel counts (measured: c2 32 steps of 32 units, VGG 64->128 and
-  // 128->128 16 steps of 48 / 64 units, VGG 3->64 32 of 20)
-  int lag = std::max(8, std::min(32, 1024 / (S::kNCG + S::kNIG)));
+  // that keeps a fixed number of units between a block's F and I units
+  // shrinks with the units per step (measured best: c2, 32 units per step,
+  // 32 steps; VGG 64->128 / 128->128 / 128->256 / 256->256, 48 / 64 / 96 /
+  // 192 units, 16 / 12 / 8 / 4 steps; c5 64->64 and 128->128 about the same)
+  const int units = S::kNCG + S::kNIG;
+  int lag = units <= 32 ? 32 : std::max(4, std::min(32, 768 / units));
   if (const char* e = getenv("WF_WS_LAG")) lag = atoi(e);
   // deadlock freedom: some L1 with 1 <= L1 < NU (when F waits on G) and L2 - L1 < NM
   const int lmax = (pl.NU >= g.n_blk ? g.n_blk + pl.NM : pl.NU + pl.NM - 2);
@@ -1029,6 +1079,7 @@ static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
     case 6128064: return f(Shape<6, 128, 64>());
     case 6128128: return f(Shape<6, 128, 128>());
     case 6128256: return f(Shape<6, 128, 256>());
+    case 6256256: return f(Shape<6, 256, 256>());   // VGG conv3_2/3_3 (36 x 4 = 144 CTAs)
     // F(6x6,3x3): the c5 sweep's layers (64 x C'/64 <= 148); C' < 64 runs
     // G units of N = C'
     case 8016016: return f(Shape<8, 16, 16>());

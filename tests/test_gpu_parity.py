@@ -309,11 +309,13 @@ def test_randomized_sweep_like_reference_acceptance():
                                   (3, 128, 128, 28, 28, 3, 1, 1),
                                   (2, 64, 256, 16, 20, 3, 1, 1),
                                   (2, 128, 256, 24, 16, 3, 1, 1),
+                                  (2, 256, 256, 28, 28, 3, 1, 1),   # 2-channel I units, 48 KB slots
+                                  (3, 256, 256, 56, 56, 3, 1, 1),
                                   (2, 3, 64, 40, 44, 3, 1, 1),      # RGB input: 16-channel K padding
                                   (2, 16, 64, 16, 24, 3, 1, 1)])
 def test_warp_specialised_kernel(dims, monkeypatch):
     """The warp-specialised fused kernel (F(4x4,3x3), C in {64, 128}, C' in
-    {64, 128, 256}, W % 4 == 0, pad 1 -- the c2 benchmark layer and the
+    {64, 128, 256}, and C = C' = 256; W % 4 == 0, pad 1 -- the c2 benchmark layer and the
     VGG 64/128-channel layers) against three-stage (bitwise), the
     item-queue persistent kernel (WF_WS=0, bitwise) and FP64 direct.  Small
     rings (WF_WS_BUDGET_MB) force slot reuse and the lagged dependencies."""
