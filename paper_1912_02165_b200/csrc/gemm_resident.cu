@@ -229,49 +229,56 @@ cudaError_t launch_gemm_resident(const uint8_t* U, const uint8_t* V, float* M, c
 }
 
 // ------------------------------------------------------------ stage C, v2
-// Thread = (TPT consecutive tiles, c'): vector loads of M[p][c'][tile..]
-// (tiles are contiguous, ldm is a multiple of 128) so a warp moves
-// 32 * TPT * 4 bytes per position per instruction.
+// A warp owns 32 * TPT consecutive tiles of one c'; thread (lane) takes the
+// tiles lane, lane + 32, ...: every M load of a warp reads 128 contiguous
+// bytes, and every output row store of a warp writes the rows of 32
+// neighbouring tiles (one vector store per tile row segment, m = 4: float4,
+// m = 6: float2 x 3), so the stores fill whole sectors.
 template <int T, int TPT>
 __global__ void __launch_bounds__(128) inverse_vec_kernel(const float* __restrict__ M, float* __restrict__ y,
                                                           Geo g, int tile0, int ntile_local, int ldm) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int tq = (blockIdx.x * blockDim.x + threadIdx.x) * TPT;
+  const int lane = threadIdx.x & 31;
+  const int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 * TPT);
   const int cp = blockIdx.y;
-  if (tq >= ntile_local) return;
+  if (base >= ntile_local) return;
   constexpr int MO = T - 2;
-  float mm[TPT][T][T];
-  const float* src = M + static_cast<size_t>(cp) * ldm + tq;
+  const float* src = M + static_cast<size_t>(cp) * ldm + base + lane;
   const size_t pstride = static_cast<size_t>(g.Cp) * ldm;
-#pragma unroll
-  for (int r = 0; r < T; ++r)
-#pragma unroll
-    for (int s = 0; s < T; ++s) {
-      const float* ptr = src + (r * T + s) * pstride;
-      if constexpr (TPT == 4) {
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(ptr));
-        mm[0][r][s] = v.x; mm[1][r][s] = v.y; mm[2][r][s] = v.z; mm[3][r][s] = v.w;
-      } else {
-        const float2 v = __ldcg(reinterpret_cast<const float2*>(ptr));
-        mm[0][r][s] = v.x; mm[1][r][s] = v.y;
-      }
-    }
+  // vector row stores need aligned, complete m-wide segments
+  const bool vec_ok = (MO == 4 && (g.Wo & 3) == 0) || (MO == 6 && (g.Wo & 1) == 0);
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
-    const int tl = tq + k;
+    const int tl = base + lane + 32 * k;
     if (tl >= ntile_local) break;
+    float mm[T][T];
+#pragma unroll
+    for (int r = 0; r < T; ++r)
+#pragma unroll
+      for (int s = 0; s < T; ++s) mm[r][s] = __ldcg(src + (r * T + s) * pstride + 32 * k);
     float out[MO][MO];
-    inverse_transform<T>(mm[k], out);
+    inverse_transform<T>(mm, out);
     int b, ty, tx;
     tile_coords(g, tile0 + tl, b, ty, tx);
     const int oy = ty * g.m, ox = tx * g.m;
     float* plane = y + (static_cast<size_t>(b) * g.Cp + cp) * g.Ho * g.Wo;
+    const bool vec = vec_ok && ox + MO <= g.Wo;
 #pragma unroll
     for (int r = 0; r < MO; ++r) {
       if (oy + r >= g.Ho) break;
+      float* row = plane + static_cast<size_t>(oy + r) * g.Wo + ox;
+      if (vec) {
+        if constexpr (MO == 4) {
+          *reinterpret_cast<float4*>(row) = make_float4(out[r][0], out[r][1], out[r][2], out[r][3]);
+        } else if constexpr (MO == 6) {
 #pragma unroll
-      for (int s = 0; s < MO; ++s)
-        if (ox + s < g.Wo) plane[static_cast<size_t>(oy + r) * g.Wo + ox + s] = out[r][s];
+          for (int s = 0; s < 6; s += 2) *reinterpret_cast<float2*>(row + s) = make_float2(out[r][s], out[r][s + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < MO; ++s)
+          if (ox + s < g.Wo) row[s] = out[r][s];
+      }
     }
   }
 }
@@ -281,7 +288,7 @@ static cudaError_t launch_inv_vec_t(const float* M, float* y, const Geo& g, int 
                                     cudaStream_t st) {
   constexpr int TPT = T <= 6 ? 4 : 2;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ceil_div(ceil_div(ntile, TPT), 128), g.Cp);
+  cfg.gridDim = dim3(ceil_div(ntile, 128 * TPT), g.Cp);
   cfg.blockDim = dim3(128);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
