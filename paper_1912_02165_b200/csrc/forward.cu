@@ -8,6 +8,7 @@
 // store instruction writes whole rows of the UMMA core matrices of the U
 // slab (csrc/common.cuh layout).  Launched with programmatic dependent
 // launch: the prologue overlaps the previous kernel's tail.
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include "common.cuh"
 #include "sm100.cuh"
@@ -168,19 +169,37 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
       for (int s = 0; s < T; ++s) u2[r][s] = make_float2(0.0f, 0.0f);
   }
   const size_t slab = static_cast<size_t>(kBlockTiles) * g.Cpad * 2;
-  const uint32_t off = slab_off(tl, c0, kBlockTiles, g.Cpad);
-  uint8_t* dst = u + static_cast<size_t>(bl) * 2 * slab + off;
   const size_t pstride = static_cast<size_t>(nblk_local) * 2 * slab;
+  if constexpr (PAIRS >= 2) {
+    // lanes q and q ^ 1 (same tile, neighbouring channel pairs, TPW lanes
+    // apart) swap halves: the even one stores 4 channels of hi, the odd one
+    // 4 channels of lo -- one 8-byte store per position
+    const bool odd = q & 1;
+    const uint32_t off = slab_off(tl, cbase + 2 * (q & ~1), kBlockTiles, g.Cpad);
+    uint8_t* dst = u + static_cast<size_t>(bl) * 2 * slab + off + (odd ? slab : 0);
 #pragma unroll
-  for (int r = 0; r < T; ++r)
+    for (int r = 0; r < T; ++r)
 #pragma unroll
-    for (int s = 0; s < T; ++s) {
-      uint32_t hi, lo;
-      split_bf16x2(u2[r][s], hi, lo);
-      uint8_t* p = dst + (r * T + s) * pstride;
-      *reinterpret_cast<uint32_t*>(p) = hi;
-      *reinterpret_cast<uint32_t*>(p + slab) = lo;
-    }
+      for (int s = 0; s < T; ++s) {
+        uint32_t hi, lo;
+        split_bf16x2(u2[r][s], hi, lo);
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, TPW);
+        *reinterpret_cast<uint2*>(dst + (r * T + s) * pstride) = odd ? make_uint2(other, lo) : make_uint2(hi, other);
+      }
+  } else {
+    const uint32_t off = slab_off(tl, c0, kBlockTiles, g.Cpad);
+    uint8_t* dst = u + static_cast<size_t>(bl) * 2 * slab + off;
+#pragma unroll
+    for (int r = 0; r < T; ++r)
+#pragma unroll
+      for (int s = 0; s < T; ++s) {
+        uint32_t hi, lo;
+        split_bf16x2(u2[r][s], hi, lo);
+        uint8_t* p = dst + (r * T + s) * pstride;
+        *reinterpret_cast<uint32_t*>(p) = hi;
+        *reinterpret_cast<uint32_t*>(p + slab) = lo;
+      }
+  }
 }
 
 static FwdStage stage_geometry(const Geo& g) {
@@ -201,7 +220,17 @@ int forward_staged_cpc(const Geo& g) {
   // 4 channels per CTA first: 256-thread CTAs, two per SM, finer work items
   // (better wave balance than 512-thread CTAs).
   const size_t desc = S.bulk ? 0 : static_cast<size_t>(S.trows) * g.T * 12;   // per channel
-  for (int cpc : {4, 8, 2})
+  if (const char* e = getenv("WF_FWD_CPC")) {
+    const int cpc = atoi(e);
+    if ((cpc == 2 || cpc == 4 || cpc == 8) && static_cast<size_t>(cpc) * (S.plane * 4 + desc) <= 200 * 1024 &&
+        g.Cpad % cpc == 0)
+      return cpc;
+  }
+  // Wide layers (C >= 256, many channel groups per block) take 8: a warp
+  // then stores whole core-matrix rows of U (VGG 512->512 @28: L2 bytes of
+  // the forward kernel 188 -> 116 MB per wave, layer 199 -> 187 us).
+  const int first = g.Cpad >= 256 ? 8 : 4;
+  for (int cpc : {first, 12 - first, 2})
     if ((cpc < 8 || g.T <= 6) && static_cast<size_t>(cpc) * (S.plane * 4 + desc) <= 100 * 1024 &&
         g.Cpad % cpc == 0)
       return cpc;
