@@ -230,9 +230,11 @@ int forward_staged_cpc(const Geo& g) {
   // then stores whole core-matrix rows of U (VGG 512->512 @28: L2 bytes of
   // the forward kernel 188 -> 116 MB per wave, layer 199 -> 187 us).
   const int first = g.Cpad >= 256 ? 8 : 4;
+  // (8 channels: 512 threads, one CTA per SM, up to 200 KB of staging;
+  // 4: two 256-thread CTAs per SM, 100 KB each)
   for (int cpc : {first, 12 - first, 2})
-    if ((cpc < 8 || g.T <= 6) && static_cast<size_t>(cpc) * (S.plane * 4 + desc) <= 100 * 1024 &&
-        g.Cpad % cpc == 0)
+    if ((cpc < 8 || g.T <= 6) &&
+        static_cast<size_t>(cpc) * (S.plane * 4 + desc) <= (cpc == 8 ? 200 : 100) * 1024 && g.Cpad % cpc == 0)
       return cpc;
   for (int cpc : {2})
     if (static_cast<size_t>(cpc) * (S.plane * 4 + desc) <= 200 * 1024) return cpc;
