@@ -312,7 +312,8 @@ def test_randomized_sweep_like_reference_acceptance():
                                   (2, 256, 256, 28, 28, 3, 1, 1),   # 2-channel I units, 48 KB slots
                                   (3, 256, 256, 56, 56, 3, 1, 1),
                                   (2, 3, 64, 40, 44, 3, 1, 1),      # RGB input: 16-channel K padding
-                                  (2, 16, 64, 16, 24, 3, 1, 1)])
+                                  (2, 16, 64, 16, 24, 3, 1, 1),
+                                  (2, 64, 64, 28, 28, 3, 1, 0)])    # pad_hi 0: odd output width
 def test_warp_specialised_kernel(dims, monkeypatch):
     """The warp-specialised fused kernel (F(4x4,3x3), C in {64, 128}, C' in
     {64, 128, 256}, and C = C' = 256; W % 4 == 0, pad 1 -- the c2 benchmark layer and the
@@ -349,7 +350,8 @@ def _check_ws(dims, t, monkeypatch):
                                   (1, 128, 128, 112, 112, 3, 1, 1),
                                   (3, 16, 16, 28, 28, 3, 1, 1),     # C' < 64: G units of N = C'
                                   (2, 32, 32, 56, 56, 3, 1, 1),
-                                  (8, 16, 16, 56, 56, 3, 1, 1)])
+                                  (8, 16, 16, 56, 56, 3, 1, 1),
+                                  (2, 64, 64, 28, 32, 3, 1, 0)])    # pad_hi 0: odd output width
 def test_warp_specialised_kernel_f6(dims, monkeypatch):
     """The warp-specialised fused kernel for F(6x6,3x3) (T = 8, C = C' in
     {16, 32, 64, 128}: the c5 sweep's layers) -- thread per (tile, channel)
