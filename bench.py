@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--precision", default="3xbf16", choices=["3xbf16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=4, help="batch slices of the host-buffer pipeline")
+    ap.add_argument("--e2e-split", default=None, help="explicit slice sizes, e.g. 8,24,24,8 (overrides --e2e-chunks)")
     return ap.parse_args()
 
 
@@ -325,7 +326,8 @@ def run_ours(args):
     # the layer and the downloads of different slices overlap
     x_host = torch.from_numpy(x_np).pin_memory()
     y_host = torch.empty(spec.output_dims(), dtype=torch.float32, pin_memory=True)
-    pipe = wf.HostPipeline(spec, pack, cfg, chunks=args.e2e_chunks)
+    split = [int(v) for v in args.e2e_split.split(",")] if args.e2e_split else None
+    pipe = wf.HostPipeline(spec, pack, cfg, chunks=args.e2e_chunks, split=split)
     for _ in range(2):
         pipe(x_host, y_host)
     torch.cuda.synchronize(dev)
@@ -382,7 +384,8 @@ def run_ours(args):
                          "unit_of_launch": "one fused layer call (all its kernels)"},
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": int(x_np.nbytes),
                     "d2h_bytes_per_step": int(np.prod(spec.output_dims()) * 4), "ms_per_step": e2e_ms,
-                    "api": f"HostPipeline(chunks={args.e2e_chunks}): pinned host in/out, copies overlap compute"},
+                    "api": f"HostPipeline({'split=' + args.e2e_split if args.e2e_split else 'chunks=' + str(args.e2e_chunks)}): "
+                           "pinned host in/out, copies overlap compute"},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

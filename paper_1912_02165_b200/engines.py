@@ -503,20 +503,27 @@ class HostPipeline:
     """
 
     def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None, chunks: int = 8,
-                 graph: bool = True):
+                 graph: bool = True, split=None):
         cfg = config or EngineConfig(kind="fused")
         self.use_graph = graph
         self._graph = None
         self._graph_key = None
-        if chunks < 1:
-            raise InvalidParameterError("chunks must be >= 1")
         self.spec, self.cfg = spec, cfg
-        chunks = min(chunks, spec.batch)
-        base, extra = divmod(spec.batch, chunks)
+        if split is not None:
+            # explicit slice sizes (e.g. small first / last slices shorten the
+            # pipeline's fill and drain)
+            sizes = [int(v) for v in split]
+            if not sizes or min(sizes) < 1 or sum(sizes) != spec.batch:
+                raise InvalidParameterError("split must be positive slice sizes summing to the batch")
+        else:
+            if chunks < 1:
+                raise InvalidParameterError("chunks must be >= 1")
+            chunks = min(chunks, spec.batch)
+            base, extra = divmod(spec.batch, chunks)
+            sizes = [base + (1 if i < extra else 0) for i in range(chunks)]
         self.bounds = []
         b0 = 0
-        for i in range(chunks):
-            nb = base + (1 if i < extra else 0)
+        for nb in sizes:
             self.bounds.append((b0, b0 + nb))
             b0 += nb
         torch = _dev.torch
