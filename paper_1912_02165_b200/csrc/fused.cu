@@ -48,9 +48,14 @@ static size_t block_bytes(const Geo& g) {
 // L2-sized block would leave most SMs idle and the wave loop would be
 // launch-bound.
 static int wave_blocks(const Geo& g) {
+  if (const char* e = getenv("WF_WAVE_BLOCKS")) return std::max(1, std::min(g.n_blk, atoi(e)));
   size_t nb = budget_cfg() / lanes_cfg() / block_bytes(g);
   const int n_nc = ceil_div(g.Cppad, gemm_nc(g.Cppad));
-  const size_t nb_par = static_cast<size_t>(ceil_div(2 * 148, g.P * n_nc));
+  // FFT-16 layers with a resident-V GEMM (C'pad <= 128): the forward and
+  // inverse kernels (128 CTAs per block) want larger waves (measured c4
+  // 64->64 @56: 3 -> 7 blocks per wave, 257 -> 244 us)
+  const int par = (g.fft && gemm_resident_fits(g)) ? 6 : 2;
+  const size_t nb_par = static_cast<size_t>(ceil_div(par * 148, g.P * n_nc));
   if (nb < nb_par) nb = nb_par;
   if (nb < 1) nb = 1;
   if (nb > static_cast<size_t>(g.n_blk)) nb = g.n_blk;
