@@ -48,6 +48,7 @@ CONFIGS = {
     "vgg6": (32, 256, 256, 56, 6, "he", "normal"),
     "vgg9": (32, 512, 512, 28, 6, "he", "normal"),
     "c5_32_112": (256, 32, 32, 112, 8, "he", "uniform"),
+    "c5_16_112": (256, 16, 16, 112, 8, "he", "uniform"),
     "c5_128_56": (256, 128, 128, 56, 8, "he", "uniform"),
 }
 

@@ -107,6 +107,7 @@ struct Params {
   int* counters;          // doneF, doneG, doneI (n_blk each)
   Geo g;
   int NU, NM, L2;
+  int gbatch;             // G units per completion publish (one fence per batch)
   int passes;
   int discard;            // drop consumed ring lines from L2 (WF_WS_DISCARD bits: 1 U, 2 M)
   int dbg;                // tuning aid (WF_WS_DBG=3: no GEMM work, results invalid)
@@ -193,6 +194,10 @@ __device__ __forceinline__ void red_release_cta_smem(int* p, int v) {
 // scope acquire that preceded it -- before the counter increment).
 __device__ __forceinline__ void red_release_gpu(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_gpu(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ int atom_acqrel_cta_smem(int* p, int v) {
   int old;
@@ -882,7 +887,17 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
       // this buffer first)
       if (atom_acqrel_cta_smem(&sy.g_cnt[buf], 1) == 4 * (k / kNAcc) + 3) {
         const long long t1 = pf.now();
-        red_release_gpu(P.counters + P.g.n_blk + b, 1);
+        if (P.gbatch == 1) {
+          red_release_gpu(P.counters + P.g.n_blk + b, 1);
+        } else if (k % P.gbatch == P.gbatch - 1 || b + gu.step >= P.g.n_blk) {
+          // batched publish (narrow C': the fence, not the GEMM, bounds the
+          // G roles): acquire the batch's earlier units through their
+          // completion counts, one fence, then the counts of every unit
+          const int k0 = k - k % P.gbatch;
+          for (int j = k0; j < k; ++j) (void)ld_acquire_cta_smem(&sy.g_cnt[j % kNAcc]);
+          fence_acq_rel_gpu();
+          for (int j = k0; j <= k; ++j) red_relaxed_gpu(P.counters + P.g.n_blk + gu.b0 + j * gu.step, 1);
+        }
         trace<PROF>(b, 3, false);
         pf.add(kPubFence, t1);
       }
@@ -1161,6 +1176,15 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   return ws::with_shape(g, [&](auto s) {
     using S = decltype(s);
     P.n_fi = g.n_blk * (S::kNCG + S::kNIG);
+    // G publishes batched for C' <= 32 (4 units per fence).  A batch delays
+    // the publish of its first unit until its last unit (step * (batch - 1)
+    // blocks later) is done, which must stay inside the ring and lag slack
+    // the deadlock-freedom argument uses.
+    const int step = std::max(1, sm_count / (S::kP * S::kNG));
+    int gb = S::CP <= 32 ? 4 : 1;
+    if (const char* e = getenv("WF_WS_GBATCH")) gb = std::max(1, std::min(ws::kNAcc, atoi(e)));
+    while (gb > 1 && (gb - 1) * step >= std::min(P.L2, std::min(P.NU, P.NM))) --gb;
+    P.gbatch = gb;
     return ws::launch_t<S>(P, sm_count, st);
   });
 }

@@ -360,6 +360,14 @@ def test_warp_specialised_kernel_f6(dims, monkeypatch):
     _check_ws(dims, 8, monkeypatch)
 
 
+@pytest.mark.parametrize("gbatch", ["1", "2", "4"])
+def test_warp_specialised_batched_g_publish(gbatch, monkeypatch):
+    """Batched G completion publishes (one fence per WF_WS_GBATCH units, the
+    C' <= 32 default is 4) with small rings: bitwise equal to three-stage."""
+    monkeypatch.setenv("WF_WS_GBATCH", gbatch)
+    _check_ws((8, 16, 16, 56, 56, 3, 1, 1), 8, monkeypatch)
+
+
 def test_planned_layer_skips_counter_reset_safely(monkeypatch):
     """LayerPlan calls wf_conv_fused_planned: the warp-specialised kernel
     leaves its dependency counters zero and repeated calls skip the reset;
