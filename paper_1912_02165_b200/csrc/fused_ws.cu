@@ -1059,9 +1059,10 @@ static Plan plan_t(const Geo& g) {
   // that keeps a fixed number of units between a block's F and I units
   // shrinks with the units per step (measured best: c2, 32 units per step,
   // 32 steps; VGG 64->128 / 128->128 / 128->256 / 256->256, 48 / 64 / 96 /
-  // 192 units, 16 / 12 / 8 / 4 steps; c5 64->64 and 128->128 about the same)
+  // 192 units, 16 / 12 / 8 / 4 steps; c5 64->64 and 128->128 about the same;
+  // c5 16->16, 16 units, 64 steps with 8-unit G publish batches)
   const int units = S::kNCG + S::kNIG;
-  int lag = units <= 32 ? 32 : std::max(4, std::min(32, 768 / units));
+  int lag = units <= 16 ? 64 : units <= 32 ? 32 : std::max(4, std::min(32, 768 / units));
   if (const char* e = getenv("WF_WS_LAG")) lag = atoi(e);
   // deadlock freedom: some L1 with 1 <= L1 < NU (when F waits on G) and L2 - L1 < NM
   const int lmax = (pl.NU >= g.n_blk ? g.n_blk + pl.NM : pl.NU + pl.NM - 2);
@@ -1181,7 +1182,7 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
     // blocks later) is done, which must stay inside the ring and lag slack
     // the deadlock-freedom argument uses.
     const int step = std::max(1, sm_count / (S::kP * S::kNG));
-    int gb = S::CP <= 32 ? 4 : 1;
+    int gb = S::CP <= 16 ? 8 : S::CP <= 32 ? 4 : 1;
     if (const char* e = getenv("WF_WS_GBATCH")) gb = std::max(1, std::min(ws::kNAcc, atoi(e)));
     while (gb > 1 && (gb - 1) * step >= std::min(P.L2, std::min(P.NU, P.NM))) --gb;
     P.gbatch = gb;
