@@ -312,6 +312,7 @@ def test_randomized_sweep_like_reference_acceptance():
                                   (2, 256, 256, 28, 28, 3, 1, 1),   # 2-channel I units, 48 KB slots
                                   (3, 256, 256, 56, 56, 3, 1, 1),
                                   (2, 3, 64, 40, 44, 3, 1, 1),      # RGB input: 16-channel K padding
+                                  (16, 3, 64, 56, 56, 3, 1, 1),     # 25 blocks: padding F units skipped on reuse
                                   (2, 16, 64, 16, 24, 3, 1, 1),
                                   (2, 64, 64, 28, 28, 3, 1, 0)])    # pad_hi 0: odd output width
 def test_warp_specialised_kernel(dims, monkeypatch):
