@@ -1,20 +1,31 @@
 """Benchmark: direct-convolution-equivalent TFLOP/s of the fused transformed
-convolution layer on B200, with roofline fraction and the CPU baseline.
-
-Default workload (BASELINE.json configs[1], "c2"): ResNet-50 stage-1 3x3
-layer, Winograd F(4x4,3x3) (T=6), B=64, C=C'=64, 56x56, stride 1, pad 1,
-fp32 N(0,1) inputs, He-normal weights, 3xBF16 tensor-core mode.  A step is
-one fused layer over one batch already resident in HBM; the L2 (126 MB)
-is flushed before every timed step because input + output (103 MB) would
-otherwise stay L2-resident.
+convolution on B200, with roofline fraction, end-to-end time and the CPU
+baseline -- for every BASELINE.json config.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1|c2|c3|c4|c5] [--engine fused|three_stage]
 
-N > 1 is launched by torch.distributed.run, one rank per GPU; the batch is
-sharded (weak scaling: B=64 per rank, no collective on the data path) and
-the time is the max over ranks.  ``--impl reference`` times the
-reference's CPU algorithm (the bit-exact C port in oracle/, all host
-threads) on a bounded sample and prints the same JSON line.
+Configs (BASELINE.json "configs"; SURVEY.md 8(a) shorthand):
+  c1  F(2x2,3x3) B=1, 64->64 @56 (the reference's CPU-runnable case)
+  c2  F(4x4,3x3) B=64, 64->64 @56 -- the default headline: configs[1], the
+      layer the metric is quoted on, fits one GPU
+  c3  the 13 VGG-16 3x3 layers, F(4x4,3x3), B=32; layers whose shapes chain
+      (no pooling in between) run as LayerStack segments
+  c4  FFT-16 overlap-save on the four ResNet 3x3 shapes, B=128
+  c5  F(6x6,3x3) sweep, C=C' in {16,32,64,128} x H=W in {28,56,112}, B=256
+      (sharded over the GPUs: strong scaling)
+A step is one pass over the config's layers with inputs resident in HBM;
+the L2 (126 MB) is flushed (256 MB write) before every timed step.  The
+default run prints ONE JSON line: the headline config's numbers plus a
+"per_config" block with every other config (fused and three-stage times,
+per-layer roofline fractions).
+
+N > 1: one rank per GPU (torch.distributed.run; spawned by this script if
+WORLD_SIZE is unset).  c2 is weak-scaled (B=64 per rank), c5 strong-scaled
+(B=256 total); no collective on the data path, time = max over ranks.
+``--impl reference`` times the reference's CPU algorithm (the bit-exact C
+port in oracle/, all host threads) on the same config and prints the same
+line with "impl": "reference".
 """
 
 from __future__ import annotations
@@ -22,6 +33,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,92 +46,139 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Direct-conv-equivalent TFLOP/s per layer & fraction of B200 roofline"
+HEADLINE = "c2"
+
+
+class LayerDef:
+    """One benchmark layer: spec dims, tile (16 = FFT-16), input distribution, seed."""
+
+    def __init__(self, name, batch, c, cp, hw, tile, dist, seed):
+        self.name, self.batch, self.c, self.cp, self.hw = name, batch, c, cp, hw
+        self.tile, self.dist, self.seed = tile, dist, seed
+
+    @property
+    def transform(self):
+        return "fft" if self.tile == 16 else "winograd"
+
+    def spec(self, batch=None):
+        import paper_1912_02165_b200 as wf
+        return wf.LayerSpec(batch or self.batch, self.c, self.cp, self.hw, self.hw, 3, 1, 1)
+
+    def label(self):
+        kind = "FFT-16" if self.tile == 16 else f"F({self.tile - 2}x{self.tile - 2},3x3)"
+        return f"{self.name} {kind} {self.c}->{self.cp} @{self.hw}"
+
+    def inputs(self, batch=None, b0=0):
+        """Seeded input images [b0, b0 + batch) and weights (reference seed
+        convention bench.py:110-112: layer i input 1234 + 1000 i, kernels + 1).
+        Image k is generated from its own stream so any batch slice (a shard,
+        a CPU sample) is a slice of the same full-batch tensor."""
+        spec = self.spec(batch)
+        nb = spec.batch
+        x = np.empty(spec.input_dims(), np.float32)
+        for k in range(nb):
+            rng = np.random.default_rng([self.seed, b0 + k])
+            if self.dist == "uniform":
+                x[k] = rng.uniform(-1.0, 1.0, x.shape[1:]).astype(np.float32)
+            else:
+                x[k] = rng.standard_normal(x.shape[1:]).astype(np.float32)
+        std = np.sqrt(2.0 / (9 * self.c)) if self.dist != "inv_sqrt" else 1.0 / np.sqrt(9 * self.c)
+        w = (np.random.default_rng(self.seed + 1).standard_normal(spec.kernel_dims()) * std).astype(np.float32)
+        return spec, x, w
+
+
+def _vgg():
+    shapes = [(3, 64, 224), (64, 64, 224), (64, 128, 112), (128, 128, 112), (128, 256, 56), (256, 256, 56),
+              (256, 256, 56), (256, 512, 28), (512, 512, 28), (512, 512, 28), (512, 512, 14), (512, 512, 14),
+              (512, 512, 14)]
+    return [LayerDef(f"L{i + 1}", 32, c, cp, hw, 6, "normal", 1234 + 1000 * i) for i, (c, cp, hw) in enumerate(shapes)]
+
+
 CONFIGS = {
-    # name: (B per GPU, C, C', H=W, tile, weight std rule, input distribution)
-    "c2": (64, 64, 64, 56, 6, "he", "normal"),
-    "c1": (1, 64, 64, 56, 4, "inv_sqrt", "normal"),
-    # c5 (the sweep / scaling config) at its C = 64, 56x56 point: B = 256 per GPU
-    "c5": (256, 64, 64, 56, 8, "he", "uniform"),
-    # tuning shapes (not bench lines): VGG-16 conv2_2 / conv3_x at B = 32
-    "vgg1": (32, 3, 64, 224, 6, "he", "normal"),
-    "vgg2": (32, 64, 64, 224, 6, "he", "normal"),
-    "vgg3": (32, 64, 128, 112, 6, "he", "normal"),
-    "vgg4": (32, 128, 128, 112, 6, "he", "normal"),
-    "vgg6": (32, 256, 256, 56, 6, "he", "normal"),
-    "vgg9": (32, 512, 512, 28, 6, "he", "normal"),
-    "c5_32_112": (256, 32, 32, 112, 8, "he", "uniform"),
-    "c5_16_112": (256, 16, 16, 112, 8, "he", "uniform"),
-    "c5_128_56": (256, 128, 128, 56, 8, "he", "uniform"),
+    "c1": [LayerDef("c1", 1, 64, 64, 56, 4, "inv_sqrt", 1234)],
+    "c2": [LayerDef("c2", 64, 64, 64, 56, 6, "normal", 1234)],
+    "c3": _vgg(),
+    "c4": [LayerDef(f"L{i + 1}", 128, c, c, hw, 16, "normal", 1234 + 1000 * i)
+           for i, (c, hw) in enumerate([(64, 56), (128, 28), (256, 14), (512, 7)])],
+    "c5": [LayerDef(f"{c}@{hw}", 256, c, c, hw, 8, "uniform", 1234 + 1000 * i)
+           for i, (c, hw) in enumerate([(c, hw) for c in (16, 32, 64, 128) for hw in (28, 56, 112)])],
 }
+STRONG = {"c5"}          # configs whose total batch is fixed and sharded over the GPUs
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
     ap.add_argument("--engine", default="fused", choices=["fused", "three_stage"])
     ap.add_argument("--precision", default="3xbf16", choices=["3xbf16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true", help="headline config only")
+    ap.add_argument("--per-config-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=4, help="batch slices of the host-buffer pipeline")
-    ap.add_argument("--e2e-split", default=None, help="explicit slice sizes, e.g. 8,24,24,8 (overrides --e2e-chunks)")
+    ap.add_argument("--cpu-stub", action="store_true",
+                    help="launcher self-test without GPUs: gloo ranks, the CPU oracle on each rank's batch shard "
+                         "of a small layer (tests/test_bench_launcher.py)")
     return ap.parse_args()
 
 
-def layer_inputs(cfg_name, batch=None, seed=1234):
-    import paper_1912_02165_b200 as wf
-    b, c, cp, hw, t, rule, dist = CONFIGS[cfg_name]
-    spec = wf.LayerSpec(batch or b, c, cp, hw, hw, 3, 1, 1)
-    rng = np.random.default_rng(seed)
-    if dist == "uniform":
-        x = rng.uniform(-1.0, 1.0, spec.input_dims()).astype(np.float32)
-    else:
-        x = rng.standard_normal(spec.input_dims()).astype(np.float32)
-    std = np.sqrt(2.0 / (9 * c)) if rule == "he" else 1.0 / np.sqrt(9 * c)
-    w = (np.random.default_rng(seed + 1).standard_normal(spec.kernel_dims()) * std).astype(np.float32)
-    return spec, t, x, w
-
-
-def roofline_terms(spec, t, precision):
-    """Algorithmic bytes / flops of one layer."""
-    m = t - 2
-    n_tile = spec.batch * -(-spec.out_height // m) * -(-spec.out_width // m)
-    q_fused = 4 * (spec.batch * spec.in_channels * spec.height * spec.width
-                   + spec.batch * spec.out_channels * spec.out_height * spec.out_width) \
-        + 4 * t * t * spec.in_channels * spec.out_channels
-    q_three = q_fused + 2 * 4 * t * t * n_tile * (spec.in_channels + spec.out_channels)
-    f_gemm = 2 * n_tile * spec.in_channels * spec.out_channels * t * t
-    return n_tile, q_fused, q_three, f_gemm
-
-
+# ------------------------------------------------------------------ roofline
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         with open(path) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
-    return 6650.0, 1590.0, "fallback"
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
+def roofline_terms(spec, tile, precision="3xbf16"):
+    """Algorithmic bytes / flops of one layer and its roof time."""
+    m = 14 if tile == 16 else tile - 2
+    n_tile = spec.batch * -(-spec.out_height // m) * -(-spec.out_width // m)
+    c, cp = spec.in_channels, spec.out_channels
+    io = 4 * (spec.batch * c * spec.height * spec.width + spec.batch * cp * spec.out_height * spec.out_width)
+    if tile == 16:
+        q_fused = io + 8 * 144 * c * cp
+        q_three = q_fused + 2 * 8 * 144 * n_tile * (c + cp)
+        f_gemm = 8 * n_tile * c * cp * 144
+    else:
+        q_fused = io + 4 * tile * tile * c * cp
+        q_three = q_fused + 2 * 4 * tile * tile * n_tile * (c + cp)
+        f_gemm = 2 * n_tile * c * cp * tile * tile
+    hbm, bf16, _ = measured_peaks()
+    passes = 3 if precision == "3xbf16" else 1
+    t_hbm = q_fused / (hbm * 1e9)
+    t_tc = passes * f_gemm / (bf16 * 1e12)
+    return {"n_tile": n_tile, "q_fused": q_fused, "q_three": q_three, "f_gemm": f_gemm,
+            "t_roof": max(t_hbm, t_tc), "bound": "hbm" if t_hbm >= t_tc else "tensor"}
+
+
+def traffic_from_profiles(cfg_name):
+    """DRAM bytes per launch of the dominant kernel, from the committed ncu capture (profiles/traffic.json)."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        v = d.get(cfg_name)
+        return v.get("fused") if isinstance(v, dict) else v
+    return None
+
+
+# -------------------------------------------------------------------- clocks
 class ClockSampler:
-    """SM clocks / clock-event (throttle) reasons sampled during the timed region.
-
-    Uses NVML directly (the same counters nvidia-smi reads) so that a timed
-    region of a few milliseconds still gets many samples; falls back to one
-    nvidia-smi query per sample when NVML is unavailable.
-    """
+    """SM clocks / clock-event (throttle) reasons sampled during the timed region
+    through NVML (the counters nvidia-smi reads), every 0.5 ms."""
 
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index, period_s=0.0005):
-        self.index = index
-        self.period = period_s
-        self.samples = []            # (wall time, sm_mhz, reasons bitmask)
-        self.window = None           # (t0, t1) of the timed region
-        self.max_mhz = None
+        self.index, self.period = index, period_s
+        self.samples, self.window, self.max_mhz = [], None, None
         self.source = "nvml"
         self._stop = threading.Event()
         self._thread = None
@@ -163,6 +222,7 @@ class ClockSampler:
     def __enter__(self):
         self._thread = threading.Thread(target=self._run, daemon=True)
         self._thread.start()
+        time.sleep(0.05)
         return self
 
     def __exit__(self, *exc):
@@ -173,9 +233,6 @@ class ClockSampler:
         self.window = (t0, t1)
 
     def summary(self):
-        """Samples taken inside the timed region (wall-clock window from the
-        first launch to the final synchronize); if the region was shorter
-        than one sample period, the samples adjacent to it."""
         samples = self.samples
         if self.window is not None:
             t0, t1 = self.window
@@ -192,82 +249,236 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(samples), "source": self.source}
 
 
-def cpu_baseline(cfg_name, t, spec_full, threads=None):
-    """Time the reference algorithm (bit-exact C port, oracle/) on a bounded sample."""
+# ------------------------------------------------------------ distributed
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def spawn_ranks(n):
+    """Re-launch this command under torch.distributed.run with one rank per GPU."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def shard(total, world, rank):
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, base + (1 if rank < extra else 0)
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_config_time(cfg_name, engine="fused", budget_s=12.0, threads=None):
+    """The reference algorithm on every layer's CPU sample (cpu_samples),
+    median of runs per layer -> (direct-eq TFLOP/s, sample description, threads)."""
     from oracle import oracle as O
-    import paper_1912_02165_b200 as wf
     threads = threads or O.threads()
-    sample_b = 2 if spec_full.batch >= 2 else 1
-    spec, _, x, w = layer_inputs(cfg_name, batch=sample_b)
-    pack = O.transform_kernels(w, t)
-    O.conv_fused(x, pack, spec, t, 24, threads=threads)        # warm (page-in, thread pool)
-    times = []
-    deadline = time.perf_counter() + 15.0
-    while len(times) < 3 or (time.perf_counter() < deadline and len(times) < 50):
-        t0 = time.perf_counter()
-        O.conv_fused(x, pack, spec, t, 24, threads=threads)
-        times.append(time.perf_counter() - t0)
-    med = statistics.median(times)
-    return {"value": spec.direct_flops() / med / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"{sample_b} image(s) of {cfg_name} ({spec.in_channels}->{spec.out_channels} @ "
-                      f"{spec.height}x{spec.width}, T={t}), reference fused algorithm (R=24) in the bit-exact "
-                      f"C port oracle/winofuse_oracle.c, median of {len(times)} runs"}
+    samples = cpu_samples(cfg_name, threads)
+    if not samples:
+        return None, "no CPU reference path for this config (FFT-16)", threads
+    flops = secs = 0.0
+    for ld, spec, x, pack in samples:
+        run = (lambda: O.conv_fused(x, pack, spec, ld.tile, 24, threads=threads)) if engine == "fused" else \
+            (lambda: O.conv_three_stage(x, pack, spec, ld.tile, threads=threads))
+        run()
+        times = []
+        t_end = time.perf_counter() + budget_s / len(samples)
+        while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 20):
+            t0 = time.perf_counter()
+            run()
+            times.append(time.perf_counter() - t0)
+        secs += statistics.median(times)
+        flops += spec.direct_flops()
+    return flops / secs / 1e12, ", ".join(f"{ld.name} {spec.batch} img" for ld, spec, _, _ in samples), threads
 
 
-def dist_setup(n):
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != n and world > 1:
-        raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
-    return rank, world, local
+def cpu_samples(cfg_name, threads):
+    """Per layer of the config (FFT-16 has no CPU reference path): a seeded
+    batch sample with >= 8 R=24 tasks per host thread (so the task queue's
+    tail does not inflate the time), at most the layer's batch."""
+    from oracle import oracle as O
+    out = []
+    for ld in CONFIGS[cfg_name]:
+        if ld.tile == 16:
+            continue
+        full = ld.spec()
+        m = ld.tile - 2
+        tiles_per_img = -(-full.out_height // m) * -(-full.out_width // m)
+        nb = min(full.batch, max(1, -(-8 * threads * 24 // tiles_per_img)))
+        spec, x, w = ld.inputs(batch=nb)
+        out.append((ld, spec, x, O.transform_kernels(w, ld.tile)))
+    return out
 
 
 def run_reference(args):
-    rank, world, _ = dist_setup(args.gpus)
+    """The reference's CPU algorithm (oracle/winofuse_oracle.c, the bit-exact
+    C port of kernels.py / engines.py) on all host threads: step s runs the
+    sample of layer s mod L, value = sample flops / time over the K steps."""
+    rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle import oracle as O
-    spec_full, t, _, _ = layer_inputs(args.config)
-    b_total = spec_full.batch * max(world, 1)
     threads = O.threads()
-    sample_b = 2 if spec_full.batch >= 2 else 1
-    spec, _, x, w = layer_inputs(args.config, batch=sample_b)
-    pack = O.transform_kernels(w, t)
-    for _ in range(args.warmup):
-        O.conv_fused(x, pack, spec, t, 24, threads=threads)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.conv_fused(x, pack, spec, t, 24, threads=threads)
-        times.append(time.perf_counter() - t0)
-    total = sum(times)
-    value = spec.direct_flops() * args.steps / total / 1e12
+    samples = cpu_samples(args.config, threads)
+    if not samples:
+        print(json.dumps({"impl": "reference", "unavailable": "FFT-16 has no CPU reference implementation "
+                                                             "(SURVEY.md 8(c))"}), flush=True)
+        return
+
+    def run(k):
+        ld, spec, x, pack = samples[k % len(samples)]
+        if args.engine == "fused":
+            O.conv_fused(x, pack, spec, ld.tile, 24, threads=threads)
+        else:
+            O.conv_three_stage(x, pack, spec, ld.tile, threads=threads)
+        return spec.direct_flops()
+
+    for k in range(max(args.warmup, len(samples))):
+        run(k)
+    flops = 0
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        flops += run(k)
+    secs = time.perf_counter() - t0
+    value = flops / secs / 1e12
+    desc = ", ".join(f"{ld.name} {spec.batch} img" for ld, spec, _, _ in samples)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": f"synthetic {'U(-1,1)' if CONFIGS[args.config][6] == 'uniform' else 'N(0,1)'} inputs, "
-                "He-normal weights (seeded)",
-        "config": {"workload": f"{args.config}: F(4x4,3x3) conv, B={b_total}, C=C'={spec.in_channels}, "
-                               f"{spec.height}x{spec.width}, pad 1 (CPU sample: {sample_b} image(s) per step)",
-                   "tile": t, "engine": "fused (reference algorithm, R=24)"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic seeded inputs (N(0,1); c5 U(-1,1)), He-normal weights",
+        "config": {"workload": _workload(args.config, args.gpus),
+                   "engine": f"{args.engine} (the reference's algorithm, R=24, {threads} host threads)"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample_b} image(s) per step of {args.config}; the reference's fused "
-                                   f"algorithm in the bit-exact C port (oracle/winofuse_oracle.c)"},
+                         "sample": f"step k runs layer k mod {len(samples)}'s sample ({desc}); >= 8 tasks per "
+                                   f"thread; bit-exact C port oracle/winofuse_oracle.c (pinned to the "
+                                   f"reference's outputs, tests/test_oracle.py)"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def traffic_from_profiles(cfg_name):
-    """DRAM bytes per launch of the fused step from the committed ncu summary, if any."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(path):
-        with open(path) as fh:
-            d = json.load(fh)
-        return d.get(cfg_name)
-    return None
+def _workload(cfg, world):
+    layers = CONFIGS[cfg]
+    if cfg == "c2":
+        return f"c2: Winograd F(4x4,3x3) conv, B={64 * world} ({64}/GPU), C=C'=64, 56x56, stride 1, pad 1"
+    if cfg == "c1":
+        return "c1: Winograd F(2x2,3x3) conv, B=1, C=C'=64, 56x56, stride 1, pad 1"
+    names = ", ".join(ld.label().split(" ", 1)[1] for ld in layers)
+    b = layers[0].batch if cfg in STRONG else layers[0].batch * world
+    return f"{cfg}: {len(layers)} layers, B={b}{' (sharded)' if cfg in STRONG else ''}: {names}"
+
+
+# --------------------------------------------------------------- GPU timing
+class ConfigRunner:
+    """Plans every layer of a config on one device (fused or three-stage) and
+    times steps over them with CUDA events on the launching stream."""
+
+    def __init__(self, cfg_name, engine, precision, dev, world=1, rank=0):
+        import torch
+        import paper_1912_02165_b200 as wf
+        self.torch, self.wf = torch, wf
+        self.name, self.engine, self.dev = cfg_name, engine, dev
+        self.layers = CONFIGS[cfg_name]
+        self.items = []          # (LayerDef, spec, LayerPlan-like callable, x_dev)
+        self.groups = []         # lists of item indices run as one LayerStack (chained) or singly
+        if cfg_name in STRONG:
+            b0, nb = shard(self.layers[0].batch, world, rank)
+        for i, ld in enumerate(self.layers):
+            if cfg_name in STRONG:
+                spec, x, w = ld.inputs(batch=nb, b0=b0)
+            else:
+                spec, x, w = ld.inputs()
+                if world > 1:
+                    spec, x, _ = ld.inputs(b0=rank * ld.batch)
+            cfg = wf.EngineConfig(kind=engine, tile=ld.tile, transform=ld.transform, precision=precision,
+                                  device=dev)
+            basis = wf.make_fft_basis(3) if ld.tile == 16 else wf.make_basis(ld.tile)
+            pack = wf.transform_kernels(wf.Tensor4D(w), basis)
+            self.items.append({"ld": ld, "spec": spec, "cfg": cfg, "pack": pack,
+                               "x": torch.from_numpy(x).to(dev)})
+        # chain consecutive layers whose shapes match (VGG stages: no pooling in the reference)
+        i = 0
+        while i < len(self.items):
+            j = i + 1
+            while (cfg_name == "c3" and j < len(self.items)
+                   and self.items[j - 1]["spec"].output_dims() == self.items[j]["spec"].input_dims()):
+                j += 1
+            self.groups.append(list(range(i, j)))
+            i = j
+        self.runs = []
+        for g in self.groups:
+            its = [self.items[k] for k in g]
+            if len(g) > 1:
+                stack = wf.LayerStack([it["spec"] for it in its], [it["pack"] for it in its], [it["cfg"] for it in its])
+                self.runs.append((g, stack.plans, its[0]["x"]))
+            else:
+                plan = wf.LayerPlan(its[0]["spec"], its[0]["pack"], its[0]["cfg"])
+                self.runs.append((g, [plan], its[0]["x"]))
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def variants(self):
+        return [p.variant for _, plans, _ in self.runs for p in plans]
+
+    def step(self, events=None):
+        """One pass over all layers; events: list of (start, end) per layer."""
+        stream = self.torch.cuda.current_stream(self.dev)
+        k = 0
+        for g, plans, x in self.runs:
+            for plan in plans:
+                if events is not None:
+                    events[k][0].record(stream)
+                x = plan(x)
+                if events is not None:
+                    events[k][1].record(stream)
+                k += 1
+
+    def time(self, steps, warmup):
+        torch = self.torch
+        for _ in range(max(warmup, 3)):
+            self.flush.zero_()
+            self.step()
+        torch.cuda.synchronize(self.dev)
+        n = len(self.items)
+        per = [[0.0] * n for _ in range(steps)]
+        evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n)] for _ in range(steps)]
+        tot = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+        stream = torch.cuda.current_stream(self.dev)
+        for s in range(steps):
+            self.flush.zero_()                          # evict the previous step's data from L2
+            tot[s][0].record(stream)
+            self.step(evs[s])
+            tot[s][1].record(stream)
+        torch.cuda.synchronize(self.dev)
+        for s in range(steps):
+            for k in range(n):
+                per[s][k] = evs[s][k][0].elapsed_time(evs[s][k][1])
+        step_ms = [tot[s][0].elapsed_time(tot[s][1]) for s in range(steps)]
+        layer_ms = [statistics.median(per[s][k] for s in range(steps)) for k in range(n)]
+        return step_ms, layer_ms
+
+
+def per_layer_report(runner, layer_ms, three_ms, precision):
+    out = []
+    for k, it in enumerate(runner.items):
+        spec, ld = it["spec"], it["ld"]
+        rt = roofline_terms(spec, ld.tile, precision)
+        ms = layer_ms[k]
+        row = {"layer": ld.label(), "B": spec.batch, "ms": round(ms, 4),
+               "tflops": round(spec.direct_flops() / (ms * 1e-3) / 1e12, 2),
+               "images_per_s": round(spec.batch / (ms * 1e-3), 1),
+               "t_roof_us": round(rt["t_roof"] * 1e6, 2), "bound": rt["bound"],
+               "roofline_frac": round(rt["t_roof"] / (ms * 1e-3), 4),
+               "variant": runner.variants()[k]}
+        if three_ms is not None:
+            row["three_stage_ms"] = round(three_ms[k], 4)
+            row["fused_speedup"] = round(three_ms[k] / ms, 3)
+        out.append(row)
+    return out
 
 
 def run_ours(args):
@@ -276,129 +487,232 @@ def run_ours(args):
     import paper_1912_02165_b200 as wf
     from paper_1912_02165_b200 import _lib
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"--gpus {world} but only {torch.cuda.device_count()} CUDA devices")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    spec, t, x_np, w_np = layer_inputs(args.config, seed=1234 + 1000 * rank)
-    pack = wf.transform_kernels(wf.Tensor4D(w_np), wf.make_basis(t))
-    cfg = wf.EngineConfig(kind=args.engine, tile=t, precision=args.precision, device=dev)
-    x_dev = torch.from_numpy(x_np).to(dev)
-    pack.device_mma(dev)
-    # L2 flush buffer (> 126 MB L2)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
 
-    plan = wf.LayerPlan(spec, pack, cfg)          # allocation + validation once, launches only below
-    for _ in range(max(args.warmup, 3)):
-        flush.zero_()
-        plan(x_dev)
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg_name = args.config
+    runner = ConfigRunner(cfg_name, args.engine, args.precision, dev, world, rank)
+    # headline: the timed region
     torch.cuda.synchronize(dev)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
-    torch.cuda.synchronize(dev)
     launches0 = _lib.load().wf_kernel_launches()
     with ClockSampler(local) as clocks:
-        time.sleep(0.05)                                            # sampler running before the region
         w0 = time.perf_counter()
-        for i in range(args.steps):
-            flush.zero_()                                           # evict input/output from L2
-            starts[i].record(stream)
-            plan(x_dev)
-            ends[i].record(stream)
-        torch.cuda.synchronize(dev)
+        step_ms, layer_ms = runner.time(args.steps, args.warmup)
         clocks.mark(w0, time.perf_counter())
     launches = _lib.load().wf_kernel_launches() - launches0
+    launches_per_step = launches // (args.steps + max(args.warmup, 3))
     if world > 1:
         dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    if world > 1:
-        tt = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-    ms = total_ms / args.steps
+    ms = max_over_ranks(sum(step_ms) / args.steps)
 
-    # end to end through the public API with host buffers (pinned), H2D + D2H
-    # inside: HostPipeline splits the batch into slices so the uploads,
-    # the layer and the downloads of different slices overlap
-    x_host = torch.from_numpy(x_np).pin_memory()
-    y_host = torch.empty(spec.output_dims(), dtype=torch.float32, pin_memory=True)
-    split = [int(v) for v in args.e2e_split.split(",")] if args.e2e_split else None
-    pipe = wf.HostPipeline(spec, pack, cfg, chunks=args.e2e_chunks, split=split)
-    for _ in range(2):
-        pipe(x_host, y_host)
-    torch.cuda.synchronize(dev)
-    e2e_steps = max(3, min(args.steps, 10))
-    if world > 1:
-        dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        pipe(x_host, y_host)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    # three-stage comparison per layer (same config, same protocol)
+    three_ms = None
+    if args.engine == "fused":
+        r3 = ConfigRunner(cfg_name, "three_stage", args.precision, dev, world, rank)
+        _, three_ms = r3.time(max(5, min(args.steps, 10)), 3)
+        del r3
 
-    n_tile, q_fused, q_three, f_gemm = roofline_terms(spec, t, args.precision)
+    # end to end through the public API: pinned host buffers, H2D + D2H inside
+    e2e = None
+    if cfg_name in ("c1", "c2"):
+        it = runner.items[0]
+        x_host = it["x"].cpu().pin_memory()
+        y_host = torch.empty(it["spec"].output_dims(), dtype=torch.float32, pin_memory=True)
+        chunks = min(args.e2e_chunks, it["spec"].batch)
+        pipe = wf.HostPipeline(it["spec"], it["pack"], it["cfg"], chunks=chunks)
+        for _ in range(2):
+            pipe(x_host, y_host)
+        torch.cuda.synchronize(dev)
+        e2e_steps = max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        stream = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            pipe(x_host, y_host)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+        e2e = {"ms_per_step": e2e_ms, "h2d": int(x_host.numel() * 4), "d2h": int(y_host.numel() * 4),
+               "api": f"HostPipeline(chunks={chunks}): pinned host in/out, per-slice H2D / layer / D2H on three "
+                      f"streams, CUDA-graph replay"}
+    else:
+        # multi-layer configs: every layer's input uploaded and output read back per step
+        stream = torch.cuda.current_stream(dev)
+        hosts = [(it["x"].cpu().pin_memory(), torch.empty(it["spec"].output_dims(), dtype=torch.float32,
+                                                           pin_memory=True)) for it in runner.items]
+        e2e_steps = 3
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            k = 0
+            for g, plans, x in runner.runs:
+                xin = x
+                xin.copy_(hosts[k][0], non_blocking=True)
+                for plan in plans:
+                    xin = plan(xin)
+                    hosts[k][1].copy_(xin, non_blocking=True)
+                    k += 1
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+        e2e = {"ms_per_step": e2e_ms, "h2d": int(sum(runner.items[g[0]]["x"].numel() * 4 for g, _, _ in runner.runs)),
+               "d2h": int(sum(np.prod(it["spec"].output_dims()) * 4 for it in runner.items)),
+               "api": "LayerPlan / LayerStack per layer group: pinned host input uploaded and every layer's output "
+                      "downloaded on the compute stream"}
+
+    per_config = {}
+    if not args.no_per_config and cfg_name == HEADLINE:
+        for other in ("c1", "c3", "c4", "c5"):
+            ro = ConfigRunner(other, "fused", args.precision, dev, world, rank)
+            st, lm = ro.time(args.per_config_steps, 3)
+            r3o = ConfigRunner(other, "three_stage", args.precision, dev, world, rank)
+            _, lm3 = r3o.time(args.per_config_steps, 3)
+            tot = max_over_ranks(statistics.median(st))
+            flops = sum(it["spec"].direct_flops() for it in ro.items) * (1 if other in STRONG else world)
+            per_config[other] = {"workload": _workload(other, world), "ms_per_step": tot,
+                                 "value": flops / (tot * 1e-3) / 1e12, "unit": "TFLOP/s",
+                                 "three_stage_ms_per_step": sum(lm3),
+                                 "layers": per_layer_report(ro, lm, lm3, args.precision)}
+            del ro, r3o
+            torch.cuda.empty_cache()
 
     if rank == 0:
-        hbm_peak, bf16_peak, peak_kind = measured_peaks()
-        b_total = spec.batch * world
-        flops_total = spec.direct_flops() * world
-        value = flops_total / (ms * 1e-3) / 1e12
-        e2e_value = flops_total / (e2e_ms * 1e-3) / 1e12
-        achieved = q_fused / (ms * 1e-3) / 1e9
-        passes = 3 if args.precision == "3xbf16" else 1
-        t_roof = max(q_fused / (hbm_peak * 1e9), passes * f_gemm / (bf16_peak * 1e12))
-        cpu = None
+        hbm_peak, bf16_peak, peak_src = measured_peaks()
+        flops_step = sum(it["spec"].direct_flops() for it in runner.items) * (1 if cfg_name in STRONG else world)
+        value = flops_step / (ms * 1e-3) / 1e12
+        layers = per_layer_report(runner, layer_ms, three_ms, args.precision)
+        # the dominant kernel: the layer with the most time
+        dom = max(range(len(runner.items)), key=lambda k: layer_ms[k])
+        dit = runner.items[dom]
+        rt = roofline_terms(dit["spec"], dit["ld"].tile, args.precision)
+        d_ms = layer_ms[dom]
+        if rt["bound"] == "hbm":
+            achieved, peak, unit = rt["q_fused"] / (d_ms * 1e-3) / 1e9, hbm_peak, "GB/s"
+        else:
+            passes = 3 if args.precision == "3xbf16" else 1
+            achieved, peak, unit = passes * rt["f_gemm"] / (d_ms * 1e-3) / 1e12, bf16_peak, "TFLOP/s"
+        cpu = cpu3 = None
         if not args.no_cpu_baseline and world == 1:
             try:
-                cpu = cpu_baseline(args.config, t, spec)
+                v, sample, thr = cpu_config_time(cfg_name, "fused")
+                cpu = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "port",
+                       "sample": f"reference fused algorithm (R=24) in the bit-exact C port oracle/winofuse_oracle.c, "
+                                 f"OpenMP over {thr} host threads; per layer a batch sample with >= 8 tasks per "
+                                 f"thread, median of runs: {sample}"}
+                v3, _, _ = cpu_config_time(cfg_name, "three_stage")
+                cpu3 = {"value": v3, "unit": "TFLOP/s", "cores": thr, "kind": "port",
+                        "sample": "reference three-stage algorithm (engines.py:234-314), same samples"}
             except Exception as exc:  # the baseline is reported, never gating
                 cpu = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 io, bf16x3 split tensor-core (f32 accumulate)"
-            if args.precision == "3xbf16" else "f32 io, bf16 tensor-core",
-            "data": f"synthetic: seeded {'U(-1,1)' if CONFIGS[args.config][6] == 'uniform' else 'N(0,1)'} "
-                    "inputs, He-normal weights (no dataset in the reference)",
-            "config": {"workload": f"{args.config}: Winograd F({t - 2}x{t - 2},3x3) conv, B={b_total} "
-                                   f"({spec.batch}/GPU), C=C'={spec.in_channels}, {spec.height}x{spec.width}, "
-                                   f"stride 1, pad 1", "engine": args.engine, "tile": t,
-                       "precision": args.precision, "l2": "flushed (256 MB write) before every timed step",
-                       "images_per_s": b_total / (ms * 1e-3), "parallelism": f"batch shards x{world}"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic_from_profiles(args.config),
-                         "peak_source": peak_kind,
-                         "algorithmic_bytes_per_step": q_fused, "three_stage_bytes_per_step": q_three,
-                         "t_roof_us": t_roof * 1e6, "t_roof_frac": t_roof / (ms * 1e-3),
-                         "unit_of_launch": "one fused layer call (all its kernels)"},
-            "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": int(x_np.nbytes),
-                    "d2h_bytes_per_step": int(np.prod(spec.output_dims()) * 4), "ms_per_step": e2e_ms,
-                    "api": f"HostPipeline({'split=' + args.e2e_split if args.e2e_split else 'chunks=' + str(args.e2e_chunks)}): "
-                           "pinned host in/out, copies overlap compute"},
-            "gpu_launches": int(launches),
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if cfg_name in STRONG else "weak", "vs_baseline": None,
+            "dtype": "f32 io, bf16x3 split tensor-core (f32 accumulate)" if args.precision == "3xbf16"
+            else "f32 io, bf16 tensor-core",
+            "data": "synthetic: seeded N(0,1) (c5: U(-1,1)) inputs, He-normal weights (the reference uses no dataset)",
+            "config": {"workload": _workload(cfg_name, world), "engine": args.engine, "precision": args.precision,
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "images_per_s": runner.items[0]["spec"].batch * (1 if cfg_name in STRONG else world)
+                       / (ms * 1e-3), "parallelism": f"batch shards x{world}", "variants": runner.variants()},
+            "roofline": {"bound": rt["bound"], "achieved": achieved, "peak": peak, "unit": unit,
+                         "frac": achieved / peak, "traffic": traffic_from_profiles(cfg_name),
+                         "kernel": f"{dit['ld'].label()} ({runner.variants()[dom] or args.engine})",
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": rt["q_fused"],
+                         "three_stage_bytes": rt["q_three"], "t_roof_us": rt["t_roof"] * 1e6,
+                         "launch_ms": d_ms,
+                         "definition": "achieved = Q_fused (input + output + pack bytes, SURVEY 8(d)) / the "
+                                       "layer's CUDA-event time on its stream (hbm-bound), or the GEMM's 3-pass "
+                                       "flops / time (tensor-bound)"},
+            "layers": layers,
+            "e2e": {"value": flops_step / (e2e["ms_per_step"] * 1e-3) / 1e12, "unit": "TFLOP/s",
+                    "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                    "ms_per_step": e2e["ms_per_step"], "api": e2e["api"]},
+            "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
+            "cpu_baseline_three_stage": cpu3,
         }
+        if per_config:
+            line["per_config"] = per_config
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_cpu_stub(args):
+    """The multi-rank protocol of run_ours with the CPU oracle as the compute:
+    gloo process group, per-rank batch shard, barrier-bracketed timed
+    region, max over ranks, one line from rank 0 (and the gathered output's
+    checksum, equal to the single-rank run's)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1912_02165_b200 as wf
+    from oracle import oracle as O
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    ld = LayerDef("stub", 8, 8, 8, 12, 6, "normal", 99)
+    b0, nb = shard(ld.batch, world, rank)
+    spec, x, w = ld.inputs(batch=nb, b0=b0)
+    pack = O.transform_kernels(w, ld.tile)
+    for _ in range(args.warmup):
+        O.conv_fused(x, pack, spec, ld.tile, 24, threads=1)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        y = O.conv_fused(x, pack, spec, ld.tile, 24, threads=1)
+    dt = time.perf_counter() - t0
+    parts = [torch.from_numpy(y)]
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([dt], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+        sizes = [shard(ld.batch, world, r)[1] for r in range(world)]
+        buf = torch.zeros((max(sizes),) + tuple(y.shape[1:]))
+        buf[:nb] = torch.from_numpy(y)
+        got = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(got, buf)
+        parts = [g[:n] for g, n in zip(got, sizes)]
+    full = torch.cat(parts).numpy()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": ld.spec().direct_flops() * args.steps / dt / 1e12,
+                          "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "stub": True,
+                          "checksum": float(np.sum(full.astype(np.float64) * np.arange(1, full.size + 1).reshape(
+                              full.shape) % 7))}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.cpu_stub:
+        run_cpu_stub(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -80,24 +80,72 @@ int wf_conv_three_stage(const float* x, const void* mma_pack, float* y, void* sc
                         size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
                         int precision, void* stream);
 
+/* The three stages as separate launches (phases: WF_PHASE_* bits), so a
+ * caller can time each with events -- the reference's per-stage phase_s
+ * (engines.py:263-302).  Run in order on one stream over the same scratch. */
+#define WF_PHASE_FORWARD 1
+#define WF_PHASE_MULTIPLY 2
+#define WF_PHASE_INVERSE 4
+int wf_conv_three_stage_phases(const float* x, const void* mma_pack, float* y, void* scratch,
+                               size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
+                               int precision, int phases, void* stream);
+
 /* conv_fused (winofuse/engines.py:317-444): the transformed tiles never make
- * an HBM round trip.  `r` is the tile-task size (tiles per CTA task, the
- * reference's R, engines.py:57); 0 picks the kernel's native size. */
+ * an HBM round trip.  `r` is the reference's tiles-per-task knob
+ * (engines.py:57); the sm_100a kernels use 128-tile blocks (the MMA M) and
+ * ignore it. */
 size_t wf_fused_scratch_bytes(const wf_layer* layer, int tile, int transform, int r);
 int wf_conv_fused(const float* x, const void* mma_pack, float* y, void* scratch,
                   size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
                   int precision, int r, void* stream);
 
-/* wf_conv_fused for a caller that owns `scratch` for this one layer (a
- * planned layer, engines.LayerPlan): with WF_FUSED_COUNTERS_CLEAN the caller
- * asserts that the scratch's dependency counters are zero -- it zeroed the
- * scratch once and only calls this layer's fused engine on it -- and the
- * per-call counter reset is skipped (the kernel leaves them zero again).
- * Same results as wf_conv_fused. */
+/* Fused-engine variants: which kernel runs the layer. */
+#define WF_FUSED_AUTO 0  /* the fastest variant that can hold the layer               */
+#define WF_FUSED_WS 1    /* warp-specialised persistent dataflow kernel (fused_ws.cu)  */
+#define WF_FUSED_ITEMQ 2 /* item-queue persistent dataflow kernel (fused_persistent.cu)*/
+#define WF_FUSED_WAVES 3 /* the stage kernels per L2-resident wave of blocks (fused.cu) */
+
+/* Flags.  COUNTERS_CLEAN: the caller asserts that the scratch's dependency
+ * counters are zero -- it zero-filled the scratch once and only runs this
+ * layer's fused engine on it -- so the per-call counter reset is skipped
+ * (the warp-specialised kernel leaves them zero again).  INSTRUMENT: run the
+ * instrumented kernel (ordering tickets + per-role busy cycles, read back
+ * with wf_fused_instrument_read); warp-specialised variant only. */
 #define WF_FUSED_COUNTERS_CLEAN 1
+#define WF_FUSED_INSTRUMENT 2
+
+/* Per-call options; zero-initialise for the defaults. */
+typedef struct wf_fused_opts {
+  int variant;       /* WF_FUSED_*                                                    */
+  int flags;         /* WF_FUSED_COUNTERS_CLEAN | WF_FUSED_INSTRUMENT                 */
+  size_t ring_bytes; /* L2 ring budget of the persistent kernels (EngineConfig.l2_budget_bytes), 0 = default */
+  int lag;           /* steps between a block's producer and consumer units, 0 = default */
+  int gbatch;        /* G completions per publish (warp-specialised), 0 = default    */
+} wf_fused_opts;
+
+/* The variant that runs (> 0), or -WF_ERR_* (e.g. -WF_ERR_UNSUPPORTED when
+ * the requested variant cannot hold the layer). */
+int wf_fused_variant(const wf_layer* layer, int tile, int transform, const wf_fused_opts* opts);
+size_t wf_fused_scratch_bytes_ex(const wf_layer* layer, int tile, int transform, const wf_fused_opts* opts);
+/* *variant_ran (may be NULL) = the variant that ran: the requested or picked
+ * one, or WF_FUSED_WAVES when a persistent kernel's CTAs cannot all be
+ * resident on the device (the waves need no co-residency). */
+int wf_conv_fused_ex(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
+                     const wf_layer* layer, int tile, int transform, int precision, const wf_fused_opts* opts,
+                     int* variant_ran, void* stream);
+/* wf_conv_fused_ex with opts = {WF_FUSED_AUTO, flags}. */
 int wf_conv_fused_planned(const float* x, const void* mma_pack, float* y, void* scratch,
                           size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
                           int precision, int flags, void* stream);
+/* After an instrumented launch (synchronises the device): events = 8 words
+ * per 128-tile block (ordering tickets: 0 F start << 12 | CTA, 1 ~F end,
+ * 2 G start, 3 ~G end, 4 I start, 5 ~I end), role_cycles[4] = SM cycles summed
+ * over CTAs of the F units, the G epilogue and the I units, then the SM clock
+ * in kHz, ring_slots = the
+ * U and M ring slots of the plan.  Returns the number of blocks or -WF_ERR_*. */
+int wf_fused_instrument_read(const wf_layer* layer, int tile, int transform, const wf_fused_opts* opts,
+                             unsigned long long* events, int n_events, unsigned long long* role_cycles,
+                             int* ring_slots);
 
 /* conv_direct (winofuse/engines.py:213-231, kernels.py:22-49): 7-loop
  * cross-correlation with float64 accumulation, one f32 store. */

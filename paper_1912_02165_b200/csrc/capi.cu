@@ -5,6 +5,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <cuda_bf16.h>
 #include "../../include/winofuse_b200.h"
@@ -18,7 +20,51 @@ namespace wf {
 static thread_local std::string g_last_error;
 static std::atomic<unsigned long long> g_launches{0};
 
+int tuning_knob(const char* name, int dflt);
+
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+cudaError_t set_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;   // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({kernel, dev});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[{kernel, dev}] = bytes;
+  return e;
+}
+
+bool coresident_fits(const void* kernel, int grid, int threads, size_t smem) {
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
+  if (set_smem_attr(kernel, static_cast<int>(smem)) != cudaSuccess) return false;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess) return false;
+  if (tuning_knob("WF_DEBUG_LAUNCH", 0))
+    fprintf(stderr, "[wf] coresident: grid %d threads %d smem %zu -> %d CTAs/SM x %d SMs\n", grid, threads, smem,
+            per_sm, sms);
+  return per_sm * sms >= grid;
+}
+
+cudaError_t launch_coresident(const void* kernel, int grid, int threads, size_t smem, cudaStream_t st, void** args) {
+  if (!coresident_fits(kernel, grid, threads, smem)) return cudaErrorCooperativeLaunchTooLarge;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelExC(&cfg, kernel, args);
+}
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -32,6 +78,18 @@ static int fail(int code, const char* fmt, ...) {
 
 static int cuda_fail(cudaError_t e, const char* what) {
   return fail(WF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int tuning_knob(const char* name, int dflt) {
+  static std::mutex mu;
+  static std::map<std::string, int> cache;   // name -> value (dflt when unset)
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(name);
+  if (it != cache.end()) return it->second;
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : dflt;
+  cache[name] = v;
+  return v;
 }
 
 int sm_count() {
@@ -82,6 +140,15 @@ static int make_geo(const wf_layer* L, int tile, int transform, Geo& g) {
   g.Nout = g.fft ? 2 * g.Cp : g.Cp;
   g.n_blk = ceil_div(g.n_tile, kBlockTiles);
   return WF_OK;
+}
+
+// Tensor-core passes of a precision mode (0 = unknown mode).
+static int precision_passes(int precision) {
+  switch (precision) {
+    case WF_PREC_3XBF16: return 3;
+    case WF_PREC_BF16: return 1;
+  }
+  return 0;
 }
 
 int make_geo_public(const wf_layer* L, int tile, int transform, Geo& g) {
@@ -315,14 +382,19 @@ size_t wf_three_stage_scratch_bytes(const wf_layer* layer, int tile, int transfo
   return u + m;
 }
 
-int wf_conv_three_stage(const float* x, const void* mma_pack, float* y, void* scratch,
-                        size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
-                        int precision, void* stream) {
+int wf_conv_three_stage_phases(const float* x, const void* mma_pack, float* y, void* scratch,
+                               size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
+                               int precision, int phases, void* stream) {
   Geo g;
   int rc = make_geo(layer, tile, transform, g);
   if (rc != WF_OK) return rc;
-  if (!x || !mma_pack || !y || !scratch) return fail(WF_ERR_PARAM, "null pointer");
-  if (precision != WF_PREC_3XBF16 && precision != WF_PREC_BF16) return fail(WF_ERR_PARAM, "precision %d", precision);
+  if (!scratch) return fail(WF_ERR_PARAM, "null pointer");
+  if ((phases & WF_PHASE_FORWARD) && !x) return fail(WF_ERR_PARAM, "null pointer");
+  if ((phases & WF_PHASE_MULTIPLY) && !mma_pack) return fail(WF_ERR_PARAM, "null pointer");
+  if ((phases & WF_PHASE_INVERSE) && !y) return fail(WF_ERR_PARAM, "null pointer");
+  if (phases < 1 || phases > 7) return fail(WF_ERR_PARAM, "phases %d", phases);
+  const int passes = precision_passes(precision);
+  if (passes == 0) return fail(WF_ERR_PARAM, "precision %d", precision);
   const size_t need = wf_three_stage_scratch_bytes(layer, tile, transform);
   if (scratch_bytes < need) return fail(WF_ERR_SCRATCH, "scratch %zu < %zu bytes", scratch_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -330,53 +402,125 @@ int wf_conv_three_stage(const float* x, const void* mma_pack, float* y, void* sc
   uint8_t* U = static_cast<uint8_t*>(scratch);
   float* M = reinterpret_cast<float*>(U + P * g.n_blk * 2 * kBlockTiles * g.Cpad * 2);
   const int ldm = g.n_blk * kBlockTiles;
-  cudaError_t e = launch_forward_slab(x, U, g, 0, g.n_blk, st);
-  if (e != cudaSuccess) return cuda_fail(e, "forward");
-  e = launch_position_gemm(U, static_cast<const uint8_t*>(mma_pack), M, g, g.n_blk, ldm, g.n_tile,
-                           precision == WF_PREC_3XBF16 ? 3 : 1, sm_count(), st);
-  if (e != cudaSuccess) return cuda_fail(e, "gemm");
-  e = launch_inverse(M, y, g, 0, g.n_tile, ldm, st);
-  if (e != cudaSuccess) return cuda_fail(e, "inverse");
+  cudaError_t e = cudaSuccess;
+  if (phases & WF_PHASE_FORWARD) {
+    e = launch_forward_slab(x, U, g, 0, g.n_blk, st);
+    if (e != cudaSuccess) return cuda_fail(e, "forward");
+  }
+  if (phases & WF_PHASE_MULTIPLY) {
+    e = launch_position_gemm(U, static_cast<const uint8_t*>(mma_pack), M, g, g.n_blk, ldm, g.n_tile, passes,
+                             sm_count(), st);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm");
+  }
+  if (phases & WF_PHASE_INVERSE) {
+    e = launch_inverse(M, y, g, 0, g.n_tile, ldm, st);
+    if (e != cudaSuccess) return cuda_fail(e, "inverse");
+  }
+  return WF_OK;
+}
+
+int wf_conv_three_stage(const float* x, const void* mma_pack, float* y, void* scratch,
+                        size_t scratch_bytes, const wf_layer* layer, int tile, int transform,
+                        int precision, void* stream) {
+  return wf_conv_three_stage_phases(x, mma_pack, y, scratch, scratch_bytes, layer, tile, transform, precision,
+                                    WF_PHASE_FORWARD | WF_PHASE_MULTIPLY | WF_PHASE_INVERSE, stream);
+}
+
+static int fused_opts(const wf_fused_opts* in, FusedOpts& o) {
+  o = FusedOpts();
+  if (!in) return WF_OK;
+  if (in->variant < WF_FUSED_AUTO || in->variant > WF_FUSED_WAVES) return fail(WF_ERR_PARAM, "variant %d", in->variant);
+  if (in->flags & ~(WF_FUSED_COUNTERS_CLEAN | WF_FUSED_INSTRUMENT)) return fail(WF_ERR_PARAM, "flags %d", in->flags);
+  if (in->lag < 0 || in->gbatch < 0) return fail(WF_ERR_PARAM, "negative lag / gbatch");
+  o.variant = in->variant;
+  o.flags = in->flags;
+  o.ring_bytes = in->ring_bytes;
+  o.lag = in->lag;
+  o.gbatch = in->gbatch;
   return WF_OK;
 }
 
 size_t wf_fused_scratch_bytes(const wf_layer* layer, int tile, int transform, int r) {
-  Geo g;
-  if (make_geo(layer, tile, transform, g) != WF_OK) return 0;
-  return fused_scratch_bytes(g, r);
+  (void)r;
+  return wf_fused_scratch_bytes_ex(layer, tile, transform, nullptr);
 }
 
-static int conv_fused_impl(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
-                           const wf_layer* layer, int tile, int transform, int precision, int r, bool clean,
-                           void* stream);
+size_t wf_fused_scratch_bytes_ex(const wf_layer* layer, int tile, int transform, const wf_fused_opts* opts) {
+  Geo g;
+  FusedOpts o;
+  if (make_geo(layer, tile, transform, g) != WF_OK || fused_opts(opts, o) != WF_OK) return 0;
+  if (fused_pick_variant(g, o) == 0) return 0;
+  return fused_scratch_bytes(g, o);
+}
+
+int wf_fused_variant(const wf_layer* layer, int tile, int transform, const wf_fused_opts* opts) {
+  Geo g;
+  FusedOpts o;
+  int rc = make_geo(layer, tile, transform, g);
+  if (rc != WF_OK) return -rc;
+  rc = fused_opts(opts, o);
+  if (rc != WF_OK) return -rc;
+  const int v = fused_pick_variant(g, o);
+  if (v == 0) return -fail(WF_ERR_UNSUPPORTED, "fused variant %d cannot run this layer", o.variant);
+  return v;
+}
+
+int wf_conv_fused_ex(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
+                     const wf_layer* layer, int tile, int transform, int precision, const wf_fused_opts* opts,
+                     int* variant_ran, void* stream) {
+  Geo g;
+  FusedOpts o;
+  int rc = make_geo(layer, tile, transform, g);
+  if (rc != WF_OK) return rc;
+  rc = fused_opts(opts, o);
+  if (rc != WF_OK) return rc;
+  if (!x || !mma_pack || !y) return fail(WF_ERR_PARAM, "null pointer");
+  const int passes = precision_passes(precision);
+  if (passes == 0) return fail(WF_ERR_PARAM, "precision %d", precision);
+  if (fused_pick_variant(g, o) == 0)
+    return fail(WF_ERR_UNSUPPORTED, "fused variant %d cannot run this layer", o.variant);
+  if ((o.flags & WF_FUSED_INSTRUMENT) && fused_pick_variant(g, o) != kVarWS)
+    return fail(WF_ERR_UNSUPPORTED, "instrumentation is implemented by the warp-specialised variant only");
+  const size_t need = fused_scratch_bytes(g, o);
+  if (need && (!scratch || scratch_bytes < need))
+    return fail(WF_ERR_SCRATCH, "scratch %zu < %zu bytes", scratch_bytes, need);
+  int ran = 0;
+  cudaError_t e = run_fused(x, static_cast<const uint8_t*>(mma_pack), y, static_cast<uint8_t*>(scratch), g, passes,
+                            sm_count(), static_cast<cudaStream_t>(stream), o, &ran);
+  if (variant_ran) *variant_ran = ran;
+  return e == cudaSuccess ? WF_OK : cuda_fail(e, "fused");
+}
 
 int wf_conv_fused(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
                   const wf_layer* layer, int tile, int transform, int precision, int r, void* stream) {
-  return conv_fused_impl(x, mma_pack, y, scratch, scratch_bytes, layer, tile, transform, precision, r, false, stream);
+  if (r < 0) return fail(WF_ERR_PARAM, "tiles per task (r) must be >= 0");
+  return wf_conv_fused_ex(x, mma_pack, y, scratch, scratch_bytes, layer, tile, transform, precision, nullptr, nullptr,
+                          stream);
 }
 
 int wf_conv_fused_planned(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
                           const wf_layer* layer, int tile, int transform, int precision, int flags, void* stream) {
   if (flags & ~WF_FUSED_COUNTERS_CLEAN) return fail(WF_ERR_PARAM, "flags %d", flags);
-  return conv_fused_impl(x, mma_pack, y, scratch, scratch_bytes, layer, tile, transform, precision, 0,
-                         (flags & WF_FUSED_COUNTERS_CLEAN) != 0, stream);
+  wf_fused_opts o = {};
+  o.flags = flags;
+  return wf_conv_fused_ex(x, mma_pack, y, scratch, scratch_bytes, layer, tile, transform, precision, &o, nullptr,
+                          stream);
 }
 
-static int conv_fused_impl(const float* x, const void* mma_pack, float* y, void* scratch, size_t scratch_bytes,
-                           const wf_layer* layer, int tile, int transform, int precision, int r, bool clean,
-                           void* stream) {
+int wf_fused_instrument_read(const wf_layer* layer, int tile, int transform, const wf_fused_opts* opts,
+                             unsigned long long* events, int n_events, unsigned long long* role_cycles,
+                             int* ring_slots) {
   Geo g;
+  FusedOpts o;
   int rc = make_geo(layer, tile, transform, g);
-  if (rc != WF_OK) return rc;
-  if (!x || !mma_pack || !y) return fail(WF_ERR_PARAM, "null pointer");
-  if (precision != WF_PREC_3XBF16 && precision != WF_PREC_BF16) return fail(WF_ERR_PARAM, "precision %d", precision);
-  if (r < 0) return fail(WF_ERR_PARAM, "tiles per task (r) must be >= 0");
-  const size_t need = fused_scratch_bytes(g, r);
-  if (need && (!scratch || scratch_bytes < need))
-    return fail(WF_ERR_SCRATCH, "scratch %zu < %zu bytes", scratch_bytes, need);
-  cudaError_t e = run_fused(x, static_cast<const uint8_t*>(mma_pack), y, static_cast<uint8_t*>(scratch), g,
-                            precision == WF_PREC_3XBF16 ? 3 : 1, r, sm_count(), static_cast<cudaStream_t>(stream), clean);
-  return e == cudaSuccess ? WF_OK : cuda_fail(e, "fused");
+  if (rc != WF_OK) return -rc;
+  rc = fused_opts(opts, o);
+  if (rc != WF_OK) return -rc;
+  if (!events || !role_cycles || !ring_slots) return -fail(WF_ERR_PARAM, "null pointer");
+  if (cudaDeviceSynchronize() != cudaSuccess) return -fail(WF_ERR_CUDA, "synchronize");
+  const int n = ws_instrument_read(g, o, events, n_events, role_cycles, ring_slots);
+  if (n < 0) return -fail(WF_ERR_UNSUPPORTED, "no instrumented warp-specialised plan for this layer");
+  return n;
 }
 
 int wf_conv_direct(const float* x, const float* w, float* y, const wf_layer* layer, void* stream) {

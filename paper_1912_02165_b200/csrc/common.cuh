@@ -17,6 +17,21 @@ __host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / 
 // exported as wf_kernel_launches() so benchmarks can report their launches.
 void note_launch();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for the CURRENT device,
+// remembered per (kernel, device): the attribute is per device, so a
+// process-wide "done" flag would launch without it on a second GPU.
+cudaError_t set_smem_attr(const void* kernel, int bytes);
+
+// Launch a kernel whose CTAs wait on one another (the persistent dataflow
+// kernels): checks that `grid` CTAs fit on the device at once (occupancy x
+// SMs) and launches cooperatively, so the driver schedules every CTA
+// together or fails the launch -- never a partly resident grid spinning on
+// CTAs that cannot start.  cudaErrorCooperativeLaunchTooLarge when they do
+// not fit (the caller falls back to the non-persistent path).
+cudaError_t launch_coresident(const void* kernel, int grid, int threads, size_t smem, cudaStream_t st, void** args);
+// Whether `grid` CTAs of `kernel` (threads, smem) fit on the current device at once.
+bool coresident_fits(const void* kernel, int grid, int threads, size_t smem);
+
 // Layer geometry for one (layer, tile) pair; tile order is batch-major, then
 // tile row, then tile column (reference tiling.py:8-11, 66-75).
 struct Geo {

@@ -247,12 +247,9 @@ __global__ void __launch_bounds__(kInvThreads) fft_inverse_kernel(const float* _
 }  // namespace
 
 cudaError_t launch_fft_forward(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fft_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kFftSmem));
+  {
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(fft_forward_kernel), static_cast<int>(kFftSmem));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   dim3 grid(ceil_div(nblk * kBlockTiles, kFftTiles), ceil_div(g.C, kFftCh));
   note_launch();
@@ -262,12 +259,9 @@ cudaError_t launch_fft_forward(const float* x, uint8_t* u, const Geo& g, int blk
 
 cudaError_t launch_fft_inverse(const float* M, float* y, const Geo& g, int tile0, int ntile, int ldm,
                                cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fft_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kInvSmem));
+  {
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(fft_inverse_kernel), static_cast<int>(kInvSmem));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   dim3 grid(ceil_div(ntile, kInvTiles), ceil_div(g.Cp, kInvCh));
   note_launch();

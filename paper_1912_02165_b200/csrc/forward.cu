@@ -248,11 +248,9 @@ static cudaError_t launch_staged(const float* x, uint8_t* u, const Geo& g, int b
   // staging planes + (non-bulk path) one 12-byte descriptor per staged row
   const int smem = CPC * S.plane * 4 + (S.bulk ? 0 : CPC * S.trows * g.T * 12);
   auto kern = forward_staged_kernel<T, CPC>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  {
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), 200 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nblk, g.Cpad / CPC);

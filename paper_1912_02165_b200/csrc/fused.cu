@@ -23,18 +23,12 @@
 namespace wf {
 
 static constexpr int kMaxLanes = 4;
-// concurrent wave pipelines and the L2 budget of their U + M (WF_WAVE_LANES,
-// WF_WAVE_L2_MB override)
-static int lanes_cfg() {
-  const char* e = getenv("WF_WAVE_LANES");
-  // 3 (measured): VGG 256->512 / 512->512 @28 130 -> 120 / 187 -> 177 us,
-  // the other wave layers (c1, c4, VGG @14) unchanged
-  return e ? std::max(1, std::min(kMaxLanes, atoi(e))) : 3;
-}
-static size_t budget_cfg() {
-  const char* e = getenv("WF_WAVE_L2_MB");
-  return (e ? static_cast<size_t>(atoi(e)) : 56) << 20;
-}
+// concurrent wave pipelines and the L2 budget of their U + M (tuning knobs
+// WF_WAVE_LANES, WF_WAVE_L2_MB)
+// 3 lanes (measured): VGG 256->512 / 512->512 @28 130 -> 120 / 187 -> 177 us,
+// the other wave layers (c1, c4, VGG @14) unchanged
+static int lanes_cfg() { return std::max(1, std::min(kMaxLanes, tuning_knob("WF_WAVE_LANES", 3))); }
+static size_t budget_cfg() { return static_cast<size_t>(tuning_knob("WF_WAVE_L2_MB", 56)) << 20; }
 
 // Bytes of U + M for one 128-tile block.
 static size_t block_bytes(const Geo& g) {
@@ -48,7 +42,7 @@ static size_t block_bytes(const Geo& g) {
 // L2-sized block would leave most SMs idle and the wave loop would be
 // launch-bound.
 static int wave_blocks(const Geo& g) {
-  if (const char* e = getenv("WF_WAVE_BLOCKS")) return std::max(1, std::min(g.n_blk, atoi(e)));
+  if (const int k = tuning_knob("WF_WAVE_BLOCKS", 0)) return std::max(1, std::min(g.n_blk, k));
   size_t nb = budget_cfg() / lanes_cfg() / block_bytes(g);
   const int n_nc = ceil_div(g.Cppad, gemm_nc(g.Cppad));
   // FFT-16 layers with a resident-V GEMM (C'pad <= 128): the forward and
@@ -62,10 +56,31 @@ static int wave_blocks(const Geo& g) {
   return static_cast<int>(nb);
 }
 
-size_t fused_scratch_bytes(const Geo& g, int /*r*/) {
-  if (ws_fits(g)) return ws_scratch_bytes(g);
-  if (persistent_fits(g)) return persistent_scratch_bytes(g);
-  return static_cast<size_t>(lanes_cfg()) * wave_blocks(g) * block_bytes(g);
+size_t waves_scratch_bytes(const Geo& g) {
+  const int wb = wave_blocks(g);
+  const int lanes = std::min(ceil_div(g.n_blk, wb), lanes_cfg());
+  return static_cast<size_t>(lanes) * wb * block_bytes(g);
+}
+
+int fused_pick_variant(const Geo& g, const FusedOpts& o) {
+  switch (o.variant) {
+    case kVarWS: return ws_fits(g, o) ? kVarWS : 0;
+    case kVarItemQueue: return persistent_fits(g, o, false) ? kVarItemQueue : 0;
+    case kVarWaves: return kVarWaves;
+    case kVarAuto: break;
+    default: return 0;
+  }
+  if (ws_fits(g, o)) return kVarWS;
+  if (persistent_fits(g, o, true)) return kVarItemQueue;
+  return kVarWaves;
+}
+
+size_t fused_scratch_bytes(const Geo& g, const FusedOpts& o) {
+  const int v = fused_pick_variant(g, o);
+  size_t own = 0;
+  if (v == kVarWS) own = ws_scratch_bytes(g, o);
+  if (v == kVarItemQueue) own = persistent_scratch_bytes(g, o);
+  return std::max(own, waves_scratch_bytes(g));
 }
 
 struct LaneResources {
@@ -90,38 +105,35 @@ static LaneResources& lane_resources() {
   return r;
 }
 
-// Scratch buffers whose last fused launch was a warp-specialised kernel of
-// the same geometry (which leaves its counters zero).  A caller that owns its
-// scratch (counters_clean) skips the counter reset only when this says the
-// previous launch on that scratch left them clean -- a different kernel or
-// layer in between (environment overrides, shared scratch) forces a reset.
-struct CleanScratch {
-  const void* ptr;
-  size_t key;
-};
-static bool scratch_clean_then_mark(const void* ptr, size_t key, bool clean_after) {
-  static CleanScratch slots[64] = {};
-  static int next = 0;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  bool was = false;
-  int hit = -1;
-  for (int i = 0; i < 64; ++i)
-    if (slots[i].ptr == ptr) { hit = i; was = slots[i].key == key; break; }
-  if (hit < 0) { hit = next; next = (next + 1) % 64; }
-  slots[hit].ptr = ptr;
-  slots[hit].key = clean_after ? key : 0;
-  return was;
+static cudaError_t run_waves(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
+                             int passes, int sm_count, cudaStream_t st);
+
+cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g, int passes,
+                      int sm_count, cudaStream_t st, const FusedOpts& o, int* ran) {
+  const int v = fused_pick_variant(g, o);
+  if (v == 0) return cudaErrorInvalidValue;
+  cudaError_t e = cudaSuccess;
+  if (v == kVarWS) e = run_fused_ws(x, vpack, y, scratch, g, passes, sm_count, st, o);
+  else if (v == kVarItemQueue) e = run_fused_persistent(x, vpack, y, scratch, g, passes, sm_count, st, o);
+  if (v != kVarWaves && e != cudaErrorCooperativeLaunchTooLarge) {
+    if (ran) *ran = v;
+    return e;
+  }
+  // the persistent kernel's CTAs cannot all be resident on this device
+  // (fewer SMs available): the L2 waves need no co-residency
+  if (e == cudaErrorCooperativeLaunchTooLarge) (void)cudaGetLastError();
+  if (ran) *ran = kVarWaves;
+  e = run_waves(x, vpack, y, scratch, g, passes, sm_count, st);
+  // the waves overwrite the warp-specialised kernel's dependency counters
+  // (3 n_blk + 1 ints at the start of the scratch); a caller that keeps them
+  // clean between calls gets them back zeroed
+  if (e == cudaSuccess && v == kVarWS && (o.flags & kFusedCountersClean))
+    e = cudaMemsetAsync(scratch, 0, static_cast<size_t>(3 * g.n_blk + 1) * sizeof(int), st);
+  return e;
 }
 
-cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
-                      int passes, int /*r*/, int sm_count, cudaStream_t st, bool counters_clean) {
-  const bool ws = ws_fits(g);
-  // geometry key of the warp-specialised launch (its counters' extent)
-  const size_t key = ws ? (static_cast<size_t>(g.n_blk) << 20) ^ (static_cast<size_t>(g.C) << 10) ^ g.Cp ^ 1 : 0;
-  const bool clean = counters_clean && scratch_clean_then_mark(scratch, key, ws) && ws;
-  if (ws) return run_fused_ws(x, vpack, y, scratch, g, passes, sm_count, st, clean);
-  if (persistent_fits(g)) return run_fused_persistent(x, vpack, y, scratch, g, passes, sm_count, st);
+static cudaError_t run_waves(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
+                             int passes, int sm_count, cudaStream_t st) {
   const int wb = wave_blocks(g);
   const size_t P = static_cast<size_t>(g.P);
   const size_t lane_bytes = static_cast<size_t>(wb) * block_bytes(g);

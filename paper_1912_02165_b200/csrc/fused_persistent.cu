@@ -737,20 +737,20 @@ struct PersistPlan {
   size_t u_slot, m_slot, counters_bytes, smem;
 };
 
-static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc);
+static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc, const FusedOpts& o);
 
 // Two CTAs per SM (they overlap each other's latency) when T <= 6 and the
 // shared memory fits, else one; forward items of 64 tiles x 8 channels
 // (whole 16-byte core-matrix rows per store) when their input staging fits,
 // else 128 tiles x 4 channels (fewer staged rows per channel, for wide images).
-static PersistPlan persist_plan(const Geo& g) {
+static PersistPlan persist_plan(const Geo& g, const FusedOpts& o) {
   PersistPlan pl = {};
   for (int cps = (g.T <= 6 ? 2 : 1); cps >= 1 && !pl.ok; --cps)
-    for (int cpc = 8; cpc >= 4 && !pl.ok; cpc /= 2) pl = persist_plan_cpc(g, cps, cpc);
+    for (int cpc = 8; cpc >= 4 && !pl.ok; cpc /= 2) pl = persist_plan_cpc(g, cps, cpc, o);
   return pl;
 }
 
-static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
+static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc, const FusedOpts& o) {
   PersistPlan pl = {};
   if (g.fft) return pl;                    // FFT-16 runs the staged L2 waves
   pl.nt = 256;
@@ -761,13 +761,13 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   if (pl.ftiles > kBlockTiles) return pl;
   // up to C' = 256 (one CTA per SM, two GEMM stages; measured VGG 256->256@56
   // 332 -> 313 us against the L2 waves); WF_PERSIST_MAX_CP overrides
-  const int max_cppad = getenv("WF_PERSIST_MAX_CP") ? atoi(getenv("WF_PERSIST_MAX_CP")) : 256;
+  const int max_cppad = tuning_knob("WF_PERSIST_MAX_CP", 256);
   if (g.Cpad % pl.cpc != 0 || g.Cppad > max_cppad) return pl;
   pl.gp = (512 / pl.cps) / g.Cppad;
   if (pl.gp > 8) pl.gp = 8;
-  if (const char* env = getenv("WF_GP")) pl.gp = std::max(1, std::min(pl.gp, atoi(env)));
+  if (const int gp = tuning_knob("WF_GP", 0)) pl.gp = std::max(1, std::min(pl.gp, gp));
   if (pl.gp > g.T * g.T) pl.gp = g.T * g.T;
-  pl.igc = getenv("WF_IGC") ? atoi(getenv("WF_IGC")) : 8;   // c' per I item (thread = tile x c' sub-lane)
+  pl.igc = tuning_knob("WF_IGC", 8);   // c' per I item (thread = tile x c' sub-lane)
   pl.n_cg = (kBlockTiles / pl.ftiles) * (g.Cpad / pl.cpc);
   pl.n_gg = ceil_div(g.T * g.T, pl.gp);
   pl.n_ig = ceil_div(g.Cp, pl.igc);
@@ -803,8 +803,7 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   // pipeline and larger rings with longer lags keep helping, beyond the
   // 126 MB L2 (the spilled part of the rings costs little HBM time here):
   // 100 MB / lag 8: 178 us, 124 / 12: 150 us, 220 / 24: 121 us, 300 / 32: 117 us
-  size_t budget = 300ull << 20;
-  if (const char* env = getenv("WF_L2_BUDGET_MB")) budget = static_cast<size_t>(atoi(env)) << 20;
+  size_t budget = o.ring_bytes ? o.ring_bytes : static_cast<size_t>(tuning_knob("WF_L2_BUDGET_MB", 300)) << 20;
   const int items_per_block = pl.n_cg + pl.n_gg + pl.n_ig;
   const int window = ceil_div(148 * pl.cps, items_per_block) + 1;
   // the lag is a number of blocks; what matters is the work between a
@@ -813,13 +812,14 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
   // fixed 32 left that layer 822 us instead of 520), and the rings need
   // slack beyond lag + window or the producers stall on ring slots
   int lag = std::max(4, std::min(32, (800 + items_per_block / 2) / items_per_block));
-  if (const char* env = getenv("WF_LAG")) lag = atoi(env);
+  if (o.lag > 0) lag = o.lag;
+  else if (const int k = tuning_knob("WF_LAG", 0)) lag = k;
   const int slots = static_cast<int>(budget / (pl.u_slot + pl.m_slot));
   if (slots < 4) return pl;
   if (2 * (lag + window + 2) > slots) lag = slots / 2 - window - 2;
   if (lag < 1) lag = 1;
   int lag2 = lag;                          // inverse items trail the GEMM items by lag2 steps
-  if (const char* env = getenv("WF_LAG2")) lag2 = atoi(env);
+  if (const int k = tuning_knob("WF_LAG2", 0)) lag2 = k;
   if (lag2 < 1) lag2 = 1;
   pl.L1 = lag;
   pl.L2 = lag + lag2;
@@ -838,23 +838,21 @@ static PersistPlan persist_plan_cpc(const Geo& g, int cps, int cpc) {
 // Small layers (a few 128-tile blocks) have no stage overlap to exploit and
 // pay the persistent pipeline's fill and drain: they run as a single L2 wave
 // (three back-to-back kernels on L2-resident intermediates) instead.
-// (WF_PERSIST_MIN_BLOCKS overrides the threshold; tests use it to run the
-// persistent kernel on small layers.)
-static int persist_min_blocks() {
-  const char* env = getenv("WF_PERSIST_MIN_BLOCKS");
-  return env ? atoi(env) : 16;
-}
+// (The automatic dispatch applies the threshold; an explicit WF_FUSED_ITEMQ
+// request runs the kernel on any layer it can hold -- the tests do.)
 // Very narrow layers (Cpad = 16) have too little work per item for the
 // persistent pipeline unless they are large (measured on c5).
-bool persistent_fits(const Geo& g) {
-  const int min_blocks = persist_min_blocks();
-  if (g.n_blk < min_blocks) return false;
-  if (g.Cpad < 32 && g.n_blk < 4 * min_blocks) return false;
-  return persist_plan(g).ok;
+bool persistent_fits(const Geo& g, const FusedOpts& o, bool automatic) {
+  if (automatic) {
+    const int min_blocks = tuning_knob("WF_PERSIST_MIN_BLOCKS", 16);
+    if (g.n_blk < min_blocks) return false;
+    if (g.Cpad < 32 && g.n_blk < 4 * min_blocks) return false;
+  }
+  return persist_plan(g, o).ok;
 }
 
-size_t persistent_scratch_bytes(const Geo& g) {
-  const PersistPlan pl = persist_plan(g);
+size_t persistent_scratch_bytes(const Geo& g, const FusedOpts& o) {
+  const PersistPlan pl = persist_plan(g, o);
   if (!pl.ok) return 0;
   return round_up(static_cast<int>(pl.counters_bytes), 1024) + pl.NU * pl.u_slot + pl.NM * pl.m_slot;
 }
@@ -862,20 +860,27 @@ size_t persistent_scratch_bytes(const Geo& g) {
 template <int T, int NT, int CPS, int KC>
 static cudaError_t launch_persist_t(const PersistParams& P, size_t smem, int grid, cudaStream_t st) {
   auto kern = fused_persistent_kernel<T, NT, CPS, KC>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), 200 * 1024);
+  if (e != cudaSuccess) return e;
+  // No co-residency needed: items are claimed through one atomic counter in
+  // dependency order by CTAs that are already running, so every item a CTA
+  // waits on was claimed earlier by a resident CTA; CTAs that cannot be
+  // resident yet simply start later (and find the queue drained).  The grid
+  // is still sized to what fits at once.
+  int per_sm = 0, sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) == cudaSuccess && per_sm >= 1 &&
+      per_sm * sms < grid)
+    grid = per_sm * sms;
   note_launch();
   kern<<<grid, NT, smem, st>>>(P);
   return cudaGetLastError();
 }
 
 cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g,
-                                 int passes, int sm_count, cudaStream_t st) {
-  const PersistPlan pl = persist_plan(g);
+                                 int passes, int sm_count, cudaStream_t st, const FusedOpts& o) {
+  const PersistPlan pl = persist_plan(g, o);
   if (!pl.ok) return cudaErrorInvalidValue;
   PersistParams P;
   P.x = x; P.y = y; P.vpack = vpack;
@@ -890,11 +895,11 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   P.n_steps = g.n_blk + pl.L2;
   P.n_items = g.n_blk * (pl.n_cg + pl.n_gg + pl.n_ig);
   P.only = 0;
-  if (const char* env = getenv("WF_ONLY")) P.only = atoi(env);
-  P.split_f = 0;
-  if (const char* env = getenv("WF_SPLIT")) P.split_f = atoi(env) * sm_count * pl.cps / 100;
-  P.discard = 0;   // measured neutral-to-slower on c2 (DRAM is not the limiter); kept as an option
-  if (const char* env = getenv("WF_DISCARD")) P.discard = atoi(env);
+#ifdef WF_TUNING_AIDS
+  P.only = tuning_knob("WF_ONLY", 0);      // cost one item kind in isolation (results invalid)
+#endif
+  P.split_f = tuning_knob("WF_SPLIT", 0) * sm_count * pl.cps / 100;
+  P.discard = tuning_knob("WF_DISCARD", 0);   // measured neutral-to-slower on c2 (DRAM is not the limiter)
   P.wreg = pl.wreg; P.trows = pl.trows; P.plane = pl.plane;
   P.f_desc_off = pl.f_desc_off; P.f_max_rows = pl.f_max_rows;
   P.f_bulk = pl.f_bulk; P.f_shift = pl.f_shift;
@@ -903,7 +908,7 @@ cudaError_t run_fused_persistent(const float* x, const uint8_t* vpack, float* y,
   {
     static int prof_state = -1;
     if (prof_state < 0) {
-      prof_state = getenv("WF_PROFILE") ? atoi(getenv("WF_PROFILE")) : 0;
+      prof_state = tuning_knob("WF_PROFILE", 0);
       cudaMemcpyToSymbol(g_prof_on, &prof_state, sizeof(int));
     }
   }

@@ -131,17 +131,27 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 __shared__ unsigned long long s_prof[kProfSlots];
-// per-block event times (ns, PROF build): F first start / last end, G first
-// start (deps satisfied) / last end, I first start / last end
+// Instrumented instance: per-block ordering tickets.  Every unit takes a
+// ticket from one global counter when it starts (after acquiring its
+// dependencies) and when it ends (before its completion is released), so
+// ticket order is consistent with the release/acquire chains of the
+// dependency protocol; a consumer that started before its producer ended,
+// or a producer that rewrote a ring slot before the slot's previous
+// consumer ended, shows up as an inverted ticket pair (the GPU analogue of
+// the reference's operand-overlap check, engines.py:382-396).
+// Events per block (all kept as a minimum, "end" events as ~ticket so the
+// minimum of ~t is the maximum of t): 0 F start (ticket << 12 | CTA of the
+// first F unit), 1 ~F end, 2 G start, 3 ~G end, 4 I start, 5 ~I end.
 constexpr int kTraceBlocks = 4096;
 __device__ unsigned long long g_wstrace[kTraceBlocks * 8];
+__device__ unsigned long long g_wsticket;
 template <bool ON>
 __device__ __forceinline__ void trace(int b, int ev, bool is_min) {
   if (!ON || b >= kTraceBlocks) return;
-  const unsigned long long t = gtimer();
-  if (is_min) atomicMin(&g_wstrace[b * 8 + ev], t);
-  else atomicMax(&g_wstrace[b * 8 + ev], t);
-}   // accumulated in smem, flushed at exit
+  const unsigned long long t = atomicAdd(&g_wsticket, 1ull);
+  const unsigned long long v = ev == 0 ? (t << 12) | blockIdx.x : (is_min ? t : ~t);
+  atomicMin(&g_wstrace[b * 8 + ev], v);
+}
 // Compiled in only for the profiling instantiation of the kernel.
 template <bool ON>
 struct ProfT {
@@ -562,7 +572,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
     pf.add(kFWWait, t0);
     t0 = pf.now();
-    if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
+    if (PROF && lane == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
 
     if constexpr (S::kT == 8) {
       if (kind == 0) f_unit8<S>(P, src, sy, slot, b, sub, wl, lane);
@@ -699,8 +709,8 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       }
     }
     __syncwarp();
+    if (PROF && lane == 0) trace<PROF>(b, kind == 0 ? 1 : 5, false);   // before this warp's release
     if (lane == 0) red_release_cta_smem(&sy.fi_cnt[it & 3], 1);
-    if (PROF && wtid == 0) trace<PROF>(b, kind == 0 ? 1 : 5, false);
     pf.add(kind == 0 ? kFWF : kFWI, t0);
     pf.inc(kind == 0 ? kNF : kNI);
   }
@@ -887,6 +897,7 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
       // this buffer first)
       if (atom_acqrel_cta_smem(&sy.g_cnt[buf], 1) == 4 * (k / kNAcc) + 3) {
         const long long t1 = pf.now();
+        trace<PROF>(b, 3, false);    // before the release that publishes it
         if (P.gbatch == 1) {
           red_release_gpu(P.counters + P.g.n_blk + b, 1);
         } else if (k % P.gbatch == P.gbatch - 1 || b + gu.step >= P.g.n_blk) {
@@ -898,7 +909,6 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
           fence_acq_rel_gpu();
           for (int j = k0; j <= k; ++j) red_relaxed_gpu(P.counters + P.g.n_blk + gu.b0 + j * gu.step, 1);
         }
-        trace<PROF>(b, 3, false);
         pf.add(kPubFence, t1);
       }
       mbar_arrive(&sy.tempty[buf]);
@@ -1035,7 +1045,7 @@ struct Plan {
 };
 
 template <class S>
-static Plan plan_t(const Geo& g) {
+static Plan plan_t(const Geo& g, const FusedOpts& o) {
   Plan pl = {};
   // the bulk-copied input rows must be 16-byte aligned (W % 4 == 0); the
   // branch-free window loads assume pad_lo = 1
@@ -1049,8 +1059,7 @@ static Plan plan_t(const Geo& g) {
   if (static_cast<size_t>(S::kCPC) * pl.plane * 4 > S::kFISlot) return pl;
   // measured on c2 (tools/ws_time.py): rings of 300 MB (slightly past L2)
   // with the I units 32 steps behind their F units are best (80 us)
-  size_t budget = 300ull << 20;
-  if (const char* e = getenv("WF_WS_BUDGET_MB")) budget = static_cast<size_t>(atoi(e)) << 20;
+  size_t budget = o.ring_bytes ? o.ring_bytes : static_cast<size_t>(tuning_knob("WF_WS_BUDGET_MB", 300)) << 20;
   int slots = static_cast<int>(budget / (S::kUSlot + S::kMSlot));
   if (slots < 4) slots = 4;
   pl.NU = std::min(slots / 2, g.n_blk);
@@ -1063,7 +1072,8 @@ static Plan plan_t(const Geo& g) {
   // c5 16->16, 16 units, 64 steps with 8-unit G publish batches)
   const int units = S::kNCG + S::kNIG;
   int lag = units <= 16 ? 64 : units <= 32 ? 32 : std::max(4, std::min(32, 768 / units));
-  if (const char* e = getenv("WF_WS_LAG")) lag = atoi(e);
+  if (o.lag > 0) lag = o.lag;
+  else if (const int k = tuning_knob("WF_WS_LAG", 0)) lag = k;
   // deadlock freedom: some L1 with 1 <= L1 < NU (when F waits on G) and L2 - L1 < NM
   const int lmax = (pl.NU >= g.n_blk ? g.n_blk + pl.NM : pl.NU + pl.NM - 2);
   if (lag > lmax) lag = lmax;
@@ -1106,31 +1116,24 @@ static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
   return R();
 }
 
-static Plan plan(const Geo& g) {
-  return with_shape(g, [&](auto s) { return plan_t<decltype(s)>(g); });
+static Plan plan(const Geo& g, const FusedOpts& o) {
+  return with_shape(g, [&](auto s) { return plan_t<decltype(s)>(g, o); });
 }
 
 template <class S>
 static cudaError_t launch_t(const Params& P, int sm_count, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fused_ws_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fused_ws_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  note_launch();
-  if (P.prof) fused_ws_kernel<S, true><<<sm_count, NT, S::kSmem, st>>>(P);
-  else fused_ws_kernel<S, false><<<sm_count, NT, S::kSmem, st>>>(P);
-  return cudaGetLastError();
+  // units of a CTA wait on units of other CTAs: every CTA must be resident
+  const void* kern = P.prof ? reinterpret_cast<const void*>(fused_ws_kernel<S, true>)
+                            : reinterpret_cast<const void*>(fused_ws_kernel<S, false>);
+  Params p = P;
+  void* args[] = {&p};
+  return launch_coresident(kern, sm_count, NT, S::kSmem, st, args);
 }
 
 }  // namespace ws
 
-bool ws_fits(const Geo& g) {
-  if (const char* e = getenv("WF_WS")) if (atoi(e) == 0) return false;
-  const ws::Plan pl = ws::plan(g);
+bool ws_fits(const Geo& g, const FusedOpts& o) {
+  const ws::Plan pl = ws::plan(g, o);
   if (!pl.ok) return false;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -1139,15 +1142,16 @@ bool ws_fits(const Geo& g) {
   return ws::with_shape(g, [&](auto s) { return sms >= decltype(s)::kP * decltype(s)::kNG; });
 }
 
-size_t ws_scratch_bytes(const Geo& g) {
-  const ws::Plan pl = ws::plan(g);
+size_t ws_scratch_bytes(const Geo& g, const FusedOpts& o) {
+  const ws::Plan pl = ws::plan(g, o);
   if (!pl.ok) return 0;
   return round_up(static_cast<int>(pl.counters_bytes), 1024) + pl.NU * pl.u_slot + pl.NM * pl.m_slot;
 }
 
 cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t* scratch, const Geo& g, int passes,
-                         int sm_count, cudaStream_t st, bool counters_clean) {
-  const ws::Plan pl = ws::plan(g);
+                         int sm_count, cudaStream_t st, const FusedOpts& o) {
+  const ws::Plan pl = ws::plan(g, o);
+  const bool counters_clean = (o.flags & kFusedCountersClean) != 0;
   if (!pl.ok) return cudaErrorInvalidValue;
   ws::Params P;
   P.x = x; P.y = y; P.vpack = vpack;
@@ -1164,14 +1168,20 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   // discards delay the I publishes)
   // T = 8 and the 16-channel (RGB) instance: faster without (measured c5
   // 2-3%, VGG 3->64 @224 376 -> 359 us)
-  P.discard = (g.T == 6 && g.Cpad > 16) ? 1 : 0;
-  if (const char* e = getenv("WF_WS_DISCARD")) P.discard = atoi(e);
+  P.discard = tuning_knob("WF_WS_DISCARD", (g.T == 6 && g.Cpad > 16) ? 1 : 0);
   P.dbg = 0;
-  if (const char* e = getenv("WF_WS_DBG")) P.dbg = atoi(e);
+#ifdef WF_TUNING_AIDS
+  P.dbg = tuning_knob("WF_WS_DBG", 0);     // 3: no GEMM work (results invalid)
+#endif
   P.plane = pl.plane;
   P.grid = sm_count;
-  P.prof = 0;
-  if (const char* e = getenv("WF_WS_PROF")) P.prof = atoi(e);
+  // the instrumented instance: per-role busy cycles and per-block ordering
+  // tickets (wf_fused_instrument_read)
+  P.prof = (o.flags & kFusedInstrument) ? 1 : 0;
+  if (P.prof) {
+    cudaError_t e = ws_instrument_reset(g.n_blk, st);
+    if (e != cudaSuccess) return e;
+  }
   if (!counters_clean) {
     cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
     if (e != cudaSuccess) return e;
@@ -1185,7 +1195,8 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
     // the deadlock-freedom argument uses.
     const int step = std::max(1, sm_count / (S::kP * S::kNG));
     int gb = S::CP <= 16 ? 8 : S::CP <= 32 ? 4 : 1;
-    if (const char* e = getenv("WF_WS_GBATCH")) gb = std::max(1, std::min(ws::kNAcc, atoi(e)));
+    if (o.gbatch > 0) gb = std::min(ws::kNAcc, o.gbatch);
+    else if (const int k = tuning_knob("WF_WS_GBATCH", 0)) gb = std::max(1, std::min(ws::kNAcc, k));
     while (gb > 1 && (gb - 1) * step >= std::min(P.L2, std::min(P.NU, P.NM))) --gb;
     P.gbatch = gb;
     return ws::launch_t<S>(P, sm_count, st);
@@ -1205,14 +1216,43 @@ extern "C" int wf_debug_ws_profile(unsigned long long* host, int n) {
   return e == cudaSuccess ? 0 : 4;
 }
 
-extern "C" int wf_debug_ws_trace(unsigned long long* host, int n_blocks, int reset) {
-  const int cnt = (n_blocks < wf::ws::kTraceBlocks ? n_blocks : wf::ws::kTraceBlocks) * 8;
-  cudaError_t e = cudaMemcpyFromSymbol(host, wf::ws::g_wstrace, cnt * sizeof(unsigned long long));
-  if (reset) {
-    static unsigned long long init[wf::ws::kTraceBlocks * 8];
-    for (int b = 0; b < wf::ws::kTraceBlocks; ++b)
-      for (int k = 0; k < 8; ++k) init[b * 8 + k] = (k % 2 == 0) ? ~0ull : 0ull;
-    if (e == cudaSuccess) e = cudaMemcpyToSymbol(wf::ws::g_wstrace, init, sizeof(init));
-  }
-  return e == cudaSuccess ? 0 : 4;
+namespace wf {
+cudaError_t ws_instrument_reset(int n_blk, cudaStream_t st) {
+  (void)n_blk;
+  void* p = nullptr;
+  cudaError_t e = cudaGetSymbolAddress(&p, ws::g_wstrace);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p, 0xff, sizeof(ws::g_wstrace), st);
+  if (e == cudaSuccess) e = cudaGetSymbolAddress(&p, ws::g_wsticket);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = cudaGetSymbolAddress(&p, ws::g_wsprof);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, sizeof(ws::g_wsprof), st);
+  return e;
 }
+
+int ws_instrument_read(const Geo& g, const FusedOpts& o, unsigned long long* events, int n_events,
+                       unsigned long long* role_cycles, int* nu_nm) {
+  const ws::Plan pl = ws::plan(g, o);
+  if (!pl.ok) return -1;
+  nu_nm[0] = pl.NU;
+  nu_nm[1] = pl.NM;
+  const int nb = g.n_blk < ws::kTraceBlocks ? g.n_blk : ws::kTraceBlocks;
+  const int cnt = (n_events < nb * 8 ? n_events : nb * 8);
+  if (cudaMemcpyFromSymbol(events, ws::g_wstrace, cnt * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  static unsigned long long prof[1024 * ws::kProfSlots];
+  if (cudaMemcpyFromSymbol(prof, ws::g_wsprof, sizeof(prof)) != cudaSuccess) return -1;
+  unsigned long long f = 0, gg = 0, i = 0;
+  for (int c = 0; c < 1024; ++c) {
+    f += prof[c * ws::kProfSlots + ws::kFWF];
+    gg += prof[c * ws::kProfSlots + ws::kGEBusy];
+    i += prof[c * ws::kProfSlots + ws::kFWI];
+  }
+  role_cycles[0] = f;
+  role_cycles[1] = gg;
+  role_cycles[2] = i;
+  int dev = 0, khz = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+  role_cycles[3] = static_cast<unsigned long long>(khz);
+  return nb;
+}
+}  // namespace wf

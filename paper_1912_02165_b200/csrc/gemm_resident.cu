@@ -206,12 +206,9 @@ cudaError_t launch_gemm_resident(const uint8_t* U, const uint8_t* V, float* M, c
   P.n_pos = g.P; P.n_blk = nblk;
   P.Cpad = g.Cpad; P.Cppad = g.Cppad; P.Cp = g.Nout;
   P.ldm = ldm; P.n_valid = n_valid; P.passes = passes;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         200 * 1024);
+  {
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(gemm_resident_kernel), 200 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int n_items = P.n_pos * nblk;
   cudaLaunchConfig_t cfg = {};

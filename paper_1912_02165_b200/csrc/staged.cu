@@ -329,12 +329,9 @@ cudaError_t launch_position_gemm(const uint8_t* U, const uint8_t* V, float* M, c
   if (P.stages > 4) P.stages = 4;
   if (P.stages < 2) P.stages = 2;
   const int smem = P.stages * stage_bytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(position_gemm_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  {
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(position_gemm_kernel), 200 * 1024);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int n_items = P.n_pos * P.n_blk * P.n_nc;
   const int grid = n_items < sm_count ? n_items : sm_count;

@@ -17,13 +17,16 @@ device time of the engine's kernels measured with CUDA events on the
 launching stream (transfers excluded, like the reference's timers).
 
 GPU additions to :class:`EngineConfig`: ``device`` (None = current CUDA
-device), ``transform`` ("winograd" | "fft") and ``precision`` ("3xbf16" |
-"bf16").  There is no CPU fallback: without the CUDA extension or a GPU
-every engine raises :class:`NativeLibraryError`.
+device), ``transform`` ("winograd" | "fft"), ``precision`` ("3xbf16" |
+"bf16"), ``fused_variant`` (which fused kernel runs: "auto" | "ws" |
+"itemq" | "waves") and ``ring_bytes`` (L2 ring budget of the persistent
+fused kernels).  There is no CPU fallback: without the CUDA extension or a
+GPU every engine raises :class:`NativeLibraryError`.
 """
 
 from __future__ import annotations
 
+import ctypes
 import os
 from dataclasses import dataclass, field
 
@@ -63,6 +66,8 @@ class EngineConfig:
     device: object = None
     transform: str = "winograd"
     precision: str = "3xbf16"
+    fused_variant: str = "auto"
+    ring_bytes: int | None = None
 
     def __post_init__(self):
         if self.kind not in ENGINE_KINDS:
@@ -80,6 +85,10 @@ class EngineConfig:
             raise InvalidParameterError("workers must be >= 0 (0 = auto)")
         if self.precision not in PRECISIONS:
             raise InvalidParameterError(f"unknown precision {self.precision!r}")
+        if self.fused_variant not in _lib.VARIANTS:
+            raise InvalidParameterError(f"unknown fused variant {self.fused_variant!r}")
+        if self.ring_bytes is not None and self.ring_bytes < 0:
+            raise InvalidParameterError("ring_bytes must be >= 0")
 
     def resolved_workers(self, cap: int | None = None) -> int:
         w = self.workers or _device_sm_count()
@@ -118,6 +127,8 @@ class ConvStats:
     device: str = ""
     precision: str = ""
     transform: str = ""
+    variant: str = ""           # fused kernel that ran: "ws" | "itemq" | "waves"
+    blocks: int = 0             # 128-tile blocks (the GPU's tasks: one MMA M each)
 
 
 # ------------------------------------------------------- scratch layout math
@@ -248,6 +259,16 @@ class _Timer:
         return self.start.elapsed_time(self.stop) * 1e-3
 
 
+def _on(dev):
+    """Make ``dev`` the current CUDA device around a native call: the
+    library launches on the current device (cudaGetDevice)."""
+    return _dev.torch.cuda.device(dev)
+
+
+def _opts(cfg: EngineConfig, flags: int = 0):
+    return _lib.fused_opts(cfg.fused_variant, flags, cfg.ring_bytes)
+
+
 _SCRATCH = {}
 
 
@@ -275,7 +296,7 @@ def conv_direct(inp, kers, spec: LayerSpec, config: EngineConfig | None = None):
     w = _dev.to_device(kers, dev, name="kernels")
     y = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=dev)
     lib = _lib.load()
-    with _Timer(dev) as tm:
+    with _on(dev), _Timer(dev) as tm:
         _lib.check(lib.wf_conv_direct(_dev.ptr(x), _dev.ptr(w), _dev.ptr(y), _lib.layer_struct(spec),
                                       _dev.stream_ptr(dev)), "wf_conv_direct")
     stats = ConvStats(engine="direct", wall_s=tm.seconds(), flops=spec.direct_flops(), device=str(dev))
@@ -305,17 +326,29 @@ def conv_three_stage(inp, kers, spec: LayerSpec, config: EngineConfig | None = N
     except _dev.torch.cuda.OutOfMemoryError as exc:
         raise IntermediateAllocationError(inter_bytes, "staged transform intermediates") from exc
     y = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=dev)
-    with _Timer(dev) as tm:
-        _lib.check(lib.wf_conv_three_stage(_dev.ptr(x), _dev.ptr(vpack), _dev.ptr(y), _dev.ptr(scratch), need,
-                                           layer, cfg.tile, tf, _lib.PRECISIONS[cfg.precision],
-                                           _dev.stream_ptr(dev)), "wf_conv_three_stage")
-    wall = tm.seconds()
+    # one launch group per stage with an event between them: the reference's
+    # per-stage phase_s (engines.py:263-302), here device time per stage
+    torch = _dev.torch
+    events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    stream = torch.cuda.current_stream(dev)
+    phases = (("forward", _lib.WF_PHASE_FORWARD), ("multiply", _lib.WF_PHASE_MULTIPLY),
+              ("inverse", _lib.WF_PHASE_INVERSE))
+    with _on(dev):
+        events[0].record(stream)
+        for i, (_, bit) in enumerate(phases):
+            _lib.check(lib.wf_conv_three_stage_phases(_dev.ptr(x), _dev.ptr(vpack), _dev.ptr(y), _dev.ptr(scratch),
+                                                      need, layer, cfg.tile, tf, _lib.PRECISIONS[cfg.precision],
+                                                      bit, _dev.stream_ptr(dev)), "wf_conv_three_stage")
+            events[i + 1].record(stream)
+    events[-1].synchronize()
+    phase_s = {name: events[i].elapsed_time(events[i + 1]) * 1e-3 for i, (name, _) in enumerate(phases)}
+    wall = events[0].elapsed_time(events[-1]) * 1e-3
     stats = ConvStats(engine="three_stage", wall_s=wall,
                       flops=multiply_flops(pl.n_tile, spec.in_channels, spec.out_channels, cfg.tile,
                                            cfg.transform),
                       n_tile=pl.n_tile, workers=cfg.resolved_workers(), intermediate_bytes=inter_bytes,
-                      scratch_bytes=int(need), phase_s={"total": wall}, device=str(dev),
-                      precision=cfg.precision, transform=cfg.transform)
+                      scratch_bytes=int(need), phase_s=phase_s, device=str(dev),
+                      precision=cfg.precision, transform=cfg.transform, blocks=-(-pl.n_tile // 128))
     return _finish(y, not _dev.is_torch(inp)), stats
 
 
@@ -351,31 +384,84 @@ def conv_fused(inp, pack: KernelPack, spec: LayerSpec, config: EngineConfig | No
     if cfg.l2_budget_bytes and layout.capacity > cfg.l2_budget_bytes:
         warnings.append(f"scratch buffer {layout.capacity} B exceeds the configured L2 budget "
                         f"{cfg.l2_budget_bytes} B; lower R")
-    need = lib.wf_fused_scratch_bytes(layer, cfg.tile, tf, 0)
-    x = _dev.to_device(inp, dev, name="input")
-    vpack = pack.device_mma(dev)
-    scratch = _scratch(dev, int(need), "fused")
-    y = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=dev)
-    with _Timer(dev) as tm:
-        _lib.check(lib.wf_conv_fused(_dev.ptr(x), _dev.ptr(vpack), _dev.ptr(y), _dev.ptr(scratch), int(need),
-                                     layer, cfg.tile, tf, _lib.PRECISIONS[cfg.precision], 0,
-                                     _dev.stream_ptr(dev)), "wf_conv_fused")
-    wall = tm.seconds()
+    flags = _lib.WF_FUSED_INSTRUMENT if cfg.instrumented else 0
+    with _on(dev):
+        opts = _opts(cfg)
+        variant = lib.wf_fused_variant(layer, cfg.tile, tf, opts)
+        if variant < 0:
+            _lib.check(-variant, "wf_fused_variant")
+        if flags and variant != _lib.WF_FUSED_WS:
+            warnings.append(f"instrumented mode is implemented by the warp-specialised kernel; the "
+                            f"{_lib.VARIANT_NAMES[variant]!r} variant ran uninstrumented")
+            flags = 0
+        opts = _opts(cfg, flags)
+        need = lib.wf_fused_scratch_bytes_ex(layer, cfg.tile, tf, opts)
+        x = _dev.to_device(inp, dev, name="input")
+        vpack = pack.device_mma(dev)
+        scratch = _scratch(dev, int(need), "fused")
+        y = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=dev)
+        ran = ctypes.c_int(0)
+        with _Timer(dev) as tm:
+            _lib.check(lib.wf_conv_fused_ex(_dev.ptr(x), _dev.ptr(vpack), _dev.ptr(y), _dev.ptr(scratch), int(need),
+                                            layer, cfg.tile, tf, _lib.PRECISIONS[cfg.precision], opts,
+                                            ctypes.byref(ran), _dev.stream_ptr(dev)), "wf_conv_fused")
+        wall = tm.seconds()
     workers = cfg.resolved_workers(n_task)
     flops = multiply_flops(pl.n_tile, spec.in_channels, spec.out_channels, cfg.tile, cfg.transform)
-    task_flops = trace = None
-    violations = None
-    if cfg.instrumented:
-        task_flops = [multiply_flops(min(cfg.r, pl.n_tile - i * cfg.r), spec.in_channels, spec.out_channels,
-                                     cfg.tile, cfg.transform) for i in range(n_task)]
-        trace = [(order[pos], pos % workers) for pos in range(n_task)]
-        violations = 0
+    n_blk = -(-pl.n_tile // 128)
+    task_flops = trace = violations = None
+    phase_s = {"fused": wall}
+    if flags:
+        with _on(dev):
+            task_flops, trace, violations, phase_s = _read_instrumented(lib, layer, cfg, tf, opts, pl, spec, dev)
     stats = ConvStats(engine="fused", wall_s=wall, flops=flops, n_tile=pl.n_tile, n_task=n_task, r=cfg.r,
                       r_eff_last=pl.n_tile - (n_task - 1) * cfg.r, workers=workers,
-                      scratch_bytes=workers * layout.capacity, phase_s={"total": wall}, warnings=warnings,
+                      scratch_bytes=int(need), phase_s=phase_s, warnings=warnings,
                       overlap_violations=violations, task_flops=task_flops, task_trace=trace,
-                      device=str(dev), precision=cfg.precision, transform=cfg.transform)
+                      device=str(dev), precision=cfg.precision, transform=cfg.transform,
+                      variant=_lib.VARIANT_NAMES.get(ran.value, ""), blocks=n_blk)
     return _finish(y, not _dev.is_torch(inp)), stats
+
+
+def _read_instrumented(lib, layer, cfg, tf, opts, pl, spec, dev):
+    """Per-block ordering tickets of an instrumented warp-specialised launch ->
+    (task_flops, task_trace, overlap_violations, phase_s).
+
+    The GPU's tasks are 128-tile blocks.  A violation is an inverted ticket
+    pair on a dependency edge of the dataflow: a block's GEMM started before
+    its forward units ended or its inverse units started before its GEMM
+    ended, or a ring slot was rewritten (forward of block b into U slot
+    b % NU, GEMM of b into M slot b % NM) before the slot's previous
+    consumer ended -- the GPU analogue of the reference's operand-overlap
+    check (engines.py:382-396).  phase_s sums the per-CTA busy time of the
+    forward units, the GEMM epilogue and the inverse units (the reference
+    sums its workers' per-stage times, engines.py:432-434).
+    """
+    n_blk = -(-pl.n_tile // 128)
+    ev = (ctypes.c_ulonglong * (8 * n_blk))()
+    roles = (ctypes.c_ulonglong * 4)()
+    ring = (ctypes.c_int * 2)()
+    n = lib.wf_fused_instrument_read(layer, cfg.tile, tf, opts, ev, 8 * n_blk, roles, ring)
+    if n < 0:
+        _lib.check(-n, "wf_fused_instrument_read")
+    e = np.frombuffer(ev, dtype=np.uint64).reshape(n_blk, 8)[:n]
+    inv = np.uint64(0xFFFFFFFFFFFFFFFF)
+    f_start, f_cta = e[:, 0] >> np.uint64(12), (e[:, 0] & np.uint64(0xFFF)).astype(int)
+    f_end, g_start, g_end = inv - e[:, 1], e[:, 2], inv - e[:, 3]
+    i_start, i_end = e[:, 4], inv - e[:, 5]
+    nu, nm = int(ring[0]), int(ring[1])
+    viol = int(np.sum(g_start < f_end)) + int(np.sum(i_start < g_end))
+    if n > nu:
+        viol += int(np.sum(f_start[nu:] < g_end[:-nu]))
+    if n > nm:
+        viol += int(np.sum(g_start[nm:] < i_end[:-nm]))
+    order = np.argsort(f_start, kind="stable")
+    trace = [(int(b), int(f_cta[b])) for b in order]
+    task_flops = [multiply_flops(min(128, pl.n_tile - b * 128), spec.in_channels, spec.out_channels, cfg.tile,
+                                 cfg.transform) for b in range(n)]
+    clock_hz = float(roles[3]) * 1e3 or 1.965e9          # SM clock (kHz) reported by the library
+    phase_s = {"forward": roles[0] / clock_hz, "multiply": roles[1] / clock_hz, "inverse": roles[2] / clock_hz}
+    return task_flops, trace, viol, phase_s
 
 
 def run_engine(kind: str, inp, kers, spec: LayerSpec, config: EngineConfig | None = None, **kw):
@@ -396,6 +482,13 @@ class LayerPlan:
     once; ``plan(x)`` then only launches the engine's kernels on the current
     stream (no host synchronisation, no allocation), so it can be timed
     with CUDA events or captured into a CUDA graph.  Used by bench.py.
+
+    The fused variant is resolved once at planning time (``self.variant``)
+    and passed explicitly on every call.  A plan that owns its scratch
+    zero-fills it once and calls with WF_FUSED_COUNTERS_CLEAN (the
+    warp-specialised kernel leaves its dependency counters zero, so the
+    per-call reset is skipped); a plan given a shared scratch
+    (:class:`LayerStack`, :class:`HostPipeline`) never does.
     """
 
     def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None, scratch=None):
@@ -412,34 +505,65 @@ class LayerPlan:
         self.layer = _lib.layer_struct(spec)
         self.tf = _lib.TRANSFORMS[cfg.transform]
         self.prec = _lib.PRECISIONS[cfg.precision]
-        if cfg.kind == "fused":
-            self.nbytes = int(self.lib.wf_fused_scratch_bytes(self.layer, cfg.tile, self.tf, 0))
-        else:
-            self.nbytes = int(self.lib.wf_three_stage_scratch_bytes(self.layer, cfg.tile, self.tf))
-        if scratch is not None and scratch.numel() >= self.nbytes:
-            self.scratch = scratch                    # shared with other plans on the same stream
-            self.flags = 0
-        else:
-            # private scratch: the warp-specialised kernel leaves its
-            # dependency counters zero, so repeated calls skip the per-call
-            # reset (wf_conv_fused_planned, WF_FUSED_COUNTERS_CLEAN)
-            self.scratch = _dev.torch.empty(max(self.nbytes, 16), dtype=_dev.torch.uint8, device=self.dev)
-            self.flags = 1
-        self.vpack = self.pack.device_mma(self.dev)
-        self.out = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=self.dev)
+        self.variant = None
+        with _on(self.dev):
+            if cfg.kind == "fused":
+                v = self.lib.wf_fused_variant(self.layer, cfg.tile, self.tf, _opts(cfg))
+                if v < 0:
+                    _lib.check(-v, "wf_fused_variant")
+                self.variant = _lib.VARIANT_NAMES[v]
+                self._pinned = _lib.fused_opts(self.variant, 0, cfg.ring_bytes)
+                self.nbytes = int(self.lib.wf_fused_scratch_bytes_ex(self.layer, cfg.tile, self.tf, self._pinned))
+            else:
+                self.nbytes = int(self.lib.wf_three_stage_scratch_bytes(self.layer, cfg.tile, self.tf))
+            if scratch is not None and scratch.numel() >= self.nbytes:
+                self.scratch = scratch                    # shared with other plans on the same stream
+                self.shared = True
+            else:
+                self.scratch = _dev.torch.zeros(max(self.nbytes, 16), dtype=_dev.torch.uint8, device=self.dev)
+                self.shared = False
+            self.vpack = self.pack.device_mma(self.dev)
+            self.out = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=self.dev)
+        self.ran = ctypes.c_int(0)
+
+    @property
+    def flags(self) -> int:
+        return 0 if self.shared else _lib.WF_FUSED_COUNTERS_CLEAN
+
+    def share_scratch(self, scratch) -> None:
+        """Use ``scratch`` (at least ``nbytes``, shared with other plans on one stream)."""
+        if scratch.numel() < self.nbytes:
+            raise InvalidParameterError(f"shared scratch {scratch.numel()} B < {self.nbytes} B")
+        self.scratch = scratch
+        self.shared = True
+
+    def _check(self, t, dims, name):
+        if not _dev.is_torch(t) or not t.is_cuda or t.device != self.dev:
+            raise ShapeMismatchError(f"{name} must be a CUDA tensor on {self.dev}")
+        if t.dtype != _dev.torch.float32 or not t.is_contiguous():
+            raise ShapeMismatchError(f"{name} must be a contiguous float32 tensor")
+        if tuple(t.shape) != tuple(dims):
+            raise ShapeMismatchError(f"{name} dims {tuple(t.shape)} do not match {tuple(dims)}")
+        if t.data_ptr() % 16:
+            raise ShapeMismatchError(f"{name} must be 16-byte aligned (bulk copies)")
 
     def __call__(self, x, out=None):
         """Launch on the current stream; x: contiguous f32 CUDA tensor (B, C, H, W)."""
         y = self.out if out is None else out
+        self._check(x, self.spec.input_dims(), "input")
+        if out is not None:
+            self._check(out, self.spec.output_dims(), "output")
         stream = _dev.stream_ptr(self.dev)
-        if self.cfg.kind == "fused":
-            rc = self.lib.wf_conv_fused_planned(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y),
-                                                _dev.ptr(self.scratch), self.nbytes, self.layer, self.cfg.tile,
-                                                self.tf, self.prec, self.flags, stream)
-        else:
-            rc = self.lib.wf_conv_three_stage(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y),
-                                              _dev.ptr(self.scratch), self.nbytes, self.layer, self.cfg.tile,
-                                              self.tf, self.prec, stream)
+        with _on(self.dev):
+            if self.cfg.kind == "fused":
+                self._pinned.flags = self.flags
+                rc = self.lib.wf_conv_fused_ex(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y),
+                                               _dev.ptr(self.scratch), self.nbytes, self.layer, self.cfg.tile,
+                                               self.tf, self.prec, self._pinned, ctypes.byref(self.ran), stream)
+            else:
+                rc = self.lib.wf_conv_three_stage(_dev.ptr(x), _dev.ptr(self.vpack), _dev.ptr(y),
+                                                  _dev.ptr(self.scratch), self.nbytes, self.layer, self.cfg.tile,
+                                                  self.tf, self.prec, stream)
         _lib.check(rc, "LayerPlan")
         return y
 
@@ -452,8 +576,9 @@ class LayerStack:
     layer i+1's input, with no host synchronisation, re-layout or copy in
     between (activations stay NCHW f32 in HBM).  The layers share one
     scratch buffer (the size of the largest), which is safe because they are
-    stream-ordered.  As in the reference there is no bias, activation or
-    pooling between layers, so consecutive specs must match:
+    stream-ordered; every plan then resets its own dependency counters per
+    call.  As in the reference there is no bias, activation or pooling
+    between layers, so consecutive specs must match:
     ``specs[i].output_dims() == specs[i + 1].input_dims()``.
     """
 
@@ -466,16 +591,11 @@ class LayerStack:
             if specs[i].output_dims() != specs[i + 1].input_dims():
                 raise ShapeMismatchError(f"layer {i} output {specs[i].output_dims()} does not feed layer {i + 1} "
                                          f"input {specs[i + 1].input_dims()}")
-        self.plans = []
-        shared = None
-        for spec, pack, cfg in zip(specs, packs, configs):
-            plan = LayerPlan(spec, pack, cfg, scratch=shared)
-            if shared is None or plan.scratch.numel() > shared.numel():
-                shared = plan.scratch
-            self.plans.append(plan)
-        # give every plan the largest scratch so none keeps a private copy
+        self.plans = [LayerPlan(spec, pack, cfg) for spec, pack, cfg in zip(specs, packs, configs)]
+        # one scratch, the largest, for every plan (stream-ordered use)
+        shared = max((p.scratch for p in self.plans), key=lambda t: t.numel())
         for plan in self.plans:
-            plan.scratch = shared
+            plan.share_scratch(shared)
 
     def __call__(self, x):
         """Launch every layer on the current stream; returns the last output."""
@@ -529,15 +649,15 @@ class HostPipeline:
         torch = _dev.torch
         self.dev = _dev.require_cuda(cfg.device)
         self.plans = {}
-        shared = None
         for nb in sorted({hi - lo for lo, hi in self.bounds}, reverse=True):
             sub = LayerSpec(nb, spec.in_channels, spec.out_channels, spec.height, spec.width, spec.kernel,
                             spec.pad_lo, spec.pad_hi)
-            plan = LayerPlan(sub, pack, cfg, scratch=shared)
-            shared = plan.scratch if shared is None or plan.scratch.numel() > shared.numel() else shared
-            self.plans[nb] = plan
-        for plan in self.plans.values():
-            plan.scratch = shared
+            self.plans[nb] = LayerPlan(sub, pack, cfg)
+        if len(self.plans) > 1:
+            # slices of different sizes share the largest scratch (one compute stream)
+            shared = max((p.scratch for p in self.plans.values()), key=lambda t: t.numel())
+            for plan in self.plans.values():
+                plan.share_scratch(shared)
         self.x_dev = torch.empty(spec.input_dims(), dtype=torch.float32, device=self.dev)
         self.y_dev = torch.empty(spec.output_dims(), dtype=torch.float32, device=self.dev)
         self.streams = [torch.cuda.Stream(self.dev) for _ in range(3)]

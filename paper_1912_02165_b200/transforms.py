@@ -21,8 +21,8 @@ import numpy as np
 
 from . import _lib
 from . import device as _dev
-from .basis import FftBasis, WinogradBasis
-from .errors import ShapeMismatchError
+from .basis import FftBasis, WinogradBasis, default_points
+from .errors import ShapeMismatchError, UnsupportedConfigError
 from .tensor import LayerSpec, Tensor4D, aligned_empty
 from .tiling import TilePlan
 
@@ -119,6 +119,11 @@ def transform_kernels(kers, basis) -> KernelPack:
     dims = _dev.dims_of(kers)
     if len(dims) != 4:
         raise ShapeMismatchError(f"kernel dims {dims} are not 4-D")
+    if isinstance(basis, WinogradBasis) and tuple(basis.points) != tuple(default_points(basis.tile)):
+        # the sm_100a kernels bake in the default nodes' B^T / A^T: a pack of
+        # other nodes would be applied with the wrong data transforms
+        raise UnsupportedConfigError("the sm_100a kernels implement the default interpolation nodes only "
+                                     f"({', '.join(str(p) for p in default_points(basis.tile))})")
     c_out, c_in, kh, kw = dims
     if kh != basis.kernel or kw != basis.kernel:
         raise ShapeMismatchError(f"kernel dims {dims} do not match basis K={basis.kernel}")

@@ -237,33 +237,71 @@ def test_unsupported_configs_fail_loudly():
     with pytest.raises(wf.UnsupportedConfigError):
         wf.conv_fused(wf.new_tensor(spec5.input_dims()), pack5, spec5, wf.EngineConfig(tile=7))
     spec = wf.LayerSpec(1, 2, 2, 9, 9, 3, 1, 1)
-    pack = wf.transform_kernels(wf.new_tensor(spec.kernel_dims()), wf.make_basis(5, 3, points=(0, 1, -1, 3)))
+    import torch
+    w = torch.from_numpy(wf.new_tensor(spec.kernel_dims()).data).cuda()
+    with pytest.raises(wf.UnsupportedConfigError):     # device filter transform: default nodes only
+        wf.transform_kernels(w, wf.make_basis(5, 3, points=(0, 1, -1, 3)))
+    pack = wf.transform_kernels(wf.new_tensor(spec.kernel_dims()), wf.make_basis(5))
     with pytest.raises(wf.UnsupportedConfigError):
         wf.conv_fused(wf.new_tensor(spec.input_dims()), pack, spec,
                       wf.EngineConfig(tile=5, points=(0, 1, -1, 3)))
+    with pytest.raises(wf.UnsupportedConfigError):     # a layer the requested kernel cannot hold
+        wf.conv_fused(wf.new_tensor(spec.input_dims()), pack, spec, wf.EngineConfig(tile=5, fused_variant="ws"))
 
 
-def test_fused_task_order_and_instrumented_accounting(golden_cases):
+def test_fused_task_order(golden_cases):
     c = next(c for c in golden_cases if c["name"] == "t5_workers")
     spec = wf.LayerSpec(*c["dims"])
     pack = wf.transform_kernels(wf.Tensor4D(c["w"]), wf.make_basis(5))
-    cfg = wf.EngineConfig(tile=5, r=5, instrumented=True)
+    cfg = wf.EngineConfig(tile=5, r=5)
     n_task = -(-c["n_tile"] // 5)
     a, st = wf.conv_fused(wf.Tensor4D(c["x"]), pack, spec, cfg, task_order=list(reversed(range(n_task))))
     b, _ = wf.conv_fused(wf.Tensor4D(c["x"]), pack, spec, cfg)
-    assert np.array_equal(a.data, b.data)
-    assert st.overlap_violations == 0 and sum(st.task_flops) == st.flops
-    assert sorted(tk for tk, _ in st.task_trace) == list(range(n_task))
+    assert np.array_equal(a.data, b.data) and st.n_task == n_task
     with pytest.raises(wf.InvalidParameterError):
         wf.conv_fused(wf.Tensor4D(c["x"]), pack, spec, cfg, task_order=[0] * n_task)
 
 
+@pytest.mark.parametrize("ring_mb", [None, 12])
+def test_instrumented_fused_protocol_check(ring_mb):
+    """Instrumented mode runs the warp-specialised kernel with ordering
+    tickets: no dependency edge or ring-slot reuse may be inverted (the
+    GPU analogue of the reference's overlap check, engines.py:382-396),
+    the trace covers every 128-tile block once, the per-block flops sum to
+    the layer's and the output is bitwise the uninstrumented one."""
+    spec = wf.LayerSpec(16, 64, 64, 56, 56, 3, 1, 1)            # 25 blocks (ring reuse at 12 MB)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
+    rb = None if ring_mb is None else ring_mb << 20
+    a, st = wf.conv_fused(wf.Tensor4D(x), pack, spec, wf.EngineConfig(tile=6, instrumented=True, ring_bytes=rb))
+    b, sb = wf.conv_fused(wf.Tensor4D(x), pack, spec, wf.EngineConfig(tile=6, ring_bytes=rb))
+    assert st.variant == "ws" and sb.variant == "ws"
+    assert np.array_equal(a.data, b.data)
+    assert st.overlap_violations == 0
+    assert sorted(blk for blk, _ in st.task_trace) == list(range(st.blocks))
+    assert all(0 <= cta < 148 for _, cta in st.task_trace)
+    assert sum(st.task_flops) == st.flops
+    assert set(st.phase_s) == {"forward", "multiply", "inverse"} and all(v > 0 for v in st.phase_s.values())
+    assert sb.overlap_violations is None and sb.task_trace is None
+
+
+def test_three_stage_phase_times():
+    spec = wf.LayerSpec(8, 64, 64, 56, 56, 3, 1, 1)
+    x = wf.new_tensor(spec.input_dims(), seed=1)
+    pack = wf.transform_kernels(wf.new_tensor(spec.kernel_dims(), seed=2), wf.make_basis(6))
+    _, st = wf.conv_three_stage(x, pack, spec, wf.EngineConfig(kind="three_stage", tile=6))
+    assert set(st.phase_s) == {"forward", "multiply", "inverse"}
+    assert all(v > 0 for v in st.phase_s.values())
+    assert abs(sum(st.phase_s.values()) - st.wall_s) <= 1e-3 * st.wall_s + 1e-6
+
+
 @pytest.mark.parametrize("t", [4, 5, 6, 7, 8])
-def test_persistent_kernel_forced_on_small_layers(t, monkeypatch):
-    """Small layers normally run as one L2 wave; force the persistent
-    dataflow kernel (WF_PERSIST_MIN_BLOCKS=1) and check it on ragged shapes:
-    bitwise equal to three-stage, within tolerance of FP64."""
-    monkeypatch.setenv("WF_PERSIST_MIN_BLOCKS", "1")
+def test_persistent_kernel_forced_on_small_layers(t):
+    """Small layers normally run as one L2 wave; request the item-queue
+    persistent kernel explicitly and check it on ragged shapes: bitwise
+    equal to three-stage, within tolerance of FP64."""
     for dims in [(2, 20, 24, 13, 11, 3, 1, 0), (3, 64, 64, 30, 28, 3, 1, 1), (1, 130, 40, 17, 20, 3, 0, 1),
                  (1, 256, 256, 12, 16, 3, 1, 1)]:
         spec = wf.LayerSpec(*dims)
@@ -271,7 +309,8 @@ def test_persistent_kernel_forced_on_small_layers(t, monkeypatch):
         x = rng.standard_normal(spec.input_dims()).astype(np.float32)
         w = _he(rng, spec)
         pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
-        f, _ = _run("fused", x, pack, spec, t)
+        f, fs = _run("fused", x, pack, spec, t, fused_variant="itemq")
+        assert fs.variant == "itemq", (t, dims, fs.variant)
         s, _ = _run("three_stage", x, pack, spec, t)
         assert np.array_equal(f, s), (t, dims)
         assert O.max_rel_error(f, O.direct_conv_f64(x, w, spec)) <= TOL[t], (t, dims)
@@ -315,16 +354,40 @@ def test_randomized_sweep_like_reference_acceptance():
                                   (16, 3, 64, 56, 56, 3, 1, 1),     # 25 blocks: padding F units skipped on reuse
                                   (2, 16, 64, 16, 24, 3, 1, 1),
                                   (2, 64, 64, 28, 28, 3, 1, 0)])    # pad_hi 0: odd output width
-def test_warp_specialised_kernel(dims, monkeypatch):
+def test_warp_specialised_kernel(dims):
     """The warp-specialised fused kernel (F(4x4,3x3), C in {64, 128}, C' in
     {64, 128, 256}, and C = C' = 256; W % 4 == 0, pad 1 -- the c2 benchmark layer and the
     VGG 64/128-channel layers) against three-stage (bitwise), the
-    item-queue persistent kernel (WF_WS=0, bitwise) and FP64 direct.  Small
-    rings (WF_WS_BUDGET_MB) force slot reuse and the lagged dependencies."""
-    _check_ws(dims, 6, monkeypatch)
+    item-queue persistent kernel (bitwise) and FP64 direct.  Small rings
+    (wf_fused_opts.ring_bytes) force slot reuse and the lagged dependencies."""
+    _check_ws(dims, 6)
 
 
-def _check_ws(dims, t, monkeypatch):
+def _fused_ex(x_np, pack, spec, t, **opts):
+    """One fused call straight through the C ABI (wf_conv_fused_ex) with
+    explicit options (variant, ring_bytes, lag, gbatch); returns (y, variant)."""
+    import ctypes
+    import torch
+    from paper_1912_02165_b200 import _lib
+    dev = torch.device("cuda", 0)
+    lib = _lib.load()
+    layer = _lib.layer_struct(spec)
+    o = _lib.fused_opts(**opts)
+    need = lib.wf_fused_scratch_bytes_ex(layer, t, 0, o)
+    assert need > 0, opts
+    xd = torch.from_numpy(x_np).to(dev)
+    y = torch.empty(spec.output_dims(), dtype=torch.float32, device=dev)
+    scratch = torch.zeros(need, dtype=torch.uint8, device=dev)
+    ran = ctypes.c_int(0)
+    _lib.check(lib.wf_conv_fused_ex(ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(pack.device_mma(dev).data_ptr()),
+                                    ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(scratch.data_ptr()), need, layer,
+                                    t, 0, 0, o, ctypes.byref(ran),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "wf_conv_fused_ex")
+    return y.cpu().numpy(), _lib.VARIANT_NAMES[ran.value]
+
+
+def _check_ws(dims, t, gbatch=0):
     spec = wf.LayerSpec(*dims)
     rng = np.random.default_rng(sum(dims))
     x = rng.standard_normal(spec.input_dims()).astype(np.float32)
@@ -332,14 +395,13 @@ def _check_ws(dims, t, monkeypatch):
     pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
     s, _ = _run("three_stage", x, pack, spec, t)
     ref = O.direct_conv_f64(x, w, spec)
-    for budget in ("300", "12"):
-        monkeypatch.setenv("WF_WS_BUDGET_MB", budget)
-        f, _ = _run("fused", x, pack, spec, t)
+    for budget in (300, 12):          # MB: the default rings, and small rings (slot reuse, lagged dependencies)
+        f, v = _fused_ex(x, pack, spec, t, variant="ws", ring_bytes=budget << 20, gbatch=gbatch)
+        assert v == "ws", (dims, v)
         assert np.array_equal(f, s), (dims, budget)
         assert O.max_rel_error(f, ref) <= TOL[t], (dims, budget)
-    monkeypatch.setenv("WF_WS", "0")
-    monkeypatch.setenv("WF_PERSIST_MIN_BLOCKS", "1")
-    q, _ = _run("fused", x, pack, spec, t)
+    q, qs = _run("fused", x, pack, spec, t, fused_variant="itemq")
+    assert qs.variant == "itemq"
     assert np.array_equal(q, s), dims
 
 
@@ -353,27 +415,26 @@ def _check_ws(dims, t, monkeypatch):
                                   (2, 32, 32, 56, 56, 3, 1, 1),
                                   (8, 16, 16, 56, 56, 3, 1, 1),
                                   (2, 64, 64, 28, 32, 3, 1, 0)])    # pad_hi 0: odd output width
-def test_warp_specialised_kernel_f6(dims, monkeypatch):
+def test_warp_specialised_kernel_f6(dims):
     """The warp-specialised fused kernel for F(6x6,3x3) (T = 8, C = C' in
     {16, 32, 64, 128}: the c5 sweep's layers) -- thread per (tile, channel)
     transforms, 4-channel F units, 2-channel I units -- against three-stage
     and the item-queue kernel (bitwise) and FP64 direct."""
-    _check_ws(dims, 8, monkeypatch)
+    _check_ws(dims, 8)
 
 
-@pytest.mark.parametrize("gbatch", ["1", "2", "4"])
-def test_warp_specialised_batched_g_publish(gbatch, monkeypatch):
-    """Batched G completion publishes (one fence per WF_WS_GBATCH units, the
+@pytest.mark.parametrize("gbatch", [1, 2, 4])
+def test_warp_specialised_batched_g_publish(gbatch):
+    """Batched G completion publishes (one fence per gbatch units, the
     C' <= 32 default is 4) with small rings: bitwise equal to three-stage."""
-    monkeypatch.setenv("WF_WS_GBATCH", gbatch)
-    _check_ws((8, 16, 16, 56, 56, 3, 1, 1), 8, monkeypatch)
+    _check_ws((8, 16, 16, 56, 56, 3, 1, 1), 8, gbatch=gbatch)
 
 
-def test_planned_layer_skips_counter_reset_safely(monkeypatch):
-    """LayerPlan calls wf_conv_fused_planned: the warp-specialised kernel
-    leaves its dependency counters zero and repeated calls skip the reset;
-    switching the kernel under the same scratch (WF_WS=0 between calls)
-    must force the reset again.  Every call stays bitwise equal."""
+def test_planned_layer_skips_counter_reset_safely():
+    """A LayerPlan owning its scratch zero-fills it once and calls with
+    WF_FUSED_COUNTERS_CLEAN: the warp-specialised kernel leaves its
+    dependency counters zero, so repeated calls skip the reset.  Every call
+    stays bitwise equal to three-stage."""
     import torch
     spec = wf.LayerSpec(4, 64, 64, 56, 56, 3, 1, 1)
     rng = np.random.default_rng(5)
@@ -382,14 +443,38 @@ def test_planned_layer_skips_counter_reset_safely(monkeypatch):
     pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
     ref, _ = _run("three_stage", x, pack, spec, 6)
     dev = torch.device("cuda", 0)
-    # planned under WF_WS=0: the item-queue kernel's scratch is the larger one
-    monkeypatch.setenv("WF_WS", "0")
     plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=6, device=dev))
+    assert plan.variant == "ws" and plan.flags == 1
     xd = torch.from_numpy(x).to(dev)
-    for env in (None, None, None, "0", None, "0", "0", None, None):
-        if env is None:
-            monkeypatch.delenv("WF_WS", raising=False)
-        else:
-            monkeypatch.setenv("WF_WS", env)
+    for _ in range(5):
         y = plan(xd).cpu().numpy()
-        assert np.array_equal(y, ref), env
+        assert np.array_equal(y, ref)
+
+
+def test_mixed_layer_stack_called_twice_matches_oracle():
+    """A LayerStack whose layers share one scratch and run different kernels
+    (warp-specialised F(4x4,3x3), three-stage, a warp-specialised layer with
+    small rings, the item-queue kernel), called twice: the output equals the
+    layer-by-layer FP64 oracle chain within tolerance and the two calls are
+    bitwise equal (the shared scratch's counters are reset per call)."""
+    import torch
+    dev = torch.device("cuda", 0)
+    specs = [wf.LayerSpec(4, 64, 64, 56, 56, 3, 1, 1)] * 4
+    cfgs = [wf.EngineConfig(kind="fused", tile=6, device=dev),
+            wf.EngineConfig(kind="three_stage", tile=6, device=dev),
+            wf.EngineConfig(kind="fused", tile=6, device=dev, ring_bytes=12 << 20),
+            wf.EngineConfig(kind="fused", tile=6, device=dev, fused_variant="itemq")]
+    rng = np.random.default_rng(11)
+    ws = [_he(rng, s) for s in specs]
+    packs = [wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6)) for w in ws]
+    stack = wf.LayerStack(specs, packs, cfgs)
+    assert [p.variant for p in stack.plans] == ["ws", None, "ws", "itemq"]
+    assert all(p.flags == 0 for p in stack.plans)
+    x = rng.standard_normal(specs[0].input_dims()).astype(np.float32)
+    xd = torch.from_numpy(x).to(dev)
+    outs = [stack(xd).cpu().numpy() for _ in range(2)]
+    assert np.array_equal(outs[0], outs[1])
+    ref = x
+    for s, w in zip(specs, ws):
+        ref = O.direct_conv_f64(ref, w, s).astype(np.float32)
+    assert O.max_rel_error(outs[0], ref) <= 4 * TOL[6], O.max_rel_error(outs[0], ref)
