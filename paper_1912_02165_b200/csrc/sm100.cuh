@@ -3,7 +3,8 @@
 // allocation, tcgen05.mma (kind::f16, SS and TS forms), tcgen05.ld/st and the
 // UMMA shared-memory / instruction descriptors.
 //
-// Layout conventions (verified by tests/test_gpu_umma.py on a B200):
+// Layout conventions (verified bit-exact against a CPU GEMM by the layout
+// checks of tools/ubench/ubench.cu on a B200, SS and TS forms):
 //   * K-major, no-swizzle ("interleaved") operand in shared memory: an operand
 //     tile of R rows x K bf16 is stored as 8-row x 16-byte core matrices.
 //     byte(r, k) = (r/8)*SBO + (k/8)*LBO + (r%8)*16 + (k%8)*2.
