@@ -424,22 +424,58 @@ class ConfigRunner:
     def variants(self):
         return [p.variant for _, plans, _ in self.runs for p in plans]
 
+    def capture(self):
+        """One CUDA graph per layer call (the launches of a step are then
+        graph replays: no Python / ctypes overhead between a layer's start
+        event and its kernels).  Returns the library launches per step."""
+        torch = self.torch
+        from paper_1912_02165_b200 import _lib
+        lib = _lib.load()
+        torch.cuda.synchronize(self.dev)
+        n0 = lib.wf_kernel_launches()
+        graphs = []
+        try:
+            for g, plans, x in self.runs:
+                for plan in plans:
+                    gr = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gr):
+                        x = plan(x)
+                    graphs.append(gr)
+        except Exception as exc:          # fall back to direct launches
+            self.graph_error = str(exc)
+            torch.cuda.synchronize(self.dev)
+            graphs = None
+        self.graphs = graphs
+        return lib.wf_kernel_launches() - n0
+
     def step(self, events=None):
         """One pass over all layers; events: list of (start, end) per layer."""
         stream = self.torch.cuda.current_stream(self.dev)
-        k = 0
-        for g, plans, x in self.runs:
-            for plan in plans:
-                if events is not None:
-                    events[k][0].record(stream)
-                x = plan(x)
-                if events is not None:
-                    events[k][1].record(stream)
-                k += 1
+        calls = self.graphs
+        if calls is None:
+            calls = []
+            for g, plans, x in self.runs:
+                for plan in plans:
+                    calls.append((plan, x))
+                    x = plan.out
+        for k, c in enumerate(calls):
+            if events is not None:
+                events[k][0].record(stream)
+            if self.graphs is not None:
+                c.replay()
+            else:
+                c[0](c[1])
+            if events is not None:
+                events[k][1].record(stream)
 
     def time(self, steps, warmup):
         torch = self.torch
         for _ in range(max(warmup, 3)):
+            self.flush.zero_()
+            self.graphs = None
+            self.step()
+        self.launches_per_step = self.capture()
+        for _ in range(2):
             self.flush.zero_()
             self.step()
         torch.cuda.synchronize(self.dev)
@@ -510,13 +546,11 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    launches0 = _lib.load().wf_kernel_launches()
     with ClockSampler(local) as clocks:
         w0 = time.perf_counter()
         step_ms, layer_ms = runner.time(args.steps, args.warmup)
         clocks.mark(w0, time.perf_counter())
-    launches = _lib.load().wf_kernel_launches() - launches0
-    launches_per_step = launches // (args.steps + max(args.warmup, 3))
+    launches_per_step = runner.launches_per_step
     if world > 1:
         dist.barrier()
     ms = max_over_ranks(sum(step_ms) / args.steps)
@@ -632,7 +666,9 @@ def run_ours(args):
             "config": {"workload": _workload(cfg_name, world), "engine": args.engine, "precision": args.precision,
                        "l2": "flushed (256 MB write) before every timed step",
                        "images_per_s": runner.items[0]["spec"].batch * (1 if cfg_name in STRONG else world)
-                       / (ms * 1e-3), "parallelism": f"batch shards x{world}", "variants": runner.variants()},
+                       / (ms * 1e-3), "parallelism": f"batch shards x{world}", "variants": runner.variants(),
+                       "launch": "one CUDA graph per layer call, replayed per step" if runner.graphs is not None
+                       else f"direct launches (graph capture failed: {getattr(runner, 'graph_error', '')})"},
             "roofline": {"bound": rt["bound"], "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak, "traffic": traffic_from_profiles(cfg_name),
                          "kernel": f"{dit['ld'].label()} ({runner.variants()[dom] or args.engine})",

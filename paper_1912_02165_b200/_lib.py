@@ -16,7 +16,7 @@ from .errors import (InvalidParameterError, NativeLibraryError, ShapeMismatchErr
                      UnsupportedConfigError, WinofuseError)
 
 LIB_NAME = "libwinofuse_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("WF_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 WF_OK, WF_ERR_PARAM, WF_ERR_SHAPE, WF_ERR_UNSUPPORTED, WF_ERR_CUDA, WF_ERR_SCRATCH = range(6)
 WF_WINOGRAD, WF_FFT16 = 0, 1

@@ -59,10 +59,11 @@ __global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __rest
     if (tvalid) tile_coords(g, tile, b, ty, tx);
     const int iy = ty * g.m - g.pad_lo + r, ox = tx * g.m - g.pad_lo;
     const bool rvalid = tvalid && iy >= 0 && iy < g.H;
-    for (int ci4 = 0; ci4 < kFftCh / 2; ++ci4) {
-      const int c = (grp >> 3) * (kFftCh / 2) + ci4;
-      const int ch = cg0 + c;
-      float row[16];
+    // the group's 4 channel rows are loaded one channel ahead of the FFT
+    // that uses them (double-buffered in registers): the global-load latency
+    // of channel c + 1 overlaps the transforms of channel c
+    auto load_row = [&](int ci4, float (&row)[16]) {
+      const int ch = cg0 + (grp >> 3) * (kFftCh / 2) + ci4;
       if (rvalid && ch < g.C) {
         const float* src = x + ((static_cast<size_t>(b) * g.C + ch) * g.H + iy) * g.W;
         const int sh = ox & 3;                       // window start inside its 16-byte word
@@ -90,6 +91,14 @@ __global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __rest
 #pragma unroll
         for (int s = 0; s < 16; ++s) row[s] = 0.0f;
       }
+    };
+    float rows[2][16];
+    load_row(0, rows[0]);
+#pragma unroll
+    for (int ci4 = 0; ci4 < kFftCh / 2; ++ci4) {
+      const int c = (grp >> 3) * (kFftCh / 2) + ci4;
+      if (ci4 + 1 < kFftCh / 2) load_row(ci4 + 1, rows[(ci4 + 1) & 1]);
+      float (&row)[16] = rows[ci4 & 1];
       float fr[9], fi[9];
       fft::rfft16(row, fr, fi);
 #pragma unroll
@@ -192,20 +201,28 @@ __global__ void __launch_bounds__(kInvThreads) fft_inverse_kernel(const float* _
   const int cg0 = blockIdx.y * kInvCh;
   const int tl = tl0 + lane;
   const bool tvalid = tl < ntile;
+  // both channels' spectrum columns are loaded before either FFT runs (64
+  // independent coalesced loads in flight per thread)
+  float rec[kInvCh][16], imc[kInvCh][16];
+#pragma unroll
   for (int c = 0; c < kInvCh; ++c) {
     const int cp = cg0 + c;
-    float re[16], im[16];
     if (tvalid && cp < g.Cp) {
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const size_t row = static_cast<size_t>(u * 9 + v) * g.Nout;
-        re[u] = __ldcg(M + (row + cp) * ldm + tl);
-        im[u] = __ldcg(M + (row + g.Cp + cp) * ldm + tl);
+        rec[c][u] = __ldcg(M + (row + cp) * ldm + tl);
+        imc[c][u] = __ldcg(M + (row + g.Cp + cp) * ldm + tl);
       }
     } else {
 #pragma unroll
-      for (int u = 0; u < 16; ++u) re[u] = im[u] = 0.0f;
+      for (int u = 0; u < 16; ++u) rec[c][u] = imc[c][u] = 0.0f;
     }
+  }
+#pragma unroll
+  for (int c = 0; c < kInvCh; ++c) {
+    float (&re)[16] = rec[c];
+    float (&im)[16] = imc[c];
     fft::fft16<1>(re, im);
 #pragma unroll
     for (int r = 0; r < 14; ++r) zs[((c * 14 + r) * 9 + v) * kInvTiles + lane] = make_float2(re[r], im[r]);

@@ -117,6 +117,36 @@ struct Params {
   int prof;
 };
 
+// Stores with the kernel's L2 eviction priorities (Params::hints).
+// Stores with the kernel's L2 eviction priorities, per window size (compile
+// time: a runtime switch in the store paths measured 12-16% slower even when
+// off): layer input and output evict-first, ring stores evict-last.
+#ifndef WF_WS_L2_HINTS_T6
+#define WF_WS_L2_HINTS_T6 1
+#endif
+#ifndef WF_WS_L2_HINTS_T8
+#define WF_WS_L2_HINTS_T8 1
+#endif
+template <class S>
+struct Hints {
+  static constexpr bool on = S::kT == 6 ? WF_WS_L2_HINTS_T6 : WF_WS_L2_HINTS_T8;
+};
+template <class S, class T>
+__device__ __forceinline__ void out_store(T* p, T v) {
+  if constexpr (Hints<S>::on) st_hint(p, v, l2_policy_evict_first());
+  else *p = v;
+}
+template <class S>
+__device__ __forceinline__ void ring_store(uint2* p, uint2 v) {
+  if constexpr (Hints<S>::on) st_hint(p, v, l2_policy_evict_last());
+  else *p = v;
+}
+template <class S>
+__device__ __forceinline__ void ring_store(float2* p, float2 v) {
+  if constexpr (Hints<S>::on) st_hint(p, v, l2_policy_evict_last());
+  else __stcg(p, v);
+}
+
 // Optional per-CTA role accounting (WF_WS_PROF=1; tools/ws_prof.py):
 // clock64 cycles per slot, globaltimer ns for the role end times.
 constexpr int kProfSlots = 32;
@@ -342,8 +372,12 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
           const int y0 = k == 0 ? fg.ya0 : 0;
           const uint32_t bytes = static_cast<uint32_t>(fg.rows(k) * g.W * 4);
           if (bytes && cl < real)
-            bulk_g2s(xs + cl * P.plane + fg.rowoff(k) * g.W,
-                     P.x + ((static_cast<size_t>(fg.bi0 + k) * g.C + c) * g.H + y0) * g.W, bytes, &sy.fi_full[slot]);
+          {
+            float* sdst = xs + cl * P.plane + fg.rowoff(k) * g.W;
+            const float* gsrc = P.x + ((static_cast<size_t>(fg.bi0 + k) * g.C + c) * g.H + y0) * g.W;
+            if constexpr (Hints<S>::on) bulk_g2s_hint(sdst, gsrc, bytes, &sy.fi_full[slot], l2_policy_evict_first());
+            else bulk_g2s(sdst, gsrc, bytes, &sy.fi_full[slot]);
+          }
         }
       }
     } else {
@@ -453,7 +487,7 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
       // step 2 (lanes cq ^ 2): channels c0 + 2, c0 + 3 join c0, c0 + 1
       const uint32_t got2 = __shfl_xor_sync(0xffffffffu, upper ? A : B, 8);
       if (live)
-        *reinterpret_cast<uint2*>(dst + (r * 8 + s) * S::kUPos) = upper ? make_uint2(got2, B) : make_uint2(A, got2);
+        ring_store<S>(reinterpret_cast<uint2*>(dst + (r * 8 + s) * S::kUPos), upper ? make_uint2(got2, B) : make_uint2(A, got2));
     }
   }
 }
@@ -493,7 +527,7 @@ __device__ __forceinline__ void i_unit6s(const Params& P, const uint8_t* src, Sy
       float o[4];
       at6_line<ScalarOps>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], o[0], o[1], o[2], o[3]);
       if (vec) {
-        *reinterpret_cast<float4*>(ybase + r * g.Wo) = make_float4(o[0], o[1], o[2], o[3]);
+        out_store<S>(reinterpret_cast<float4*>(ybase + r * g.Wo), make_float4(o[0], o[1], o[2], o[3]));
       } else if (oy + r < g.Ho) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -542,7 +576,7 @@ __device__ __forceinline__ void i_unit8(const Params& P, const uint8_t* src, Syn
       if (vec) {
 #pragma unroll
         for (int c = 0; c < 6; c += 2)
-          *reinterpret_cast<float2*>(ybase + r * g.Wo + c) = make_float2(out[c], out[c + 1]);
+          out_store<S>(reinterpret_cast<float2*>(ybase + r * g.Wo + c), make_float2(out[c], out[c + 1]));
       } else if (oy + r < g.Ho) {
 #pragma unroll
         for (int c = 0; c < 6; ++c)
@@ -572,6 +606,14 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
     pf.add(kFWWait, t0);
     t0 = pf.now();
+    if (kind == 2 && (P.discard & 2)) {
+      // the I unit's products are in shared memory now: drop their L2 lines
+      // (dead; a write-back would cost DRAM bandwidth), 2-3 lines per worker
+      // thread, ordered before the unit's release like a write
+      const uint8_t* m = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * S::kMSlot +
+                         static_cast<size_t>(sub) * S::kMUnit;
+      for (int i = wtid; i < static_cast<int>(S::kMUnit / 128); i += 256) discard_l2(m + static_cast<size_t>(i) * 128);
+    }
     if (PROF && lane == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
 
     if constexpr (S::kT == 8) {
@@ -656,7 +698,8 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
             split_bf16x2(w[r][s], hi, lo);
             const uint32_t other = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 8);
             if (live)
-              *reinterpret_cast<uint2*>(dst + (r * kT + s) * S::kUPos) = odd ? make_uint2(other, lo) : make_uint2(hi, other);
+              ring_store<S>(reinterpret_cast<uint2*>(dst + (r * kT + s) * S::kUPos),
+                         odd ? make_uint2(other, lo) : make_uint2(hi, other));
           }
         }
       }
@@ -695,8 +738,9 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           float2 o[MO];
           at6_line<PairOps>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], o[0], o[1], o[2], o[3]);
           if (vec) {
-            *reinterpret_cast<float4*>(ybase + r * g.Wo) = make_float4(o[0].x, o[1].x, o[2].x, o[3].x);
-            *reinterpret_cast<float4*>(ybase + plane + r * g.Wo) = make_float4(o[0].y, o[1].y, o[2].y, o[3].y);
+            out_store<S>(reinterpret_cast<float4*>(ybase + r * g.Wo), make_float4(o[0].x, o[1].x, o[2].x, o[3].x));
+            out_store<S>(reinterpret_cast<float4*>(ybase + plane + r * g.Wo),
+                      make_float4(o[0].y, o[1].y, o[2].y, o[3].y));
           } else if (oy + r < g.Ho) {
 #pragma unroll
             for (int c = 0; c < MO; ++c)
@@ -874,7 +918,7 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int k = gu.ng * (kN / 2) + c / 2 + i;
-            __stcg(mrow + (k / S::kIPairs) * (S::kMUnit / 8) + (k % S::kIPairs) * kBlockTiles,
+            ring_store<S>(mrow + (k / S::kIPairs) * (S::kMUnit / 8) + (k % S::kIPairs) * kBlockTiles,
                    make_float2(vv[2 * i], vv[2 * i + 1]));
           }
         }
@@ -920,9 +964,7 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
 // --------------------------------------------------------------- publisher
 template <class S, bool PROF>
 __device__ void publisher(const Params& P, Sync& sy, int n_g) {
-  // lane 0 polls and publishes; for I units the whole warp first drops the
-  // unit's products from L2 (dead once staged; dropped before the release
-  // that lets G units of a later block write the ring slot again)
+  // lane 0 polls the per-unit worker counts and publishes the unit
   const int lane = threadIdx.x & 31;
   const ProfT<PROF> pf(P.prof && lane == 0);
   int* doneF = P.counters;
@@ -936,12 +978,6 @@ __device__ void publisher(const Params& P, Sync& sy, int n_g) {
     __syncwarp();
     int kind, b, sub;
     wk.decode(P, uf, kind, b, sub);
-    if (kind == 2 && (P.discard & 2)) {
-      const uint8_t* m = reinterpret_cast<const uint8_t*>(P.mring) + static_cast<size_t>(b % P.NM) * S::kMSlot +
-                         static_cast<size_t>(sub) * S::kMUnit;
-      for (int i = lane; i < static_cast<int>(S::kMUnit / 128); i += 32) discard_l2(m + static_cast<size_t>(i) * 128);
-      __syncwarp();
-    }
     if (lane == 0) {
       const long long t0 = pf.now();
       red_release_gpu((kind == 0 ? doneF : doneI) + b, 1);
@@ -1057,9 +1093,11 @@ static Plan plan_t(const Geo& g, const FusedOpts& o) {
   }
   pl.plane = round_up(max_rows * g.W, 32) + 16;
   if (static_cast<size_t>(S::kCPC) * pl.plane * 4 > S::kFISlot) return pl;
-  // measured on c2 (tools/ws_time.py): rings of 300 MB (slightly past L2)
-  // with the I units 32 steps behind their F units are best (80 us)
-  size_t budget = o.ring_bytes ? o.ring_bytes : static_cast<size_t>(tuning_knob("WF_WS_BUDGET_MB", 300)) << 20;
+  // ring budget 140 MB (the U + M rings of c2 take 70 MB: inside the 126 MB
+  // L2 next to the streamed input and output).  Measured (tools/ring_sweep.py,
+  // c2): budget 100 / 120 / 140 / 200 / 300 MB -> 103 / 87 / 82 / 81 / 82 us;
+  // smaller rings starve the lagged pipeline
+  size_t budget = o.ring_bytes ? o.ring_bytes : static_cast<size_t>(tuning_knob("WF_WS_BUDGET_MB", 140)) << 20;
   int slots = static_cast<int>(budget / (S::kUSlot + S::kMSlot));
   if (slots < 4) slots = 4;
   pl.NU = std::min(slots / 2, g.n_blk);
@@ -1161,14 +1199,15 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.g = g;
   P.NU = pl.NU; P.NM = pl.NM; P.L2 = pl.L2;
   P.passes = passes;
-  // consumed ring lines dropped from L2 (discard.global.L2) instead of being
-  // written back dead (measured on c2, ncu DRAM bytes / time): none 281 MB;
-  // U only (by the epilogue warps, default) 175 MB at the same time; M only
-  // (by the publisher) 212 MB, same time; both 99 MB but +2-4 us (the M
-  // discards delay the I publishes)
-  // T = 8 and the 16-channel (RGB) instance: faster without (measured c5
-  // 2-3%, VGG 3->64 @224 376 -> 359 us)
-  P.discard = tuning_knob("WF_WS_DISCARD", (g.T == 6 && g.Cpad > 16) ? 1 : 0);
+  // Dead ring lines dropped from L2 (discard.global.L2) instead of being
+  // written back (bit 1: U, by the G epilogue; bit 2: M, by the I workers).
+  // Measured with the L2 eviction priorities (Hints) and 70 MB rings
+  // (tools/ring_sweep.py under ncu, L2 cleaned before the call): c2 without
+  // discards 170 MB of DRAM per call at 79.9 us, with the U discards 97 MB
+  // (0.94 x Q_fused) at 81.9 us; c5 64->64 @56 866 MB without, 554 MB with
+  // U, 449 MB (1.09 x Q_fused) with M discards at +2.5% (128->128 @112 +7%),
+  // 385 MB with both at +6%.  The 16-channel (RGB) instance runs without.
+  P.discard = tuning_knob("WF_WS_DISCARD", g.T == 8 ? 2 : (g.Cpad > 16 ? 1 : 0));
   P.dbg = 0;
 #ifdef WF_TUNING_AIDS
   P.dbg = tuning_knob("WF_WS_DBG", 0);     // 3: no GEMM work (results invalid)
