@@ -256,6 +256,7 @@ class B200PlanReport:
     bytes: dict = field(default_factory=dict)      # per level, fused and three-stage
     seconds: dict = field(default_factory=dict)    # per level / engine prediction
     predicted_winner: str = ""
+    fitted: dict = field(default_factory=dict)     # times from the measurement-fitted rates (B200Fit)
 
     def format(self) -> str:
         s, b = self.seconds, self.bytes
@@ -270,6 +271,8 @@ class B200PlanReport:
              f"L2 bytes fused {b['l2_fused'] / 1e6:.1f} MB"),
             (f"time (us): HBM fused {s['hbm_fused'] * 1e6:.1f}, L2 fused {s['l2_fused'] * 1e6:.1f}, tensor "
              f"{s['tensor'] * 1e6:.1f} -> fused {s['fused'] * 1e6:.1f}; three-stage {s['three'] * 1e6:.1f}"),
+            (f"fitted to measured layers (machines/b200_fit.json): fused {self.fitted['fused'] * 1e6:.1f} us, "
+             f"three-stage {self.fitted['three'] * 1e6:.1f} us" if self.fitted else "no fitted rates for this transform"),
             f"predicted winner: {self.predicted_winner}",
         ])
 
@@ -329,9 +332,142 @@ def plan_b200(layer: LayerSpec, tile: int, machine: B200Model | None = None, tra
     else:
         variant = "L2 waves (three kernels per wave)"
     winner = "fused" if t_fused < 0.95 * t_three else ("three_stage" if t_three < 0.95 * t_fused else "tie")
+    fitted = {}
+    fit_path = Path(__file__).parent / "machines" / "b200_fit.json"
+    if transform != "fft" and fit_path.exists():
+        # rates fitted to measured layers (fit_b200): the prediction that decides the crossover
+        fit = B200Fit.from_file(fit_path)
+        ops = transform_ops(layer, tile)
+        tens = passes * f_tile * n_tile
+        tf = fit.t0_fused + max(l2_fused / fit.l2_rate, tens / (fit.tc_eff * mach.tensor_bf16_flops), ops / fit.cc_rate)
+        t3 = 3 * fit.t0_launch + hbm_three / fit.hbm_rate + tens / (fit.tc_eff * mach.tensor_bf16_flops) + \
+            ops / fit.cc_rate
+        fitted = {"fused": tf, "three": t3}
+        winner = "fused" if tf < t3 else "three_stage"
     return B200PlanReport(layer=layer, tile=tile, transform=transform, passes=passes, n_tile=n_tile,
                           block_tiles=block_tiles, blocks=blocks, fused_variant=variant, r_lower=r_lo, r_upper=r_up,
                           bytes={"hbm_fused": hbm_fused, "hbm_three": hbm_three, "l2_fused": l2_fused},
                           seconds={"hbm_fused": t_hbm_f, "hbm_three": t_hbm_3, "l2_fused": t_l2, "tensor": tensor,
                                    "fused": t_fused, "three": t_three},
-                          predicted_winner=winner)
+                          predicted_winner=winner, fitted=fitted)
+
+
+# ------------------------------------------------- B200 model fitted to measurements
+# CUDA-core operations per transform line (the factored 1-D transforms of
+# csrc/common.cuh: bt*_line / at*_line) and per bf16 hi/lo split of a value.
+_BT_LINE = {4: 6, 5: 12, 6: 14, 7: 22, 8: 26}
+_AT_LINE = {4: 4, 5: 8, 6: 10, 7: 16, 8: 20}
+_SPLIT_OPS = 4
+
+
+def transform_ops(layer: LayerSpec, tile: int) -> float:
+    """CUDA-core operations of the forward (2T lines + T^2 splits per tile and
+    input channel) and inverse (T + m lines per tile and output channel)
+    transforms of one Winograd layer."""
+    m = tile - layer.kernel + 1
+    n_tile = layer.batch * -(-layer.out_height // m) * -(-layer.out_width // m)
+    fwd = 2 * tile * _BT_LINE[tile] + _SPLIT_OPS * tile * tile
+    inv = (tile + m) * _AT_LINE[tile]
+    return float(n_tile) * (layer.in_channels * fwd + layer.out_channels * inv)
+
+
+@dataclass(frozen=True)
+class B200Fit:
+    """Effective rates of the B200 engines, fitted to measured layer times
+    (``fit_b200``).  Fused (L2-staged dataflow kernel):
+
+        t_fused = t0_fused + max(L2 ring bytes / l2_rate, tensor / tc_eff, ops / cc_rate)
+
+    Three-stage (three kernels, the intermediates make an HBM round trip):
+
+        t_three = 3 t0_launch + HBM bytes / hbm_rate + tensor / tc_eff + ops / cc_rate
+    """
+
+    l2_rate: float          # bytes/s of ring traffic the fused kernel sustains
+    hbm_rate: float         # bytes/s the stage kernels sustain
+    cc_rate: float          # transform operations/s (all SMs)
+    tc_eff: float           # fraction of the bf16 tensor peak the GEMMs reach
+    t0_fused: float         # fixed cost of a fused launch (fill + drain), s
+    t0_launch: float        # fixed cost per stage kernel, s
+    rms_log_error: float = 0.0
+    samples: int = 0
+
+    def predict(self, layer: LayerSpec, tile: int, machine: "B200Model | None" = None, precision: str = "3xbf16"):
+        """-> (t_fused, t_three) in seconds."""
+        mach = machine or B200Model()
+        rep = plan_b200(layer, tile, mach, precision=precision)
+        tensor = rep.seconds["tensor"] * mach.tensor_bf16_flops
+        ops = transform_ops(layer, tile)
+        t_f = self.t0_fused + max(rep.bytes["l2_fused"] / self.l2_rate, tensor / (self.tc_eff * mach.tensor_bf16_flops),
+                                  ops / self.cc_rate)
+        t_3 = 3 * self.t0_launch + rep.bytes["hbm_three"] / self.hbm_rate + \
+            tensor / (self.tc_eff * mach.tensor_bf16_flops) + ops / self.cc_rate
+        return t_f, t_3
+
+    def winner(self, layer: LayerSpec, tile: int, machine=None, precision: str = "3xbf16") -> str:
+        t_f, t_3 = self.predict(layer, tile, machine, precision)
+        return "fused" if t_f < t_3 else "three_stage"
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k in self.__dataclass_fields__}
+
+    @classmethod
+    def from_file(cls, path) -> "B200Fit":
+        return cls(**json.loads(Path(path).read_text()))
+
+
+def fit_b200(measurements, machine: "B200Model | None" = None) -> B200Fit:
+    """Least-squares fit (in log time) of the B200Fit rates to measured
+    Winograd layers: ``measurements`` = iterable of dicts with ``layer``
+    (LayerSpec), ``tile``, ``fused_s`` (warp-specialised kernel) and
+    ``three_s`` -- e.g. the per-layer rows of bench.py's per_config block
+    (machines/b200_measured.json).  The reference fits nothing (its planner
+    reads given machine numbers, roofline.py:227-254); on the B200 the
+    achievable rates of the dataflow kernels are what decides the
+    fused / three-stage crossover, so they are measured and fitted."""
+    import numpy as np
+    from scipy.optimize import least_squares
+
+    mach = machine or B200Model()
+    rows = list(measurements)
+    if len(rows) < 6:
+        raise InvalidParameterError("need at least 6 measured layers to fit the B200 model")
+    feats = []
+    for r in rows:
+        rep = plan_b200(r["layer"], r["tile"], mach)
+        feats.append((rep.bytes["l2_fused"], rep.bytes["hbm_three"], rep.seconds["tensor"] * mach.tensor_bf16_flops,
+                      transform_ops(r["layer"], r["tile"]), r["fused_s"], r["three_s"]))
+    f = np.array(feats, dtype=np.float64)
+
+    def model(x):
+        l2, hbm, cc, tc, t0f, t0l = np.exp(x)
+        tens = f[:, 2] / (tc * mach.tensor_bf16_flops)
+        ops = f[:, 3] / cc
+        tf = t0f + np.maximum(np.maximum(f[:, 0] / l2, tens), ops)
+        t3 = 3 * t0l + f[:, 1] / hbm + tens + ops
+        return tf, t3
+
+    def resid(x):
+        tf, t3 = model(x)
+        return np.concatenate([np.log(tf / f[:, 4]), np.log(t3 / f[:, 5])])
+
+    x0 = np.log([5e12, 4e12, 3e13, 0.4, 10e-6, 5e-6])
+    lo = np.log([1e11, 1e11, 1e11, 0.01, 1e-7, 1e-7])
+    hi = np.log([1e15, 2e13, 1e16, 1.0, 1e-3, 1e-3])
+    sol = least_squares(resid, x0, bounds=(lo, hi))
+    p = np.exp(sol.x)
+    err = float(np.sqrt(np.mean(resid(sol.x) ** 2)))
+    return B200Fit(l2_rate=float(p[0]), hbm_rate=float(p[1]), cc_rate=float(p[2]), tc_eff=float(p[3]),
+                   t0_fused=float(p[4]), t0_launch=float(p[5]), rms_log_error=err, samples=len(rows))
+
+
+def measured_layers(path=None):
+    """The measured per-layer table shipped with the package
+    (machines/b200_measured.json: bench.py per_config rows) as fit_b200 input."""
+    p = Path(path) if path else Path(__file__).parent / "machines" / "b200_measured.json"
+    doc = json.loads(p.read_text())
+    out = []
+    for r in doc["layers"]:
+        out.append({"layer": LayerSpec(r["batch"], r["c"], r["cp"], r["hw"], r["hw"], 3, 1, 1), "tile": r["tile"],
+                    "fused_s": r["fused_ms"] * 1e-3, "three_s": r["three_stage_ms"] * 1e-3, "name": r["name"]})
+    return out

@@ -478,3 +478,26 @@ def test_mixed_layer_stack_called_twice_matches_oracle():
     for s, w in zip(specs, ws):
         ref = O.direct_conv_f64(ref, w, s).astype(np.float32)
     assert O.max_rel_error(outs[0], ref) <= 4 * TOL[6], O.max_rel_error(outs[0], ref)
+
+
+def test_concurrent_persistent_launches_on_two_streams():
+    """Two warp-specialised fused layers launched back to back on two streams
+    (the co-residency hazard of spin-waiting persistent kernels): the
+    cooperative launch makes the driver schedule each grid whole, so both
+    complete, bitwise equal to a serial run."""
+    import torch
+    dev = torch.device("cuda", 0)
+    spec = wf.LayerSpec(16, 64, 64, 56, 56, 3, 1, 1)
+    rng = np.random.default_rng(9)
+    x = torch.from_numpy(rng.standard_normal(spec.input_dims()).astype(np.float32)).to(dev)
+    pack = wf.transform_kernels(wf.Tensor4D(_he(rng, spec)), wf.make_basis(6))
+    plans = [wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=6, device=dev)) for _ in range(2)]
+    ref = plans[0](x).clone()
+    streams = [torch.cuda.Stream(dev) for _ in range(2)]
+    for _ in range(20):
+        for p, s in zip(plans, streams):
+            with torch.cuda.stream(s):
+                p(x)
+    torch.cuda.synchronize()
+    assert all(p.variant == "ws" and p.ran.value == 1 for p in plans)
+    assert all(torch.equal(p.out, ref) for p in plans)

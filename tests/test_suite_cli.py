@@ -135,3 +135,23 @@ def test_host_pipeline_matches_single_call(cuda_dev):
         y_host.zero_()
         wf.HostPipeline(spec, pack, cfg, chunks=chunks)(x_host, y_host)
         assert np.array_equal(y_host.numpy(), ref), chunks
+
+
+def test_b200_model_fitted_to_measured_layers():
+    """The B200 planner's rates are fitted to measured layer times (the
+    warp-specialised fused kernel and the three-stage engine, bench.py
+    per_config rows shipped in machines/b200_measured.json): the fit
+    reproduces the measurements within ~20% RMS (log) and predicts the
+    measured fused / three-stage winner of every layer, including the c5
+    crossover sweep."""
+    from paper_1912_02165_b200 import roofline
+    rows = roofline.measured_layers()
+    fit = roofline.fit_b200(rows)
+    assert fit.samples == len(rows) >= 12 and fit.rms_log_error < 0.3
+    for r in rows:
+        want = "fused" if r["fused_s"] < r["three_s"] else "three_stage"
+        assert fit.winner(r["layer"], r["tile"]) == want, r["name"]
+    shipped = roofline.B200Fit.from_file(roofline.sample_model_path("b200_fit"))
+    assert abs(shipped.l2_rate / fit.l2_rate - 1) < 0.05
+    rep = roofline.plan_b200(wf.LayerSpec(256, 16, 16, 28, 28, 3, 1, 1), 8)
+    assert rep.fitted and rep.predicted_winner == "fused" and "fitted" in rep.format()
