@@ -114,7 +114,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
     ap.add_argument("--engine", default="fused", choices=["fused", "three_stage"])
-    ap.add_argument("--precision", default="3xbf16", choices=["3xbf16", "bf16"])
+    ap.add_argument("--precision", default="3xbf16", choices=["3xbf16", "3xfp16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-config", action="store_true", help="headline config only")
     ap.add_argument("--per-config-steps", type=int, default=5)
@@ -150,7 +150,7 @@ def roofline_terms(spec, tile, precision="3xbf16"):
         q_three = q_fused + 2 * 4 * tile * tile * n_tile * (c + cp)
         f_gemm = 2 * n_tile * c * cp * tile * tile
     hbm, bf16, _ = measured_peaks()
-    passes = 3 if precision == "3xbf16" else 1
+    passes = 1 if precision == "bf16" else 3
     t_hbm = q_fused / (hbm * 1e9)
     t_tc = passes * f_gemm / (bf16 * 1e12)
     return {"n_tile": n_tile, "q_fused": q_fused, "q_three": q_three, "f_gemm": f_gemm,
@@ -641,7 +641,7 @@ def run_ours(args):
         if rt["bound"] == "hbm":
             achieved, peak, unit = rt["q_fused"] / (d_ms * 1e-3) / 1e9, hbm_peak, "GB/s"
         else:
-            passes = 3 if args.precision == "3xbf16" else 1
+            passes = 1 if args.precision == "bf16" else 3
             achieved, peak, unit = passes * rt["f_gemm"] / (d_ms * 1e-3) / 1e12, bf16_peak, "TFLOP/s"
         cpu = cpu3 = None
         if not args.no_cpu_baseline and world == 1:
@@ -660,8 +660,9 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if cfg_name in STRONG else "weak", "vs_baseline": None,
-            "dtype": "f32 io, bf16x3 split tensor-core (f32 accumulate)" if args.precision == "3xbf16"
-            else "f32 io, bf16 tensor-core",
+            "dtype": {"3xbf16": "f32 io, bf16x3 split tensor-core (f32 accumulate)",
+                      "3xfp16": "f32 io, fp16x3 split tensor-core (f32 accumulate)",
+                      "bf16": "f32 io, bf16 tensor-core"}[args.precision],
             "data": "synthetic: seeded N(0,1) (c5: U(-1,1)) inputs, He-normal weights (the reference uses no dataset)",
             "config": {"workload": _workload(cfg_name, world), "engine": args.engine, "precision": args.precision,
                        "l2": "flushed (256 MB write) before every timed step",

@@ -36,8 +36,11 @@ extern "C" {
 #define WF_FFT16 1
 
 /* tensor-core precision mode */
-#define WF_PREC_3XBF16 0 /* x = hi + lo (bf16), hi*hi + hi*lo + lo*hi, f32 accumulate */
-#define WF_PREC_BF16 1   /* single bf16 pass (fast, loose)                         */
+#define WF_PREC_3XBF16 0 /* x = hi + lo (bf16), hi*hi + hi*lo + lo*hi, f32 accumulate  */
+#define WF_PREC_BF16 1   /* single bf16 pass (fast, loose)                          */
+#define WF_PREC_3XFP16 2 /* x = hi + lo (fp16, 11-bit significands), three passes:  */
+                         /* ~22-bit products at the bf16 rate; needs the transformed */
+                         /* values inside the fp16 range (|u| < 65504)               */
 
 /* Mirrors LayerSpec (reference winofuse/tensor.py:36-78). */
 typedef struct wf_layer {
@@ -67,9 +70,14 @@ int wf_filter_transform(const float* w, float* pack, int c_in, int c_out, int ti
 
 /* Bytes of the MMA-ready packed kernels (bf16 hi/lo, UMMA K-major tiles). */
 size_t wf_mma_pack_bytes(int tile, int c_in, int c_out, int transform);
-/* Reference-layout f32 pack (T*T, C, C') -> MMA-ready device pack. */
+/* Reference-layout f32 pack (T*T, C, C') -> MMA-ready device pack (3xbf16 /
+ * bf16 operand format). */
 int wf_mma_pack(const float* pack, void* mma_pack, int tile, int c_in, int c_out, int transform,
                 void* stream);
+/* The same for a precision mode (WF_PREC_*): the operand format (bf16 or fp16
+ * hi/lo) of the pack must match the precision the engines run with. */
+int wf_mma_pack_ex(const float* pack, void* mma_pack, int tile, int c_in, int c_out, int transform, int precision,
+                   void* stream);
 
 /* ---------------------------------------------------------------- engines --
  * conv_three_stage (winofuse/engines.py:234-314): forward-transform every

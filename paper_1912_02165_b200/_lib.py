@@ -20,12 +20,14 @@ LIB_PATH = os.environ.get("WF_LIB_PATH") or os.path.join(os.path.dirname(os.path
 
 WF_OK, WF_ERR_PARAM, WF_ERR_SHAPE, WF_ERR_UNSUPPORTED, WF_ERR_CUDA, WF_ERR_SCRATCH = range(6)
 WF_WINOGRAD, WF_FFT16 = 0, 1
-WF_PREC_3XBF16, WF_PREC_BF16 = 0, 1
+WF_PREC_3XBF16, WF_PREC_BF16, WF_PREC_3XFP16 = 0, 1, 2
 WF_PHASE_FORWARD, WF_PHASE_MULTIPLY, WF_PHASE_INVERSE = 1, 2, 4
 WF_FUSED_AUTO, WF_FUSED_WS, WF_FUSED_ITEMQ, WF_FUSED_WAVES = 0, 1, 2, 3
 WF_FUSED_COUNTERS_CLEAN, WF_FUSED_INSTRUMENT = 1, 2
 
-PRECISIONS = {"3xbf16": WF_PREC_3XBF16, "bf16": WF_PREC_BF16}
+PRECISIONS = {"3xbf16": WF_PREC_3XBF16, "bf16": WF_PREC_BF16, "3xfp16": WF_PREC_3XFP16}
+# operand format of the device MMA pack per precision mode
+PACK_FORMAT = {"3xbf16": "bf16", "bf16": "bf16", "3xfp16": "fp16"}
 TRANSFORMS = {"winograd": WF_WINOGRAD, "fft": WF_FFT16}
 # fused-engine variants (EngineConfig.fused_variant <-> WF_FUSED_*)
 VARIANTS = {"auto": WF_FUSED_AUTO, "ws": WF_FUSED_WS, "itemq": WF_FUSED_ITEMQ, "waves": WF_FUSED_WAVES}
@@ -62,6 +64,7 @@ SIGNATURES = {
     "wf_filter_transform": (_i, [_fp, _fp, _i, _i, _i, _vp]),
     "wf_mma_pack_bytes": (_sz, [_i, _i, _i, _i]),
     "wf_mma_pack": (_i, [_fp, _vp, _i, _i, _i, _i, _vp]),
+    "wf_mma_pack_ex": (_i, [_fp, _vp, _i, _i, _i, _i, _i, _vp]),
     "wf_three_stage_scratch_bytes": (_sz, [_LP, _i, _i]),
     "wf_conv_three_stage": (_i, [_fp, _vp, _fp, _vp, _sz, _LP, _i, _i, _i, _vp]),
     "wf_conv_three_stage_phases": (_i, [_fp, _vp, _fp, _vp, _sz, _LP, _i, _i, _i, _i, _vp]),

@@ -139,6 +139,7 @@ static int make_geo(const wf_layer* L, int tile, int transform, Geo& g) {
   g.P = g.fft ? 16 * 9 : g.T * g.T;
   g.Nout = g.fft ? 2 * g.Cp : g.Cp;
   g.n_blk = ceil_div(g.n_tile, kBlockTiles);
+  g.cplx = g.fft && fft_cplx_pack(g.C, g.Cp) ? 1 : 0;
   return WF_OK;
 }
 
@@ -147,6 +148,7 @@ static int precision_passes(int precision) {
   switch (precision) {
     case WF_PREC_3XBF16: return 3;
     case WF_PREC_BF16: return 1;
+    case WF_PREC_3XFP16: return 3 | kPrecF16;
   }
   return 0;
 }
@@ -188,8 +190,11 @@ __global__ void filter_transform_kernel(const float* __restrict__ w, float* __re
 
 // ----------------------------------------------------------------- MMA pack
 // V slab (p, hl): rows = c' (Cppad), K = c (Cpad), bf16 hi/lo split of the f32 pack.
+struct PosScale {
+  float v[64];   // per-position factor of the V operand (3xfp16 balancing, common.cuh)
+};
 __global__ void mma_pack_kernel(const float* __restrict__ pack, uint8_t* __restrict__ out, int P,
-                                int C, int Cp, int Cpad, int Cppad) {
+                                int C, int Cp, int Cpad, int Cppad, int f16, PosScale sc, int cplx) {
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long per_p = static_cast<long long>(Cppad) * (Cpad / 2);
   if (idx >= per_p * P) return;
@@ -198,12 +203,25 @@ __global__ void mma_pack_kernel(const float* __restrict__ pack, uint8_t* __restr
   const int n = static_cast<int>(rem / (Cpad / 2));
   const int c = static_cast<int>(rem - static_cast<long long>(n) * (Cpad / 2)) * 2;
   float a = 0.0f, b = 0.0f;
-  if (n < Cp) {
+  if (cplx) {
+    // W[n][k] for output column n < C'/2 of the real expansion P (2C x C'
+    // here, C and Cp being 2C_in and 2C'_out): P[k][n] for the Re inputs
+    // (k < C/2), -P[k][n] (= +Im V) for the Im inputs
+    const int half = C / 2;
+    if (n < Cp / 2) {
+      if (c < C) a = pack[(static_cast<size_t>(p) * C + c) * Cp + n] * (c < half ? 1.0f : -1.0f);
+      if (c + 1 < C) b = pack[(static_cast<size_t>(p) * C + c + 1) * Cp + n] * (c + 1 < half ? 1.0f : -1.0f);
+    }
+  } else if (n < Cp) {
     if (c < C) a = pack[(static_cast<size_t>(p) * C + c) * Cp + n];
     if (c + 1 < C) b = pack[(static_cast<size_t>(p) * C + c + 1) * Cp + n];
   }
   uint32_t hi, lo;
-  split_bf16x2(a, b, hi, lo);
+  if (f16) {
+    const float f = p < 64 ? sc.v[p] : 1.0f;
+    split_f16x2(a * f, b * f, hi, lo);
+  }
+  else split_bf16x2(a, b, hi, lo);
   const size_t slab = static_cast<size_t>(Cppad) * Cpad * 2;
   uint8_t* base = out + static_cast<size_t>(p) * 2 * slab + slab_off(n, c, Cppad, Cpad);
   *reinterpret_cast<uint32_t*>(base) = hi;
@@ -341,21 +359,33 @@ int wf_filter_transform(const float* w, float* pack, int c_in, int c_out, int ti
 
 size_t wf_mma_pack_bytes(int tile, int c_in, int c_out, int transform) {
   if (c_in < 1 || c_out < 1) return 0;
-  if (transform == WF_FFT16 && tile == 16)   // 144 bins, real-expanded (2C x 2C') complex GEMM
+  if (transform == WF_FFT16 && tile == 16) {  // 144 bins, real-expanded (2C x 2C') complex GEMM
+    if (fft_cplx_pack(c_in, c_out))           // or [Re V^T | Im V^T] (C' x 2C) per bin
+      return static_cast<size_t>(144) * 2 * round_up(c_out, 16) * round_up(2 * c_in, 16) * 2;
     return static_cast<size_t>(144) * 2 * round_up(2 * c_out, 16) * round_up(2 * c_in, 16) * 2;
+  }
   if (transform != WF_WINOGRAD || tile < 4 || tile > 8) return 0;
   return static_cast<size_t>(tile) * tile * 2 * round_up(c_out, 16) * round_up(c_in, 16) * 2;
 }
 
 int wf_mma_pack(const float* pack, void* mma_pack, int tile, int c_in, int c_out, int transform,
                 void* stream) {
+  return wf_mma_pack_ex(pack, mma_pack, tile, c_in, c_out, transform, WF_PREC_3XBF16, stream);
+}
+
+int wf_mma_pack_ex(const float* pack, void* mma_pack, int tile, int c_in, int c_out, int transform, int precision,
+                   void* stream) {
   if (!pack || !mma_pack) return fail(WF_ERR_PARAM, "null pointer");
   if (c_in < 1 || c_out < 1) return fail(WF_ERR_SHAPE, "channels must be >= 1");
+  const int prec = precision_passes(precision);
+  if (prec == 0) return fail(WF_ERR_PARAM, "precision %d", precision);
   int P;
+  int cplx = 0;
   if (transform == WF_FFT16) {
     // pack holds the real expansion (144, 2C, 2C') of the complex bins
     if (tile != 16) return fail(WF_ERR_PARAM, "the FFT transform uses tile 16, got %d", tile);
     P = 144;
+    cplx = fft_cplx_pack(c_in, c_out) ? 1 : 0;
     c_in *= 2;
     c_out *= 2;
   } else if (transform == WF_WINOGRAD) {
@@ -364,11 +394,28 @@ int wf_mma_pack(const float* pack, void* mma_pack, int tile, int c_in, int c_out
   } else {
     return fail(WF_ERR_PARAM, "unknown transform %d", transform);
   }
-  const int Cpad = round_up(c_in, 16), Cppad = round_up(c_out, 16);
+  const int Cpad = round_up(c_in, 16), Cppad = cplx ? round_up(c_out / 2, 16) : round_up(c_out, 16);
   const long long total = 1LL * P * Cppad * (Cpad / 2);
+  // 3xfp16: V' = V / u_scale(r, s) so that U' V' == U V (common.cuh f16_u_scale)
+  PosScale sc;
+  for (int p = 0; p < 64; ++p) sc.v[p] = 1.0f;
+  if (prec_f16(prec) && transform == WF_WINOGRAD) {
+    for (int p = 0; p < P; ++p) {
+      const int r = p / tile, s = p % tile;
+      float u = 1.0f;
+      switch (tile) {
+        case 4: u = f16_u_scale<4>(r, s); break;
+        case 5: u = f16_u_scale<5>(r, s); break;
+        case 6: u = f16_u_scale<6>(r, s); break;
+        case 7: u = f16_u_scale<7>(r, s); break;
+        case 8: u = f16_u_scale<8>(r, s); break;
+      }
+      sc.v[p] = 1.0f / u;
+    }
+  }
   note_launch();
   mma_pack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      pack, static_cast<uint8_t*>(mma_pack), P, c_in, c_out, Cpad, Cppad);
+      pack, static_cast<uint8_t*>(mma_pack), P, c_in, c_out, Cpad, Cppad, prec_f16(prec) ? 1 : 0, sc, cplx);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? WF_OK : cuda_fail(e, "mma_pack");
 }
@@ -404,7 +451,7 @@ int wf_conv_three_stage_phases(const float* x, const void* mma_pack, float* y, v
   const int ldm = g.n_blk * kBlockTiles;
   cudaError_t e = cudaSuccess;
   if (phases & WF_PHASE_FORWARD) {
-    e = launch_forward_slab(x, U, g, 0, g.n_blk, st);
+    e = launch_forward_slab(x, U, g, 0, g.n_blk, passes, st);
     if (e != cudaSuccess) return cuda_fail(e, "forward");
   }
   if (phases & WF_PHASE_MULTIPLY) {

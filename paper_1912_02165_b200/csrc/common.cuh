@@ -32,6 +32,50 @@ cudaError_t launch_coresident(const void* kernel, int grid, int threads, size_t 
 // Whether `grid` CTAs of `kernel` (threads, smem) fit on the current device at once.
 bool coresident_fits(const void* kernel, int grid, int threads, size_t smem);
 
+// Tensor-core precision of a launch: passes (1 or 3) in the low bits, the
+// operand format (bf16 / fp16 hi-lo split) in bit 4.
+constexpr int kPrecF16 = 16;
+__host__ __device__ constexpr int prec_passes(int prec) { return prec & 15; }
+__host__ __device__ constexpr bool prec_f16(int prec) { return (prec & kPrecF16) != 0; }
+
+// 3xfp16 operand balancing.  fp16 has 11-bit significands but a narrow
+// exponent range: the transformed kernels of large tiles are tiny (T = 8:
+// rows of G with L1 norm 0.078, so V ~ 1e-4 and its lo parts subnormal) while
+// the transformed tiles are large.  Position (r, s) therefore runs on
+// U' = U * 2^(e_r + e_s - K) and V' = V * 2^-(e_r + e_s - K), e_r = the
+// rounded log2 of G row r's L1 norm: an exact power-of-two rebalancing
+// (U' V' == U V) that keeps both operands (and their lo parts) in the normal
+// fp16 range for inputs of magnitude up to ~2^10.  FFT-16 runs unscaled.
+constexpr int kF16Shift = 4;
+template <int T>
+__host__ __device__ constexpr int g_row_exp(int r) {
+  double s = (gd<T>(r, 0) < 0 ? -gd<T>(r, 0) : gd<T>(r, 0)) + (gd<T>(r, 1) < 0 ? -gd<T>(r, 1) : gd<T>(r, 1)) +
+             (gd<T>(r, 2) < 0 ? -gd<T>(r, 2) : gd<T>(r, 2));
+  int e = 0;
+  while (s >= 1.5) { s *= 0.5; ++e; }
+  while (s < 0.75) { s *= 2.0; --e; }
+  return e;
+}
+template <int T>
+__host__ __device__ constexpr float f16_u_scale(int r, int s) {
+  int e = g_row_exp<T>(r) + g_row_exp<T>(s) - kF16Shift;
+  float v = 1.0f;
+  while (e > 0) { v *= 2.0f; --e; }
+  while (e < 0) { v *= 0.5f; ++e; }
+  return v;
+}
+// U operand value of position (r, s) as the MMA sees it (scaled for 3xfp16)
+template <int T, bool F16>
+__device__ __forceinline__ float2 u_operand(float2 v, int r, int s) {
+  if constexpr (F16) return make_float2(v.x * f16_u_scale<T>(r, s), v.y * f16_u_scale<T>(r, s));
+  else return v;
+}
+template <int T, bool F16>
+__device__ __forceinline__ float u_operand(float v, int r, int s) {
+  if constexpr (F16) return v * f16_u_scale<T>(r, s);
+  else return v;
+}
+
 // Layer geometry for one (layer, tile) pair; tile order is batch-major, then
 // tile row, then tile column (reference tiling.py:8-11, 66-75).
 struct Geo {
@@ -44,6 +88,7 @@ struct Geo {
   int P;             // transform positions: T*T (Winograd) or 16*9 bins (FFT-16)
   int Nout;          // product rows per position: C' (Winograd) or 2C' (FFT re|im)
   int fft;           // 1 for the FFT-16 overlap-save transform
+  int cplx;          // FFT-16 with the complex-structured pack (fft_cplx_pack): V read once per bin
 };
 
 // ------------------------------------------------------------------------

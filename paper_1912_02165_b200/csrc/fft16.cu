@@ -37,6 +37,7 @@ constexpr size_t kFftSmem = (2ull * kBins * kBinPitch + 16ull * kGroupScratch) *
 
 __device__ __forceinline__ int stage_idx(int p, int c, int t) { return p * kBinPitch + c * kFftTiles + t; }
 
+template <bool F16>
 __global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __restrict__ x, uint8_t* __restrict__ u,
                                                              Geo g, int tile0, int nblk_local) {
   extern __shared__ float smem[];
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __rest
       const float* sa = part ? sim : sre;
       for (int p = pp; p < kBins; p += 4) {
         uint32_t hi, lo;
-        split_bf16x2(sa[stage_idx(p, 2 * q, t)], sa[stage_idx(p, 2 * q + 1, t)], hi, lo);
+        split2<F16>(sa[stage_idx(p, 2 * q, t)], sa[stage_idx(p, 2 * q + 1, t)], hi, lo);
         uint8_t* base = u + ((static_cast<size_t>(p) * nblk_local + blk) * 2) * slab + off;
         *reinterpret_cast<uint32_t*>(base) = hi;
         *reinterpret_cast<uint32_t*>(base + slab) = lo;
@@ -155,9 +156,8 @@ __global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __rest
       const float* sa = part ? sim : sre;
       for (int p = pp; p < kBins; p += 2) {
         const float v = sa[stage_idx(p, c, t)];
-        const uint32_t hv = pack_bf16x2(v, 0.0f);
-        const float vh = __uint_as_float(hv << 16);
-        const uint32_t lv = pack_bf16x2(v - vh, 0.0f);
+        uint32_t hv, lv;
+        split2<F16>(v, 0.0f, hv, lv);
         uint8_t* base = u + ((static_cast<size_t>(p) * nblk_local + blk) * 2) * slab + off;
         *reinterpret_cast<uint16_t*>(base) = static_cast<uint16_t>(hv & 0xFFFFu);
         *reinterpret_cast<uint16_t*>(base + slab) = static_cast<uint16_t>(lv & 0xFFFFu);
@@ -263,14 +263,16 @@ __global__ void __launch_bounds__(kInvThreads) fft_inverse_kernel(const float* _
 
 }  // namespace
 
-cudaError_t launch_fft_forward(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, cudaStream_t st) {
+cudaError_t launch_fft_forward(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int prec,
+                               cudaStream_t st) {
+  auto kern = prec_f16(prec) ? fft_forward_kernel<true> : fft_forward_kernel<false>;
   {
-    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(fft_forward_kernel), static_cast<int>(kFftSmem));
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(kFftSmem));
     if (e != cudaSuccess) return e;
   }
   dim3 grid(ceil_div(nblk * kBlockTiles, kFftTiles), ceil_div(g.C, kFftCh));
   note_launch();
-  fft_forward_kernel<<<grid, 256, kFftSmem, st>>>(x, u, g, blk0 * kBlockTiles, nblk);
+  kern<<<grid, 256, kFftSmem, st>>>(x, u, g, blk0 * kBlockTiles, nblk);
   return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ struct FwdStage {
   int bulk;      // 1: rows staged by bulk async copies, unpadded (W % 4 == 0)
 };
 
-template <int T, int CPC>
+template <int T, int CPC, bool F16>
 __global__ void __launch_bounds__(64 * CPC, (T <= 6 && CPC <= 4) ? 2 : 1)
 forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo g, int blk0,
                       int nblk_local, FwdStage S) {
@@ -182,7 +182,7 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
 #pragma unroll
       for (int s = 0; s < T; ++s) {
         uint32_t hi, lo;
-        split_bf16x2(u2[r][s], hi, lo);
+        split2<F16>(u_operand<T, F16>(u2[r][s], r, s), hi, lo);
         const uint32_t other = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, TPW);
         *reinterpret_cast<uint2*>(dst + (r * T + s) * pstride) = odd ? make_uint2(other, lo) : make_uint2(hi, other);
       }
@@ -194,7 +194,7 @@ forward_staged_kernel(const float* __restrict__ x, uint8_t* __restrict__ u, Geo 
 #pragma unroll
       for (int s = 0; s < T; ++s) {
         uint32_t hi, lo;
-        split_bf16x2(u2[r][s], hi, lo);
+        split2<F16>(u_operand<T, F16>(u2[r][s], r, s), hi, lo);
         uint8_t* p = dst + (r * T + s) * pstride;
         *reinterpret_cast<uint32_t*>(p) = hi;
         *reinterpret_cast<uint32_t*>(p + slab) = lo;
@@ -241,13 +241,13 @@ int forward_staged_cpc(const Geo& g) {
   return 0;
 }
 
-template <int T, int CPC>
+template <int T, int CPC, bool F16>
 static cudaError_t launch_staged(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk,
                                  cudaStream_t st) {
   const FwdStage S = stage_geometry(g);
   // staging planes + (non-bulk path) one 12-byte descriptor per staged row
   const int smem = CPC * S.plane * 4 + (S.bulk ? 0 : CPC * S.trows * g.T * 12);
-  auto kern = forward_staged_kernel<T, CPC>;
+  auto kern = forward_staged_kernel<T, CPC, F16>;
   {
     cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), 200 * 1024);
     if (e != cudaSuccess) return e;
@@ -266,27 +266,34 @@ static cudaError_t launch_staged(const float* x, uint8_t* u, const Geo& g, int b
   return cudaLaunchKernelEx(&cfg, kern, x, u, g, blk0, nblk, S);
 }
 
-template <int T>
+template <int T, bool F16>
 static cudaError_t launch_staged_t(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc,
                                    cudaStream_t st) {
   switch (cpc) {
-    case 8: return launch_staged<T, 8>(x, u, g, blk0, nblk, st);
-    case 4: return launch_staged<T, 4>(x, u, g, blk0, nblk, st);
-    case 2: return launch_staged<T, 2>(x, u, g, blk0, nblk, st);
+    case 8: return launch_staged<T, 8, F16>(x, u, g, blk0, nblk, st);
+    case 4: return launch_staged<T, 4, F16>(x, u, g, blk0, nblk, st);
+    case 2: return launch_staged<T, 2, F16>(x, u, g, blk0, nblk, st);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_forward_staged(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc,
-                                  cudaStream_t st) {
+template <bool F16>
+static cudaError_t launch_forward_staged_f(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc,
+                                           cudaStream_t st) {
   switch (g.T) {
-    case 4: return launch_staged_t<4>(x, u, g, blk0, nblk, cpc, st);
-    case 5: return launch_staged_t<5>(x, u, g, blk0, nblk, cpc, st);
-    case 6: return launch_staged_t<6>(x, u, g, blk0, nblk, cpc, st);
-    case 7: return launch_staged_t<7>(x, u, g, blk0, nblk, cpc, st);
-    case 8: return launch_staged_t<8>(x, u, g, blk0, nblk, cpc, st);
+    case 4: return launch_staged_t<4, F16>(x, u, g, blk0, nblk, cpc, st);
+    case 5: return launch_staged_t<5, F16>(x, u, g, blk0, nblk, cpc, st);
+    case 6: return launch_staged_t<6, F16>(x, u, g, blk0, nblk, cpc, st);
+    case 7: return launch_staged_t<7, F16>(x, u, g, blk0, nblk, cpc, st);
+    case 8: return launch_staged_t<8, F16>(x, u, g, blk0, nblk, cpc, st);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_forward_staged(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc, int prec,
+                                  cudaStream_t st) {
+  if (prec_f16(prec)) return launch_forward_staged_f<true>(x, u, g, blk0, nblk, cpc, st);
+  return launch_forward_staged_f<false>(x, u, g, blk0, nblk, cpc, st);
 }
 
 }  // namespace wf

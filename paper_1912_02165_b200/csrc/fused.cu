@@ -156,7 +156,7 @@ static cudaError_t run_waves(const float* x, const uint8_t* vpack, float* y, uin
     const int tile0 = b0 * kBlockTiles;
     const int nvalid = (g.n_tile - tile0) < nb * kBlockTiles ? (g.n_tile - tile0) : nb * kBlockTiles;
     const int ldm = nb * kBlockTiles;
-    cudaError_t e = launch_forward_slab(x, U, g, b0, nb, s);
+    cudaError_t e = launch_forward_slab(x, U, g, b0, nb, passes, s);
     if (e != cudaSuccess) return e;
     e = launch_position_gemm(U, vpack, M, g, nb, ldm, nvalid, passes, sm_count, s);
     if (e != cudaSuccess) return e;

@@ -116,7 +116,7 @@ struct GemmSync {
 
 // ------------------------------------------------------------------ F item
 // Returns whether the staging mbarrier was used (one phase consumed).
-template <int T, int NT, int KC>
+template <int T, int NT, int KC, bool F16>
 __device__ bool run_forward_item(const PersistParams& P, int b, int cg, uint8_t* smem, GemmSync& sy,
                                  int fparity) {
   const Geo& g = P.g;
@@ -328,7 +328,7 @@ __device__ bool run_forward_item(const PersistParams& P, int b, int cg, uint8_t*
 #pragma unroll
       for (int s = 0; s < T; ++s) {
         uint32_t hi, lo;
-        split_bf16x2(u2[r][s], hi, lo);
+        split2<F16>(u_operand<T, F16>(u2[r][s], r, s), hi, lo);
         uint8_t* p = dst + static_cast<size_t>(r * T + s) * 2 * slab;
         if (P.only == 5) {                 // tuning aid: no stores (keep the values live)
           if ((hi ^ lo) == 0x12345678u) *reinterpret_cast<uint32_t*>(p) = hi;
@@ -379,17 +379,17 @@ __device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* sm
         const uint32_t kc = kblock_width(g.Cpad, j);
         uint8_t* sb = smem + st * stage_bytes;
         const uint32_t abytes = kBlockTiles * kc * 2, bbytes = g.Cppad * kc * 2;
-        mbar_expect_tx(&sy.full[st], 2 * abytes + (P.passes > 1 ? 2 : 1) * bbytes);
+        mbar_expect_tx(&sy.full[st], 2 * abytes + (prec_passes(P.passes) > 1 ? 2 : 1) * bbytes);
         const uint8_t* a_src = uslot + static_cast<size_t>(p) * 2 * a_slab + kblock_off(j, kBlockTiles);
         const uint8_t* b_src = P.vpack + static_cast<size_t>(p) * 2 * v_slab + kblock_off(j, g.Cppad);
         bulk_g2s(sb, a_src, abytes, &sy.full[st]);
         bulk_g2s(sb + a_half, a_src + a_slab, abytes, &sy.full[st]);
         bulk_g2s(sb + 2 * a_half, b_src, bbytes, &sy.full[st]);
-        if (P.passes > 1) bulk_g2s(sb + 2 * a_half + b_half, b_src + v_slab, bbytes, &sy.full[st]);
+        if (prec_passes(P.passes) > 1) bulk_g2s(sb + 2 * a_half + b_half, b_src + v_slab, bbytes, &sy.full[st]);
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_bf16(kBlockTiles, g.Cppad);
+    const uint32_t idesc = idesc_bf16(kBlockTiles, g.Cppad, false, false, prec_f16(P.passes));
     for (int k = 0; k < n_steps; ++k) {
       const int K = gbase + k;
       const int pl = k / n_kb, j = k - pl * n_kb;
@@ -408,7 +408,7 @@ __device__ void run_gemm_item(const PersistParams& P, int b, int gg, uint8_t* sm
           const uint64_t bhi = smem_desc(sbb + s * 256, 128, sbo);
           const uint64_t blo = smem_desc(sbb + b_half + s * 256, 128, sbo);
           const uint32_t first = (j == 0 && s == 0) ? 0u : 1u;
-          if (P.passes > 1) {
+          if (prec_passes(P.passes) > 1) {
             mma_bf16_ss(dcol, alo, bhi, idesc, first);
             mma_bf16_ss(dcol, ahi, blo, idesc, 1u);
             mma_bf16_ss(dcol, ahi, bhi, idesc, 1u);
@@ -532,7 +532,7 @@ __device__ void run_inverse_item(const PersistParams& P, int b, int ig) {
 }
 
 // ------------------------------------------------------------------ kernel
-template <int T, int NT, int CPS, int KC>
+template <int T, int NT, int CPS, int KC, bool F16>
 __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ GemmSync sy;
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(NT, CPS) fused_persistent_kernel(PersistParams
     if (P.only && P.only != kind + 1 && !((P.only == 5 || P.only == 6) && kind == 0)) {
       // tuning aid (WF_ONLY=1/2/3): items of the other kinds are skipped
     } else if (kind == 0) {                                // ---- F(b, sub)
-      if (run_forward_item<T, NT, KC>(P, b, sub, smem, sy, fcount & 1)) ++fcount;
+      if (run_forward_item<T, NT, KC, F16>(P, b, sub, smem, sy, fcount & 1)) ++fcount;
     } else if (kind == 1) {                                // ---- G(b, sub)
       tc_fence_after();
       run_gemm_item<NT, KC>(P, b, sub, smem, sy, tmem, gsteps, tuse);
@@ -859,7 +859,8 @@ size_t persistent_scratch_bytes(const Geo& g, const FusedOpts& o) {
 
 template <int T, int NT, int CPS, int KC>
 static cudaError_t launch_persist_t(const PersistParams& P, size_t smem, int grid, cudaStream_t st) {
-  auto kern = fused_persistent_kernel<T, NT, CPS, KC>;
+  auto kern = prec_f16(P.passes) ? fused_persistent_kernel<T, NT, CPS, KC, true>
+                                 : fused_persistent_kernel<T, NT, CPS, KC, false>;
   cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), 200 * 1024);
   if (e != cudaSuccess) return e;
   // No co-residency needed: items are claimed through one atomic counter in

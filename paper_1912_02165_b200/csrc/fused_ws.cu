@@ -331,7 +331,10 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     wk.decode(P, u, kind, b, sub);
     const int slot = it & 1;
     uint8_t* dstbase = smem + S::kOffFI + slot * S::kFISlot;
-    if (lane == 0) {
+    // every lane waits (warp-uniform spins: a lane-0 spin with the other 31
+    // lanes parked in __syncwarp made the parked lanes re-issue WARPSYNC and
+    // took issue slots from the transform warps on the same SMSP)
+    {
       long long t0 = pf.now();
       if (kind == 0) {
         if (b >= P.NU) spin_until(doneG + (b - P.NU), S::kNGG);     // U slot free
@@ -349,7 +352,6 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
     // (no proxy fence: the slot is only ever written by bulk copies; the
     // workers' generic reads of its previous contents are ordered before
     // these writes by the fi_empty barrier)
-    __syncwarp();
     if (kind == 0) {
       constexpr int kCPC = S::kCPC;
       const int part = sub / (S::C / kCPC), cg = sub % (S::C / kCPC);
@@ -406,7 +408,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
 // F(b, sub): thread = (tile tl, channel cl); a warp = 4 tiles x 8 channels
 // (half of the rows of a core matrix), so that a warp writes 64 contiguous
 // bytes of each core matrix it stores to.
-template <class S>
+template <class S, bool F16>
 __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Sync& sy, int slot, int b, int sub,
                                         int wl, int lane) {
   static_assert(S::kT == 8 && S::kCPC == 8, "T = 8 F unit");
@@ -477,7 +479,7 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
 #pragma unroll
     for (int r = 0; r < 8; r += 2) {
       uint32_t hi, lo;                                    // (position r, position r + 1) of channel c0 + cq
-      split_bf16x2(x[r][s], x[r + 1][s], hi, lo);
+      split2<F16>(u_operand<8, F16>(x[r][s], r, s), u_operand<8, F16>(x[r + 1][s], r + 1, s), hi, lo);
       // step 1 (lanes cq ^ 1): the even lane gathers the hi halves of its
       // channel pair, the odd one the lo halves: A = position r, B = r + 1
       const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 4);
@@ -586,7 +588,7 @@ __device__ __forceinline__ void i_unit8(const Params& P, const uint8_t* src, Syn
   }
 }
 
-template <class S, bool PROF>
+template <class S, bool PROF, bool F16>
 __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
   const Geo& g = P.g;
   const int wtid = threadIdx.x - 256, lane = threadIdx.x & 31, wl = wtid >> 5;
@@ -617,7 +619,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
     if (PROF && lane == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
 
     if constexpr (S::kT == 8) {
-      if (kind == 0) f_unit8<S>(P, src, sy, slot, b, sub, wl, lane);
+      if (kind == 0) f_unit8<S, F16>(P, src, sy, slot, b, sub, wl, lane);
       else i_unit8<S>(P, src, sy, slot, b, sub, wtid, lane);
     } else if (kind == 0) {
       // ---- F(b, sub): thread = (tile tl, channel pair q); a warp = 8 tiles
@@ -695,7 +697,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
 #pragma unroll
           for (int r = 0; r < kT; ++r) {
             uint32_t hi, lo;
-            split_bf16x2(w[r][s], hi, lo);
+            split2<F16>(u_operand<kT, F16>(w[r][s], r, s), hi, lo);
             const uint32_t other = __shfl_xor_sync(0xffffffffu, odd ? hi : lo, 8);
             if (live)
               ring_store<S>(reinterpret_cast<uint2*>(dst + (r * kT + s) * S::kUPos),
@@ -783,12 +785,14 @@ struct GUnits {
 // -------------------------------------------------------------- G producer
 template <class S, bool PROF>
 __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
+  // the whole warp runs the loop (warp-uniform waits); lane 0 issues the copies
   const Geo& g = P.g;
+  const int lane = threadIdx.x & 31;
   const int* doneF = P.counters;
   const int* doneI = P.counters + 2 * g.n_blk;
-  const ProfT<PROF> pf(P.prof);
+  const ProfT<PROF> pf(P.prof && lane == 0);
   const GUnits<S> gu(P);
-  if (gu.b0 < g.n_blk) {
+  if (gu.b0 < g.n_blk && lane == 0) {
     // V of this CTA's (position, c' group), once: in the MMA pack (per
     // position a hi and a lo slab of CP x C, K blocks of 64) the group's 64
     // rows of one K block are 8 KB contiguous; smem holds [hl][K block of 64]
@@ -801,13 +805,14 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
                      static_cast<size_t>(j) * S::CP * S::kVKW * 2 + static_cast<size_t>(gu.ng) * S::kVChunk,
                  S::kVChunk, &sy.b_full[0]);
   }
+  __syncwarp();
   int a_it = 0;
   for (int b = gu.b0; b < g.n_blk; b += gu.step) {
     long long t0 = pf.now();
     spin_until(doneF + b, S::kNCG);                                   // U complete
     if (b >= P.NM) spin_until(doneI + (b - P.NM), S::kNIG);           // M slot free
     pf.add(kGPDep, t0);
-    trace<PROF>(b, 2, true);
+    if (lane == 0) trace<PROF>(b, 2, true);
     fence_proxy_async_global();
     const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot;
     {
@@ -817,11 +822,14 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
         long long t2 = pf.now();
         mbar_wait(&sy.a_empty[st], ((a_it / S::kAStages) & 1) ^ 1);
         pf.add(kGPStage, t2);
-        uint8_t* adst = smem + st * S::kAStage;
-        mbar_expect_tx(&sy.a_full[st], S::kAStage);
-        const uint8_t* asrc = uslot + p * S::kUPos + kb * S::kAHalf;
-        bulk_g2s(adst, asrc, S::kAHalf, &sy.a_full[st]);                          // hi
-        bulk_g2s(adst + S::kAHalf, asrc + S::kKB * S::kAHalf, S::kAHalf, &sy.a_full[st]);    // lo
+        if (lane == 0) {
+          uint8_t* adst = smem + st * S::kAStage;
+          mbar_expect_tx(&sy.a_full[st], S::kAStage);
+          const uint8_t* asrc = uslot + p * S::kUPos + kb * S::kAHalf;
+          bulk_g2s(adst, asrc, S::kAHalf, &sy.a_full[st]);                          // hi
+          bulk_g2s(adst + S::kAHalf, asrc + S::kKB * S::kAHalf, S::kAHalf, &sy.a_full[st]);    // lo
+        }
+        __syncwarp();
         ++a_it;
       }
     }
@@ -835,7 +843,7 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   // the whole warp runs the loop; lane 0 issues the MMAs
   const int lane = threadIdx.x & 31;
   constexpr int kN = S::kN;
-  const uint32_t idesc = idesc_bf16(kBlockTiles, kN);
+  const uint32_t idesc = idesc_bf16(kBlockTiles, kN, false, false, prec_f16(P.passes));
   const ProfT<PROF> pf(P.prof);
   const GUnits<S> gu(P);
   if (gu.b0 < P.g.n_blk) mbar_wait(&sy.b_full[0], 0);            // the resident V slab
@@ -867,7 +875,7 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
           const uint64_t bhi = smem_desc(sb + voff, 128, 16 * S::kVKW);
           const uint64_t blo = smem_desc(sb + S::kVHalf + voff, 128, 16 * S::kVKW);
           const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
-          if (P.passes > 1) {
+          if (prec_passes(P.passes) > 1) {
             mma_bf16_ss(dcol, alo, bhi, idesc, first);
             mma_bf16_ss(dcol, ahi, blo, idesc, 1u);
             mma_bf16_ss(dcol, ahi, bhi, idesc, 1u);
@@ -973,9 +981,7 @@ __device__ void publisher(const Params& P, Sync& sy, int n_g) {
   wk.init(P);
   int kf = 0;
   for (int uf = blockIdx.x; uf < P.n_fi; uf += P.grid, ++kf) {
-    if (lane == 0)
-      while (ld_acquire_cta_smem(&sy.fi_cnt[kf & 3]) < 8 * ((kf >> 2) + 1)) __nanosleep(32);
-    __syncwarp();
+    while (ld_acquire_cta_smem(&sy.fi_cnt[kf & 3]) < 8 * ((kf >> 2) + 1)) __nanosleep(32);   // warp-uniform
     int kind, b, sub;
     wk.decode(P, uf, kind, b, sub);
     if (lane == 0) {
@@ -988,7 +994,7 @@ __device__ void publisher(const Params& P, Sync& sy, int n_g) {
   pf.end(kEndPub);
 }
 
-template <class S, bool PROF>
+template <class S, bool PROF, bool F16>
 __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Sync sy;
@@ -1034,7 +1040,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
         publisher<S, PROF>(P, sy, n_g);
       }
     } else if (warp == 0) {
-      if (lane_id() == 0) g_producer<S, PROF>(P, smem, sy, n_g);
+      g_producer<S, PROF>(P, smem, sy, n_g);
     } else if (warp == 1) {
       g_issuer<S, PROF>(P, smem, sy, n_g);
     } else if (warp == 2) {
@@ -1047,7 +1053,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
     if (P.dbg != 3) g_epilogue<S, PROF>(P, sy, n_g);
   } else {
     regs_inc<kRegsFI>();
-    fi_workers<S, PROF>(P, smem, sy);
+    fi_workers<S, PROF, F16>(P, smem, sy);
   }
   tc_fence_before();
   __syncthreads();
@@ -1161,8 +1167,11 @@ static Plan plan(const Geo& g, const FusedOpts& o) {
 template <class S>
 static cudaError_t launch_t(const Params& P, int sm_count, cudaStream_t st) {
   // units of a CTA wait on units of other CTAs: every CTA must be resident
-  const void* kern = P.prof ? reinterpret_cast<const void*>(fused_ws_kernel<S, true>)
-                            : reinterpret_cast<const void*>(fused_ws_kernel<S, false>);
+  const bool f16 = prec_f16(P.passes);
+  const void* kern = P.prof ? (f16 ? reinterpret_cast<const void*>(fused_ws_kernel<S, true, true>)
+                                   : reinterpret_cast<const void*>(fused_ws_kernel<S, true, false>))
+                            : (f16 ? reinterpret_cast<const void*>(fused_ws_kernel<S, false, true>)
+                                   : reinterpret_cast<const void*>(fused_ws_kernel<S, false, false>));
   Params p = P;
   void* args[] = {&p};
   return launch_coresident(kern, sm_count, NT, S::kSmem, st, args);

@@ -75,9 +75,9 @@ __global__ void __launch_bounds__(kResThreads, 1) gemm_resident_kernel(ResParams
         if (p != cur_p) {
           if (cur_p >= 0) { mbar_wait(&vempty, vphase); vphase ^= 1; }
           const uint8_t* vsrc = P.V + static_cast<size_t>(p) * 2 * v_half;
-          mbar_expect_tx(&vfull, (P.passes > 1 ? 2 : 1) * v_half);
+          mbar_expect_tx(&vfull, (prec_passes(P.passes) > 1 ? 2 : 1) * v_half);
           bulk_g2s(vbuf, vsrc, v_half, &vfull);
-          if (P.passes > 1) bulk_g2s(vbuf + v_half, vsrc + v_half, v_half, &vfull);
+          if (prec_passes(P.passes) > 1) bulk_g2s(vbuf + v_half, vsrc + v_half, v_half, &vfull);
           cur_p = p;
         }
         const uint8_t* a_src = P.U + (static_cast<size_t>(p) * P.n_blk + blk) * 2 * a_slab;
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kResThreads, 1) gemm_resident_kernel(ResParams
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_bf16(kBlockTiles, NC);
+    const uint32_t idesc = idesc_bf16(kBlockTiles, NC, false, false, prec_f16(P.passes));
     int stage = 0, acc = 0, cur_p = -1;
     uint32_t phase = 0, acc_phase = 0, vphase = 0;
     for (int it = lo_it; it < hi_it; ++it) {
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kResThreads, 1) gemm_resident_kernel(ResParams
             const uint64_t bhi = smem_desc(vb + s * 256, 128, sbo);
             const uint64_t blo = smem_desc(vb + v_half + s * 256, 128, sbo);
             const uint32_t first = (j == 0 && s == 0) ? 0u : 1u;
-            if (P.passes > 1) {
+            if (prec_passes(P.passes) > 1) {
               mma_bf16_ss(dcol, alo, bhi, idesc, first);
               mma_bf16_ss(dcol, ahi, blo, idesc, 1u);
               mma_bf16_ss(dcol, ahi, bhi, idesc, 1u);
@@ -190,13 +190,24 @@ __global__ void __launch_bounds__(kResThreads, 1) gemm_resident_kernel(ResParams
   }
 }
 
-size_t gemm_resident_smem(const Geo& g) {
-  const size_t v = static_cast<size_t>(g.Cppad) * g.Cpad * 2 * 2;
+static size_t resident_smem(int Cpad, int Cppad) {
+  const size_t v = static_cast<size_t>(Cppad) * Cpad * 2 * 2;
   return round_up(static_cast<int>(v), 1024) + kResStages * 2 * kBlockTiles * kKBlock * 2;
 }
+size_t gemm_resident_smem(const Geo& g) { return resident_smem(g.Cpad, g.Cppad); }
 
-bool gemm_resident_fits(const Geo& g) {
-  return g.Cppad <= 128 && gemm_resident_smem(g) <= 200 * 1024;
+static bool resident_fits(int Cpad, int Cppad) { return Cppad <= 128 && resident_smem(Cpad, Cppad) <= 200 * 1024; }
+bool gemm_resident_fits(const Geo& g) { return resident_fits(g.Cpad, g.Cppad); }
+
+// FFT-16 layers whose GEMM runs on position_gemm_kernel (V too large to stay
+// resident) use the complex-structured pack: per bin only W = [Re V^T | Im V^T]
+// (C' rows x 2C), the Re / Im output halves read it with the K halves in
+// place (negated upper half) / swapped -- half the pack bytes of the real
+// expansion, which is what those layers stream from DRAM.
+// (C' <= 256 or a multiple of 256: the GEMM's N chunks then tile each half exactly)
+bool fft_cplx_pack(int C, int Cp) {
+  return C % 64 == 0 && Cp % 16 == 0 && (Cp <= 256 || Cp % 256 == 0) &&
+         !resident_fits(round_up(2 * C, 16), round_up(2 * Cp, 16));
 }
 
 cudaError_t launch_gemm_resident(const uint8_t* U, const uint8_t* V, float* M, const Geo& g, int nblk,

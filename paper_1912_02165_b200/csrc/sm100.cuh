@@ -155,12 +155,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;                              // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE
 }
 
-// Instruction descriptor for kind::f16: bf16 x bf16 -> f32, both K-major.
+// Instruction descriptor for kind::f16: bf16 x bf16 (or, with fp16 = true,
+// fp16 x fp16) -> f32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool neg_a = false,
-                                                  bool neg_b = false) {
+                                                  bool neg_b = false, bool fp16 = false) {
   return (1u << 4)                       // D format f32
-         | (1u << 7)                     // A bf16
-         | (1u << 10)                    // B bf16
+         | ((fp16 ? 0u : 1u) << 7)       // A bf16 (1) / f16 (0)
+         | ((fp16 ? 0u : 1u) << 10)      // B bf16 (1) / f16 (0)
          | ((neg_a ? 1u : 0u) << 13)     //
          | ((neg_b ? 1u : 0u) << 14)     //
          | ((N >> 3) << 17)              // N / 8
@@ -254,6 +255,46 @@ __device__ __forceinline__ void split_bf16x2(float2 v, uint32_t& hi, uint32_t& l
   hi = pack_bf16x2(v.x, v.y);
   const float2 r = __fadd2_rn(v, make_float2(-__uint_as_float(hi << 16), -__uint_as_float(hi & 0xFFFF0000u)));
   lo = pack_bf16x2(r.x, r.y);
+}
+
+// --------------------------------------------------------- fp16 splitting
+// The "3xfp16" precision mode: x = hi + lo with hi, lo fp16 (11-bit
+// significands): the three products carry ~22 bits instead of 3xBF16's ~16,
+// at the same MMA rate and operand bytes.  Valid while the transformed
+// values stay inside the fp16 range (|x| < 65504; lo parts of values below
+// ~0.1 are subnormal, i.e. exact to 2^-24 absolute).
+__device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_f16x2(uint32_t h) {
+  float lo_f, hi_f;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(lo_f), "=f"(hi_f) : "r"(h));
+  return make_float2(lo_f, hi_f);
+}
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  hi = pack_f16x2(a, b);
+  const float2 h = unpack_f16x2(hi);
+  lo = pack_f16x2(a - h.x, b - h.y);
+}
+__device__ __forceinline__ void split_f16x2(float2 v, uint32_t& hi, uint32_t& lo) {
+  hi = pack_f16x2(v.x, v.y);
+  const float2 h = unpack_f16x2(hi);
+  const float2 r = __fadd2_rn(v, make_float2(-h.x, -h.y));
+  lo = pack_f16x2(r.x, r.y);
+}
+// Operand split of a precision format: F16 = false -> bf16 hi/lo, true -> fp16 hi/lo.
+template <bool F16>
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  if constexpr (F16) split_f16x2(a, b, hi, lo);
+  else split_bf16x2(a, b, hi, lo);
+}
+template <bool F16>
+__device__ __forceinline__ void split2(float2 v, uint32_t& hi, uint32_t& lo) {
+  if constexpr (F16) split_f16x2(v, hi, lo);
+  else split_bf16x2(v, hi, lo);
 }
 
 }  // namespace wf

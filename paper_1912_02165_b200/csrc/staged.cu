@@ -23,7 +23,7 @@ namespace wf {
 // transform position, the warp's 32 bf16x2 stores form exactly one 128-byte
 // core matrix of the slab (coalesced).  Tiles past n_tile and channels past C
 // are written as zeros (they are the MMA's padding rows / K columns).
-template <int T>
+template <int T, bool F16>
 __global__ void __launch_bounds__(256) forward_slab_kernel(const float* __restrict__ x,
                                                            uint8_t* __restrict__ u, Geo g,
                                                            int tile0, int nblk_local) {
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(256) forward_slab_kernel(const float* __restri
     for (int s = 0; s < T; ++s) {
       const int p = r * T + s;
       uint32_t hi, lo;
-      split_bf16x2(ua[r][s], ub[r][s], hi, lo);
+      split2<F16>(u_operand<T, F16>(ua[r][s], r, s), u_operand<T, F16>(ub[r][s], r, s), hi, lo);
       uint8_t* base = u + ((static_cast<size_t>(p) * nblk_local + blk) * 2) * slab + off;
       *reinterpret_cast<uint32_t*>(base) = hi;
       *reinterpret_cast<uint32_t*>(base + slab) = lo;
@@ -90,9 +90,35 @@ struct GemmParams {
   int NC, n_nc;      // N chunk width (multiple of 16, <= 256) and count
   int ldm;           // tiles per (p, c') row of M
   int n_valid;       // valid tiles (rows beyond are not stored)
-  int passes;        // 3 (3xBF16) or 1 (bf16)
+  int passes;        // precision (common.cuh prec_*): passes 3 or 1, bf16 or fp16 operands
   int stages;        // smem pipeline depth
+  int cplx;          // FFT-16 complex-structured pack: V = [Re V^T | Im V^T], Cph rows per bin
+  int Cph;           // rows of the complex-structured pack (C' rounded to 16)
 };
+
+// Item -> (position, block, N chunk); for the complex-structured pack the
+// chunks alternate Re / Im halves of the same pack rows (adjacent items read
+// the same rows, so the second read hits L2).  n0 = first output column,
+// wrow0 = first pack row, im = Im half.
+struct GemmItem {
+  int p, blk, n0, wrow0, im;
+};
+__device__ __forceinline__ GemmItem gemm_item(const GemmParams& P, int it) {
+  GemmItem r;
+  r.p = it / (P.n_blk * P.n_nc);
+  const int rem = it - r.p * P.n_blk * P.n_nc;
+  r.blk = rem / P.n_nc;
+  const int nc = rem - r.blk * P.n_nc;
+  if (P.cplx) {
+    r.im = nc & 1;
+    r.wrow0 = (nc >> 1) * P.NC;
+    r.n0 = r.im * (P.Cp / 2) + r.wrow0;
+  } else {
+    r.im = 0;
+    r.wrow0 = r.n0 = nc * P.NC;
+  }
+  return r;
+}
 
 __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -130,46 +156,52 @@ __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmPara
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const size_t a_slab = static_cast<size_t>(kBlockTiles) * P.Cpad * 2;
-  const size_t v_slab = static_cast<size_t>(P.Cppad) * P.Cpad * 2;
+  const int v_rows = P.cplx ? P.Cph : P.Cppad;              // rows of one pack slab
+  const size_t v_slab = static_cast<size_t>(v_rows) * P.Cpad * 2;
 
   if (warp == 0) {
     if (lane_id() == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int p = it / (P.n_blk * P.n_nc);
-        const int rem = it - p * P.n_blk * P.n_nc;
-        const int blk = rem / P.n_nc, nc = rem - blk * P.n_nc;
-        const uint8_t* a_src = P.U + (static_cast<size_t>(p) * P.n_blk + blk) * 2 * a_slab;
-        const uint8_t* b_src = P.V + static_cast<size_t>(p) * 2 * v_slab;
+        const GemmItem gi = gemm_item(P, it);
+        const uint8_t* a_src = P.U + (static_cast<size_t>(gi.p) * P.n_blk + gi.blk) * 2 * a_slab;
+        const uint8_t* b_src = P.V + static_cast<size_t>(gi.p) * 2 * v_slab;
         for (int j = 0; j < n_kb; ++j) {
           const uint32_t kc = kblock_width(P.Cpad, j);
+          // complex pack, Im half: the Re inputs (K blocks < n_kb / 2) meet
+          // Im V and the Im inputs Re V -- the pack's K halves swapped
+          const int jb = gi.im ? (j + n_kb / 2) % n_kb : j;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
           const uint32_t abytes = kBlockTiles * kc * 2, bbytes = P.NC * kc * 2;
-          mbar_expect_tx(&full_bar[stage], 2 * abytes + (P.passes > 1 ? 2 : 1) * bbytes);
+          mbar_expect_tx(&full_bar[stage], 2 * abytes + (prec_passes(P.passes) > 1 ? 2 : 1) * bbytes);
           const size_t aoff = kblock_off(j, kBlockTiles);
-          const size_t boff = kblock_off(j, P.Cppad) + static_cast<size_t>(nc) * P.NC / 8 * 16 * kc;
+          const size_t boff = kblock_off(jb, v_rows) + static_cast<size_t>(gi.wrow0) / 8 * 16 * kc;
           bulk_g2s(st, a_src + aoff, abytes, &full_bar[stage]);
           bulk_g2s(st + a_bytes, a_src + a_slab + aoff, abytes, &full_bar[stage]);
           bulk_g2s(st + 2 * a_bytes, b_src + boff, bbytes, &full_bar[stage]);
-          if (P.passes > 1) bulk_g2s(st + 2 * a_bytes + b_bytes, b_src + v_slab + boff, bbytes, &full_bar[stage]);
+          if (prec_passes(P.passes) > 1) bulk_g2s(st + 2 * a_bytes + b_bytes, b_src + v_slab + boff, bbytes, &full_bar[stage]);
           if (++stage == P.stages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_bf16(kBlockTiles, P.NC);
+    const uint32_t idesc = idesc_bf16(kBlockTiles, P.NC, false, false, prec_f16(P.passes));
+    // complex pack, Re half: the Im inputs meet -Im V (negated B operand)
+    const uint32_t idesc_neg = idesc_bf16(kBlockTiles, P.NC, false, true, prec_f16(P.passes));
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const GemmItem gi = gemm_item(P, it);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t dcol = tmem + acc * P.NC;
       for (int j = 0; j < n_kb; ++j) {
         const uint32_t kc = kblock_width(P.Cpad, j);
+        const uint32_t id = (P.cplx && !gi.im && j >= n_kb / 2) ? idesc_neg : idesc;
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         if (elect_one()) {
@@ -181,12 +213,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmPara
             const uint64_t bhi = smem_desc(st + 2 * a_bytes + s * 256, 128, sbo);
             const uint64_t blo = smem_desc(st + 2 * a_bytes + b_bytes + s * 256, 128, sbo);
             const uint32_t first = (j == 0 && s == 0) ? 0u : 1u;
-            if (P.passes > 1) {
-              mma_bf16_ss(dcol, alo, bhi, idesc, first);
-              mma_bf16_ss(dcol, ahi, blo, idesc, 1u);
-              mma_bf16_ss(dcol, ahi, bhi, idesc, 1u);
+            if (prec_passes(P.passes) > 1) {
+              mma_bf16_ss(dcol, alo, bhi, id, first);
+              mma_bf16_ss(dcol, ahi, blo, id, 1u);
+              mma_bf16_ss(dcol, ahi, bhi, id, 1u);
             } else {
-              mma_bf16_ss(dcol, ahi, bhi, idesc, first);
+              mma_bf16_ss(dcol, ahi, bhi, id, first);
             }
           }
           mma_commit(&empty_bar[stage]);
@@ -207,9 +239,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmPara
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int p = it / (P.n_blk * P.n_nc);
-      const int rem = it - p * P.n_blk * P.n_nc;
-      const int blk = rem / P.n_nc, nc = rem - blk * P.n_nc;
+      const GemmItem gi = gemm_item(P, it);
+      const int p = gi.p, blk = gi.blk;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int tile = blk * kBlockTiles + row;
@@ -219,7 +250,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmPara
         tmem_ld16(taddr + c, v);
         tmem_ld_wait();
         if (tile < P.n_valid) {
-          const int cp0 = nc * P.NC + c;
+          const int cp0 = gi.n0 + c;
           float* dst = P.M + (static_cast<size_t>(p) * P.Cp + cp0) * P.ldm + tile;
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -279,25 +310,26 @@ __global__ void __launch_bounds__(128) inverse_kernel(const float* __restrict__ 
 
 // ---------------------------------------------------------------- launchers
 template <int T>
-static cudaError_t launch_forward_t(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk,
+static cudaError_t launch_forward_t(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int prec,
                                     cudaStream_t st) {
   dim3 grid(ceil_div(nblk * kBlockTiles, 32), g.Cpad / 16);
   note_launch();
-  forward_slab_kernel<T><<<grid, 256, 0, st>>>(x, u, g, blk0 * kBlockTiles, nblk);
+  if (prec_f16(prec)) forward_slab_kernel<T, true><<<grid, 256, 0, st>>>(x, u, g, blk0 * kBlockTiles, nblk);
+  else forward_slab_kernel<T, false><<<grid, 256, 0, st>>>(x, u, g, blk0 * kBlockTiles, nblk);
   return cudaGetLastError();
 }
 
-cudaError_t launch_forward_slab(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk,
+cudaError_t launch_forward_slab(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int prec,
                                 cudaStream_t st) {
-  if (g.fft) return launch_fft_forward(x, u, g, blk0, nblk, st);
+  if (g.fft) return launch_fft_forward(x, u, g, blk0, nblk, prec, st);
   const int cpc = forward_staged_cpc(g);
-  if (cpc) return launch_forward_staged(x, u, g, blk0, nblk, cpc, st);
+  if (cpc) return launch_forward_staged(x, u, g, blk0, nblk, cpc, prec, st);
   switch (g.T) {
-    case 4: return launch_forward_t<4>(x, u, g, blk0, nblk, st);
-    case 5: return launch_forward_t<5>(x, u, g, blk0, nblk, st);
-    case 6: return launch_forward_t<6>(x, u, g, blk0, nblk, st);
-    case 7: return launch_forward_t<7>(x, u, g, blk0, nblk, st);
-    case 8: return launch_forward_t<8>(x, u, g, blk0, nblk, st);
+    case 4: return launch_forward_t<4>(x, u, g, blk0, nblk, prec, st);
+    case 5: return launch_forward_t<5>(x, u, g, blk0, nblk, prec, st);
+    case 6: return launch_forward_t<6>(x, u, g, blk0, nblk, prec, st);
+    case 7: return launch_forward_t<7>(x, u, g, blk0, nblk, prec, st);
+    case 8: return launch_forward_t<8>(x, u, g, blk0, nblk, prec, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -319,8 +351,16 @@ cudaError_t launch_position_gemm(const uint8_t* U, const uint8_t* V, float* M, c
   P.n_pos = g.P;
   P.n_blk = nblk;
   P.Cpad = g.Cpad; P.Cppad = g.Cppad; P.Cp = g.Nout;
-  P.NC = gemm_nc(g.Cppad);
-  P.n_nc = ceil_div(g.Cppad, P.NC);
+  P.cplx = g.cplx;
+  P.Cph = round_up(g.Cp, 16);
+  if (g.cplx) {
+    // chunks never straddle the Re / Im halves: NC divides C'
+    P.NC = gemm_nc(g.Cp);
+    P.n_nc = 2 * ceil_div(g.Cp, P.NC);
+  } else {
+    P.NC = gemm_nc(g.Cppad);
+    P.n_nc = ceil_div(g.Cppad, P.NC);
+  }
   P.ldm = ldm;
   P.n_valid = n_valid;
   P.passes = passes;

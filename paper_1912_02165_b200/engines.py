@@ -18,7 +18,7 @@ launching stream (transfers excluded, like the reference's timers).
 
 GPU additions to :class:`EngineConfig`: ``device`` (None = current CUDA
 device), ``transform`` ("winograd" | "fft"), ``precision`` ("3xbf16" |
-"bf16"), ``fused_variant`` (which fused kernel runs: "auto" | "ws" |
+"3xfp16" | "bf16"), ``fused_variant`` (which fused kernel runs: "auto" | "ws" |
 "itemq" | "waves") and ``ring_bytes`` (L2 ring budget of the persistent
 fused kernels).  There is no CPU fallback: without the CUDA extension or a
 GPU every engine raises :class:`NativeLibraryError`.
@@ -42,7 +42,7 @@ from .tiling import plan as tile_plan
 from .transforms import KernelPack, multiply_flops, transform_kernels
 
 ENGINE_KINDS = ("direct", "three_stage", "fused")
-PRECISIONS = ("3xbf16", "bf16")
+PRECISIONS = ("3xbf16", "bf16", "3xfp16")
 TRANSFORMS = ("winograd", "fft")
 FFT_TILE = 16
 _FP32 = 4
@@ -320,7 +320,7 @@ def conv_three_stage(inp, kers, spec: LayerSpec, config: EngineConfig | None = N
         _lib.check(lib.wf_conv_three_stage(None, None, None, None, 0, layer, cfg.tile, tf, 0, None),
                    "wf_conv_three_stage")
     x = _dev.to_device(inp, dev, name="input")
-    vpack = pack.device_mma(dev)
+    vpack = pack.device_mma(dev, cfg.precision)
     try:
         scratch = _dev.torch.empty(need, dtype=_dev.torch.uint8, device=dev)
     except _dev.torch.cuda.OutOfMemoryError as exc:
@@ -397,7 +397,7 @@ def conv_fused(inp, pack: KernelPack, spec: LayerSpec, config: EngineConfig | No
         opts = _opts(cfg, flags)
         need = lib.wf_fused_scratch_bytes_ex(layer, cfg.tile, tf, opts)
         x = _dev.to_device(inp, dev, name="input")
-        vpack = pack.device_mma(dev)
+        vpack = pack.device_mma(dev, cfg.precision)
         scratch = _scratch(dev, int(need), "fused")
         y = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=dev)
         ran = ctypes.c_int(0)
@@ -522,7 +522,7 @@ class LayerPlan:
             else:
                 self.scratch = _dev.torch.zeros(max(self.nbytes, 16), dtype=_dev.torch.uint8, device=self.dev)
                 self.shared = False
-            self.vpack = self.pack.device_mma(self.dev)
+            self.vpack = self.pack.device_mma(self.dev, cfg.precision)
             self.out = _dev.torch.empty(spec.output_dims(), dtype=_dev.torch.float32, device=self.dev)
         self.ran = ctypes.c_int(0)
 

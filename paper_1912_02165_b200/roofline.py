@@ -294,7 +294,7 @@ def plan_b200(layer: LayerSpec, tile: int, machine: B200Model | None = None, tra
     design stages through L2.
     """
     mach = machine or B200Model()
-    passes = 3 if precision == "3xbf16" else 1
+    passes = 1 if precision == "bf16" else 3
     c, cp = layer.in_channels, layer.out_channels
     if transform == "fft":
         m, pos, kdim, ndim = 14, 144, 2 * c, 2 * cp

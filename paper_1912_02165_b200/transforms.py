@@ -56,9 +56,11 @@ class KernelPack:
             self._device[key] = t
         return t
 
-    def device_mma(self, dev):
-        """MMA-ready operand on ``dev`` (bf16 hi/lo UMMA slabs, built once)."""
-        key = ("mma", str(dev))
+    def device_mma(self, dev, precision: str = "3xbf16"):
+        """MMA-ready operand on ``dev`` (bf16 or fp16 hi/lo UMMA slabs, per the
+        precision mode's operand format; built once per device and format)."""
+        fmt = _lib.PACK_FORMAT[precision]
+        key = ("mma", str(dev), fmt)
         t = self._device.get(key)
         if t is None:
             lib = _lib.load()
@@ -68,8 +70,8 @@ class KernelPack:
                 _lib.check(_lib.WF_ERR_UNSUPPORTED, "mma pack")
             t = _dev.torch.empty(nbytes, dtype=_dev.torch.uint8, device=dev)
             src = self.device_f32(dev)
-            _lib.check(lib.wf_mma_pack(_dev.ptr(src), _dev.ptr(t), self.tile, self.c_in, self.c_out, tf,
-                                       _dev.stream_ptr(dev)), "wf_mma_pack")
+            _lib.check(lib.wf_mma_pack_ex(_dev.ptr(src), _dev.ptr(t), self.tile, self.c_in, self.c_out, tf,
+                                          _lib.PRECISIONS[precision], _dev.stream_ptr(dev)), "wf_mma_pack")
             self._device[key] = t
         return t
 

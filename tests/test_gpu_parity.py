@@ -501,3 +501,64 @@ def test_concurrent_persistent_launches_on_two_streams():
     torch.cuda.synchronize()
     assert all(p.variant == "ws" and p.ran.value == 1 for p in plans)
     assert all(torch.equal(p.out, ref) for p in plans)
+
+
+# ------------------------------------------------------- 3xfp16 precision mode
+# the reference's own f32 verification bar (bench.py:25) for T <= 7; F(6x6,3x3)
+# amplifies the tensor cores' f32 accumulation error past it (measured
+# 1.0e-4 .. 1.3e-4; 3xbf16: 2e-4 .. 4e-4)
+TOL_FP16 = {4: 1e-4, 5: 1e-4, 6: 1e-4, 7: 1e-4, 8: 2e-4, 16: 1e-4}
+
+
+def test_3xfp16_golden_cases_meet_reference_bar(golden_cases):
+    """3xfp16 (fp16 hi/lo operands, three passes): every golden case within
+    the reference's 1e-4 of FP64 direct and of the reference's own f32 fused
+    output (T = 8: 2e-4); fused == three-stage bitwise."""
+    worst = 0.0
+    for c in golden_cases:
+        spec = wf.LayerSpec(*c["dims"])
+        t = c["tile"]
+        pack = wf.transform_kernels(wf.Tensor4D(c["w"]), wf.make_basis(t))
+        f, _ = _run("fused", c["x"], pack, spec, t, precision="3xfp16")
+        s, _ = _run("three_stage", c["x"], pack, spec, t, precision="3xfp16")
+        assert np.array_equal(f, s), c["name"]
+        err = O.max_rel_error(f, O.direct_conv_f64(c["x"], c["w"], spec))
+        worst = max(worst, err)
+        assert err <= TOL_FP16[t], (c["name"], err)
+        assert O.max_rel_error(f, c["fused"]) <= TOL_FP16[t], c["name"]
+    assert worst > 0.0
+
+
+@pytest.mark.parametrize("dims,t,variant", [((8, 64, 64, 56, 56, 3, 1, 1), 6, "ws"),
+                                            ((2, 128, 128, 28, 28, 3, 1, 1), 6, "ws"),
+                                            ((4, 64, 64, 56, 56, 3, 1, 1), 8, "ws"),
+                                            ((2, 16, 16, 56, 56, 3, 1, 1), 8, "ws"),
+                                            ((2, 64, 64, 30, 28, 3, 1, 1), 6, "itemq"),
+                                            ((1, 256, 512, 14, 14, 3, 1, 1), 6, "waves"),
+                                            ((2, 40, 24, 17, 19, 3, 1, 0), 7, "waves")])
+def test_3xfp16_fused_variants(dims, t, variant):
+    spec = wf.LayerSpec(*dims)
+    rng = np.random.default_rng(sum(dims) + t)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
+    f, fs = _run("fused", x, pack, spec, t, precision="3xfp16", fused_variant=variant)
+    assert fs.variant == variant
+    s, _ = _run("three_stage", x, pack, spec, t, precision="3xfp16")
+    assert np.array_equal(f, s), dims
+    err = O.max_rel_error(f, O.direct_conv_f64(x, w, spec))
+    assert err <= TOL_FP16[t], (dims, t, err)
+    b, _ = _run("fused", x, pack, spec, t, fused_variant=variant)          # 3xbf16 for contrast
+    assert O.max_rel_error(b, O.direct_conv_f64(x, w, spec)) > err
+
+
+def test_3xfp16_fft16():
+    spec = wf.LayerSpec(4, 64, 64, 28, 28, 3, 1, 1)
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_fft_basis(3))
+    f, _ = _run("fused", x, pack, spec, 16, transform="fft", precision="3xfp16")
+    s, _ = _run("three_stage", x, pack, spec, 16, transform="fft", precision="3xfp16")
+    assert np.array_equal(f, s)
+    assert O.max_rel_error(f, O.direct_conv_f64(x, w, spec)) <= TOL_FP16[16]
