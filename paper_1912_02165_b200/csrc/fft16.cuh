@@ -68,38 +68,93 @@ __device__ __forceinline__ void fft16(float (&re)[16], float (&im)[16]) {
   }
 }
 
-// Real 16-point forward DFT, bins 0..8 (direct form; constant twiddles fold).
+// In-place radix-2 DIT complex FFT of 8 points (sign -1 forward, +1 inverse,
+// no scaling); twiddles are the even 16th roots (compile-time constants).
+template <int SIGN>
+__device__ __forceinline__ void fft8(float (&r)[8], float (&q)[8]) {
+  float a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j = ((i & 1) << 2) | (i & 2) | ((i & 4) >> 2);
+    a[i] = r[j];
+    b[i] = q[j];
+  }
+#pragma unroll
+  for (int len = 2; len <= 8; len <<= 1) {
+    const int half = len >> 1;
+    const int step = 16 / len;
+#pragma unroll
+    for (int base = 0; base < 8; base += len)
+#pragma unroll
+      for (int k = 0; k < half; ++k) {
+        const float wr = kc(k * step);
+        const float wi = SIGN * ks(k * step);
+        const int u = base + k, v = u + half;
+        const float tr = a[v] * wr - b[v] * wi;
+        const float ti = a[v] * wi + b[v] * wr;
+        a[v] = a[u] - tr;
+        b[v] = b[u] - ti;
+        a[u] = a[u] + tr;
+        b[u] = b[u] + ti;
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    r[i] = a[i];
+    q[i] = b[i];
+  }
+}
+
+// Real 16-point forward DFT, bins 0..8: the even / odd samples as one
+// 8-point complex FFT (z[n] = x[2n] + i x[2n+1]), then the split
+// X[k] = E[k] + W16^k O[k] with E, O recovered from Z[k] and conj(Z[8-k])
+// (about half the operations of the direct 16 x 9 form).
 __device__ __forceinline__ void rfft16(const float (&x)[16], float (&re)[9], float (&im)[9]) {
+  float zr[8], zi[8];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) {
-    float sr = 0.0f, si = 0.0f;
+  for (int n = 0; n < 8; ++n) {
+    zr[n] = x[2 * n];
+    zi[n] = x[2 * n + 1];
+  }
+  fft8<-1>(zr, zi);
+  re[0] = zr[0] + zi[0];
+  im[0] = 0.0f;
+  re[8] = zr[0] - zi[0];
+  im[8] = 0.0f;
 #pragma unroll
-    for (int n = 0; n < 16; ++n) {
-      const int t = (k * n) & 15;
-      if (kc(t) != 0.0f) sr = fmaf(x[n], kc(t), sr);
-      if (ks(t) != 0.0f) si = fmaf(-x[n], ks(t), si);
-    }
-    re[k] = sr;
-    im[k] = si;
+  for (int k = 1; k < 8; ++k) {
+    const int j = 8 - k;
+    const float er = 0.5f * (zr[k] + zr[j]), ei = 0.5f * (zi[k] - zi[j]);
+    const float orr = 0.5f * (zi[k] + zi[j]), oi = 0.5f * (zr[j] - zr[k]);
+    const float c = kc(k), s = ks(k);
+    re[k] = fmaf(s, oi, fmaf(c, orr, er));
+    im[k] = fmaf(-s, orr, fmaf(c, oi, ei));
   }
 }
 
 // Inverse of rfft16 for a Hermitian spectrum given by bins 0..8 (imag parts
-// of bins 0 and 8 ignored); first NOUT outputs, no 1/16 scaling.
+// of bins 0 and 8 ignored); first NOUT outputs, no 1/16 scaling.  The 16
+// outputs come out of one 8-point complex inverse FFT of
+// Z[k] = (X[k] + conj(X[8-k])) + i (X[k] - conj(X[8-k])) e^{+2 pi i k/16}:
+// x[2n] = Re z[n], x[2n+1] = Im z[n].
 template <int NOUT>
 __device__ __forceinline__ void irfft16(const float (&re)[9], const float (&im)[9], float (&x)[NOUT]) {
+  static_assert(NOUT <= 16, "irfft16 outputs");
+  float zr[8], zi[8];
+  zr[0] = re[0] + re[8];
+  zi[0] = re[0] - re[8];
 #pragma unroll
-  for (int n = 0; n < NOUT; ++n) {
-    float s = re[0] + ((n & 1) ? -re[8] : re[8]);
-#pragma unroll
-    for (int k = 1; k < 8; ++k) {
-      const int t = (k * n) & 15;
-      // 2 * Re(X[k] e^{+i 2pi kn/16}) = 2 (re cos - im sin)
-      if (kc(t) != 0.0f) s = fmaf(2.0f * re[k], kc(t), s);
-      if (ks(t) != 0.0f) s = fmaf(-2.0f * im[k], ks(t), s);
-    }
-    x[n] = s;
+  for (int k = 1; k < 8; ++k) {
+    const int j = 8 - k;
+    const float sr = re[k] + re[j], si = im[k] - im[j];
+    const float dr = re[k] - re[j], di = im[k] + im[j];
+    const float c = kc(k), s = ks(k);
+    zr[k] = sr - fmaf(dr, s, di * c);
+    zi[k] = si + fmaf(dr, c, -di * s);
   }
+  fft8<1>(zr, zi);
+#pragma unroll
+  for (int n = 0; n < NOUT; ++n) x[n] = (n & 1) ? zi[n >> 1] : zr[n >> 1];
 }
 
 }  // namespace fft
