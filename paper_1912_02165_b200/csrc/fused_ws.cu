@@ -53,8 +53,9 @@ constexpr int kMaxAStages = 4;
 // (GEMM K, 32-channel K blocks), CP output channels (GEMM N, 64-wide G
 // units).  Shared memory: A stages + the V slab of the CTA's (position, c'
 // group) + two 72 KB F/I slots <= 227 KB.
-template <int T_, int C_, int CP_>
+template <int T_, int C_, int CP_, int SL_ = 2>
 struct Shape {
+  static constexpr int kSlots = SL_;                    // F/I staging slots (2 x 72 KB or 3 x 48 KB)
   static constexpr int kT = T_, kP = T_ * T_;
   static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
   static constexpr int kN = CP < 64 ? CP : 64;           // output channels per G unit (MMA N)
@@ -67,11 +68,11 @@ struct Shape {
   static constexpr int kFT = T_ == 6 ? 64 : 32;
   // F staging or I staging slot (two of them)
   // (C = 256, T = 6: 48 KB, room for the 64 KB V slab; 2-channel I units)
-  static constexpr uint32_t kFISlot = (T_ == 6 ? (C_ >= 256 ? 48 : 72) : 73) * 1024;
+  static constexpr uint32_t kFISlot = (SL_ == 3 ? 48 : T_ == 6 ? (C_ >= 256 ? 48 : 72) : 73) * 1024;
   // I unit: kIPairs c' pairs.  M ring slot layout: [I unit][position][c' pair
   // in unit][tile][2]: the products one I unit needs are one contiguous
   // range (72 KB for T = 6, 64 KB for T = 8) -- one bulk copy
-  static constexpr int kIPairs = (T_ == 6 && C_ < 256) ? 2 : 1;
+  static constexpr int kIPairs = (T_ == 6 && C_ < 256 && SL_ == 2) ? 2 : 1;
   static constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;
   static constexpr uint32_t kMUnit = kP * kIPos;
   static constexpr int kKBW = C < 32 ? C : 32;           // K block width (channels per A stage)
@@ -93,7 +94,7 @@ struct Shape {
   static constexpr size_t kMSlot = kP * kMPos;
   static constexpr uint32_t kOffB = kAStages * kAStage;
   static constexpr uint32_t kOffFI = kOffB + kVGroup;
-  static constexpr uint32_t kSmem = kOffFI + 2 * kFISlot;
+  static constexpr uint32_t kSmem = kOffFI + kSlots * kFISlot;
   static_assert(kSmem <= 227 * 1024 && kAStages <= kMaxAStages && C % 16 == 0 && CP % kN == 0, "shape");
   static_assert((T_ == 6 || T_ == 8) && kMUnit <= kFISlot, "window");
 };
@@ -197,7 +198,7 @@ struct Sync {
   uint64_t a_full[kMaxAStages], a_empty[kMaxAStages];
   uint64_t b_full[2], b_empty[2];
   uint64_t tfull[kNAcc][kGP], tempty[kNAcc];
-  uint64_t fi_full[2], fi_empty[2];
+  uint64_t fi_full[3], fi_empty[3];
   // completion counts: F/I unit k adds 8 (one per worker warp) to fi_cnt[k % 4],
   // G unit k adds 4 (one per epilogue warp) to g_cnt[k % kNAcc].  A warp can
   // not get a full counter ring ahead of another (the F/I slot ring and the
@@ -329,7 +330,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
   for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
     int kind, b, sub;
     wk.decode(P, u, kind, b, sub);
-    const int slot = it & 1;
+    const int slot = it % S::kSlots;
     uint8_t* dstbase = smem + S::kOffFI + slot * S::kFISlot;
     // every lane waits (warp-uniform spins: a lane-0 spin with the other 31
     // lanes parked in __syncwarp made the parked lanes re-issue WARPSYNC and
@@ -344,7 +345,7 @@ __device__ void fi_producer(const Params& P, uint8_t* smem, Sync& sy) {
       }
       pf.add(kFPDep, t0);
       t0 = pf.now();
-      mbar_wait(&sy.fi_empty[slot], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&sy.fi_empty[slot], ((it / S::kSlots) & 1) ^ 1);
       pf.add(kFPSlot, t0);
     }
 
@@ -602,10 +603,10 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
   for (int u = blockIdx.x; u < P.n_fi; u += P.grid, ++it) {
     int kind, b, sub;
     wk.decode(P, u, kind, b, sub);
-    const int slot = it & 1;
+    const int slot = it % S::kSlots;
     const uint8_t* src = smem + S::kOffFI + slot * S::kFISlot;
     long long t0 = pf.now();
-    mbar_wait(&sy.fi_full[slot], (it >> 1) & 1);
+    mbar_wait(&sy.fi_full[slot], (it / S::kSlots) & 1);
     pf.add(kFWWait, t0);
     t0 = pf.now();
     if (kind == 2 && (P.discard & 2)) {
@@ -1004,6 +1005,8 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sy.b_full[s], 1);
       mbar_init(&sy.b_empty[s], 1);
+    }
+    for (int s = 0; s < S::kSlots; ++s) {
       mbar_init(&sy.fi_full[s], 1);
       mbar_init(&sy.fi_empty[s], 8);
     }
@@ -1131,6 +1134,18 @@ static Plan plan_t(const Geo& g, const FusedOpts& o) {
   return pl;
 }
 
+template <class S>
+static bool staging_fits(const Geo& g) {
+  if (g.W % 4 != 0 || g.m != S::kT - 2 || g.pad_lo != 1 || g.W < 8) return false;
+  int max_rows = 0;
+  for (int t0 = 0; t0 < g.n_tile; t0 += S::kFT) {
+    const FGeo fg(g, t0, std::min(t0 + S::kFT, g.n_tile) - 1);
+    max_rows = std::max(max_rows, fg.total());
+  }
+  const int plane = round_up(max_rows * g.W, 32) + 16;
+  return static_cast<size_t>(S::kCPC) * plane * 4 <= S::kFISlot;
+}
+
 // Shapes with a kernel instance: T = 6 with Cpad in {64, 128} (= C) and 16
 // (C <= 16), C' (= C'pad) in {64, 128, 256}; T = 8 with C = C' in {64, 128}
 // -- every (position, c' group) pair gets a CTA of its own (T^2 x C'/64 <=
@@ -1143,7 +1158,11 @@ static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
   if (g.fft || g.Cp != g.Cppad || (g.C != g.Cpad && g.Cpad != 16)) return R();
   switch (g.T * 1000000 + g.Cpad * 1000 + g.Cp) {
     case 6016064: return f(Shape<6, 16, 64>());
-    case 6064064: return f(Shape<6, 64, 64>());
+    case 6064064:
+      // three 48 KB F/I slots (2-channel I units) when an F unit's input
+      // staging fits 48 KB (images up to ~64 wide): one more unit in flight
+      if (tuning_knob("WF_WS_SLOTS3", 1) && staging_fits<Shape<6, 64, 64, 3>>(g)) return f(Shape<6, 64, 64, 3>());
+      return f(Shape<6, 64, 64>());
     case 6064128: return f(Shape<6, 64, 128>());
     case 6064256: return f(Shape<6, 64, 256>());
     case 6128064: return f(Shape<6, 128, 64>());
