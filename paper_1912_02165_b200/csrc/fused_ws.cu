@@ -55,7 +55,9 @@ constexpr int kMaxAStages = 4;
 // group) + two 72 KB F/I slots <= 227 KB.
 template <int T_, int C_, int CP_, int SL_ = 2>
 struct Shape {
-  static constexpr int kSlots = SL_;                    // F/I staging slots (2 x 72 KB or 3 x 48 KB)
+  // F/I staging slots: 2 x 72 KB.  (3 x 48 KB with 2-channel I units was
+  // measured on c2: 98 vs 80 us -- twice the I units and a shorter lag)
+  static constexpr int kSlots = SL_;
   static constexpr int kT = T_, kP = T_ * T_;
   static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
   static constexpr int kN = CP < 64 ? CP : 64;           // output channels per G unit (MMA N)
@@ -1134,18 +1136,6 @@ static Plan plan_t(const Geo& g, const FusedOpts& o) {
   return pl;
 }
 
-template <class S>
-static bool staging_fits(const Geo& g) {
-  if (g.W % 4 != 0 || g.m != S::kT - 2 || g.pad_lo != 1 || g.W < 8) return false;
-  int max_rows = 0;
-  for (int t0 = 0; t0 < g.n_tile; t0 += S::kFT) {
-    const FGeo fg(g, t0, std::min(t0 + S::kFT, g.n_tile) - 1);
-    max_rows = std::max(max_rows, fg.total());
-  }
-  const int plane = round_up(max_rows * g.W, 32) + 16;
-  return static_cast<size_t>(S::kCPC) * plane * 4 <= S::kFISlot;
-}
-
 // Shapes with a kernel instance: T = 6 with Cpad in {64, 128} (= C) and 16
 // (C <= 16), C' (= C'pad) in {64, 128, 256}; T = 8 with C = C' in {64, 128}
 // -- every (position, c' group) pair gets a CTA of its own (T^2 x C'/64 <=
@@ -1158,11 +1148,7 @@ static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
   if (g.fft || g.Cp != g.Cppad || (g.C != g.Cpad && g.Cpad != 16)) return R();
   switch (g.T * 1000000 + g.Cpad * 1000 + g.Cp) {
     case 6016064: return f(Shape<6, 16, 64>());
-    case 6064064:
-      // three 48 KB F/I slots (2-channel I units) when an F unit's input
-      // staging fits 48 KB (images up to ~64 wide): one more unit in flight
-      if (tuning_knob("WF_WS_SLOTS3", 1) && staging_fits<Shape<6, 64, 64, 3>>(g)) return f(Shape<6, 64, 64, 3>());
-      return f(Shape<6, 64, 64>());
+    case 6064064: return f(Shape<6, 64, 64>());
     case 6064128: return f(Shape<6, 64, 128>());
     case 6064256: return f(Shape<6, 64, 256>());
     case 6128064: return f(Shape<6, 128, 64>());
