@@ -322,6 +322,8 @@ static cudaError_t launch_forward_t(const float* x, uint8_t* u, const Geo& g, in
 cudaError_t launch_forward_slab(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int prec,
                                 cudaStream_t st) {
   if (g.fft) return launch_fft_forward(x, u, g, blk0, nblk, prec, st);
+  const int pcpc = forward_pipe_cpc(g);
+  if (pcpc) return launch_forward_pipe(x, u, g, blk0, nblk, pcpc, prec, st);
   const int cpc = forward_staged_cpc(g);
   if (cpc) return launch_forward_staged(x, u, g, blk0, nblk, cpc, prec, st);
   switch (g.T) {

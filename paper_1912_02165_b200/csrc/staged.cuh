@@ -19,6 +19,9 @@ cudaError_t launch_inverse(const float* M, float* y, const Geo& g, int tile0, in
 int gemm_nc(int Cppad);
 // Shared-memory-staged forward transform (forward.cu); 0 = geometry too wide.
 int forward_staged_cpc(const Geo& g);
+int forward_pipe_cpc(const Geo& g);
+cudaError_t launch_forward_pipe(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc, int prec,
+                                cudaStream_t st);
 cudaError_t launch_forward_staged(const float* x, uint8_t* u, const Geo& g, int blk0, int nblk, int cpc,
                                   int prec, cudaStream_t st);
 
