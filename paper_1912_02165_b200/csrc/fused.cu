@@ -19,6 +19,7 @@
 #include <mutex>
 #include "fused.cuh"
 #include "staged.cuh"
+#include "gemm.cuh"
 
 namespace wf {
 
@@ -52,6 +53,8 @@ static int wave_blocks(const Geo& g) {
   const size_t nb_par = static_cast<size_t>(ceil_div(par * 148, g.P * n_nc));
   if (nb < nb_par) nb = nb_par;
   if (nb < 1) nb = 1;
+  // CTA-pair GEMM (gemm_pair.cu): whole block pairs per wave
+  if (gemm_pair_layer(g) && !gemm_resident_fits(g) && (nb & 1)) ++nb;
   if (nb > static_cast<size_t>(g.n_blk)) nb = g.n_blk;
   return static_cast<int>(nb);
 }

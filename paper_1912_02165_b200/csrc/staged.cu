@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "sm100.cuh"
 #include "staged.cuh"
+#include "gemm.cuh"
 
 namespace wf {
 
@@ -81,44 +82,6 @@ __global__ void __launch_bounds__(256) forward_slab_kernel(const float* __restri
 // 3xBF16: D = Uhi*Vhi + Uhi*Vlo + Ulo*Vhi (f32 accumulate); 1 pass for bf16.
 constexpr int kGemmThreads = 320;
 constexpr int kGemmEpiWarps = 8;
-
-struct GemmParams {
-  const uint8_t* U;  // [p][blk][hl] slabs of 128 x Cpad
-  const uint8_t* V;  // [p][hl] slabs of Cppad x Cpad
-  float* M;          // [p][c'][tile], tile stride ldm
-  int n_pos, n_blk, Cpad, Cppad, Cp;
-  int NC, n_nc;      // N chunk width (multiple of 16, <= 256) and count
-  int ldm;           // tiles per (p, c') row of M
-  int n_valid;       // valid tiles (rows beyond are not stored)
-  int passes;        // precision (common.cuh prec_*): passes 3 or 1, bf16 or fp16 operands
-  int stages;        // smem pipeline depth
-  int cplx;          // FFT-16 complex-structured pack: V = [Re V^T | Im V^T], Cph rows per bin
-  int Cph;           // rows of the complex-structured pack (C' rounded to 16)
-};
-
-// Item -> (position, block, N chunk); for the complex-structured pack the
-// chunks alternate Re / Im halves of the same pack rows (adjacent items read
-// the same rows, so the second read hits L2).  n0 = first output column,
-// wrow0 = first pack row, im = Im half.
-struct GemmItem {
-  int p, blk, n0, wrow0, im;
-};
-__device__ __forceinline__ GemmItem gemm_item(const GemmParams& P, int it) {
-  GemmItem r;
-  r.p = it / (P.n_blk * P.n_nc);
-  const int rem = it - r.p * P.n_blk * P.n_nc;
-  r.blk = rem / P.n_nc;
-  const int nc = rem - r.blk * P.n_nc;
-  if (P.cplx) {
-    r.im = nc & 1;
-    r.wrow0 = (nc >> 1) * P.NC;
-    r.n0 = r.im * (P.Cp / 2) + r.wrow0;
-  } else {
-    r.im = 0;
-    r.wrow0 = r.n0 = nc * P.NC;
-  }
-  return r;
-}
 
 __global__ void __launch_bounds__(kGemmThreads, 1) position_gemm_kernel(GemmParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -366,6 +329,11 @@ cudaError_t launch_position_gemm(const uint8_t* U, const uint8_t* V, float* M, c
   P.ldm = ldm;
   P.n_valid = n_valid;
   P.passes = passes;
+  if (gemm_pair_fits(g, nblk, P.NC, sm_count)) {
+    const cudaError_t e = launch_position_gemm_pair(P, g, sm_count, st);
+    if (e == cudaSuccess) return e;
+    (void)cudaGetLastError();   // pair launch refused (tensor map / cluster resources): one CTA per block
+  }
   const int stage_bytes = 2 * kBlockTiles * kKBlock * 2 + 2 * P.NC * kKBlock * 2;
   P.stages = 200 * 1024 / stage_bytes;
   if (P.stages > 4) P.stages = 4;
