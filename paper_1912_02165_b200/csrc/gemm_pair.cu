@@ -41,11 +41,16 @@ namespace {
 
 constexpr int kPairThreads = 320;
 constexpr int kPairEpiWarps = 8;
-constexpr int kPairMaxStages = 4;
+constexpr int kPairMaxStages = 8;
 
-// Operand buffers are addressed as 2-D tensors of 128-byte rows (64 x 16
-// bit): a full K block (64 channels) of R operand rows is R * 128 contiguous
-// bytes = R rows of the view -- one box per (operand, hl, K block).
+// Operand buffers are addressed as 3-D tensors over the K-block layout
+// (csrc/common.cuh): {64 x 16 bit = one 8-row x 8-channel core matrix row
+// group's 128 bytes, 8 channel groups of a K block, 8-row groups}.  A box of
+// {64, KS / 8, R / 8} gathers KS channels of R rows and lands in shared
+// memory as the same layout with K block width KS (SBO = 16 KS): a stage
+// holds KS channels, so KS = 32 doubles the stage count of KS = 64 for the
+// same shared memory.
+template <int KS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     position_gemm_pair_kernel(GemmParams P, int n_bp, const __grid_constant__ CUtensorMap tmA,
                               const __grid_constant__ CUtensorMap tmB) {
@@ -56,11 +61,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const int warp = threadIdx.x >> 5;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  constexpr int kSub = kKBlock / KS;                       // stages per K block
   const int n_kb = P.Cpad / kKBlock;
   const int nh = prec_passes(P.passes) > 1 ? 2 : 1;        // hl halves streamed per operand
-  const uint32_t a_bytes = kBlockTiles * kKBlock * 2;      // one hl half of this CTA's A block
+  const uint32_t a_bytes = kBlockTiles * KS * 2;           // one hl half of this CTA's A block
   const int bh = P.NC / 2;                                 // B rows staged by this CTA
-  const uint32_t b_bytes = static_cast<uint32_t>(bh) * kKBlock * 2;
+  const uint32_t b_bytes = static_cast<uint32_t>(bh) * KS * 2;
   const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
   const int n_items = P.n_pos * n_bp * P.n_nc;
   const uint32_t tcols = P.NC * 2 <= 32 ? 32 : (P.NC * 2 <= 64 ? 64 : (P.NC * 2 <= 128 ? 128 : (P.NC * 2 <= 256 ? 256 : 512)));
@@ -109,17 +115,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int blk = min(2 * gi.blk + static_cast<int>(rank), P.n_blk - 1);
         const size_t a_base = (static_cast<size_t>(gi.p) * P.n_blk + blk) * 2 * a_slab;
         const size_t b_base = static_cast<size_t>(gi.p) * 2 * v_slab;
-        for (int j = 0; j < n_kb; ++j) {
+        for (int jq = 0; jq < n_kb * kSub; ++jq) {
+          const int j = jq / kSub, kq = (jq - j * kSub) * (KS / 8);   // K block, first channel group
           const int jb = gi.im ? (j + n_kb / 2) % n_kb : j;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
           if (rank == 0) mbar_expect_tx(&full_bar[stage], 2 * nh * (a_bytes + b_bytes));
+          // 8-row group indices (1 KB each) of the A block / B half rows
           const size_t aoff = a_base + kblock_off(j, kBlockTiles);
           const size_t boff = b_base + kblock_off(jb, v_rows) +
                               static_cast<size_t>(gi.wrow0 + static_cast<int>(rank) * bh) / 8 * 16 * kKBlock;
           for (int h = 0; h < nh; ++h) {
-            tma_load_2d_pair(st + h * a_bytes, &tmA, 0, static_cast<int>((aoff + h * a_slab) >> 7), full_c[stage]);
-            tma_load_2d_pair(st + 2 * a_bytes + h * b_bytes, &tmB, 0, static_cast<int>((boff + h * v_slab) >> 7),
+            tma_load_3d_pair(st + h * a_bytes, &tmA, 0, kq, static_cast<int>((aoff + h * a_slab) >> 10), full_c[stage]);
+            tma_load_3d_pair(st + 2 * a_bytes + h * b_bytes, &tmB, 0, kq, static_cast<int>((boff + h * v_slab) >> 10),
                              full_c[stage]);
           }
           if (++stage == P.stages) { stage = 0; phase ^= 1; }
@@ -139,19 +147,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t dcol = tmem + acc * P.NC;
-        for (int j = 0; j < n_kb; ++j) {
+        for (int jq = 0; jq < n_kb * kSub; ++jq) {
+          const int j = jq / kSub;
           const uint32_t id = (P.cplx && !gi.im && j >= n_kb / 2) ? idesc_neg : idesc;
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t st = smem_u32(smem + stage * stage_bytes);
-            constexpr uint32_t sbo = 16 * kKBlock;
-            for (uint32_t s = 0; s < kKBlock / 16; ++s) {
+            constexpr uint32_t sbo = 16 * KS;
+            for (uint32_t s = 0; s < KS / 16; ++s) {
               const uint64_t ahi = smem_desc(st + s * 256, 128, sbo);
               const uint64_t alo = smem_desc(st + a_bytes + s * 256, 128, sbo);
               const uint64_t bhi = smem_desc(st + 2 * a_bytes + s * 256, 128, sbo);
               const uint64_t blo = smem_desc(st + 2 * a_bytes + b_bytes + s * 256, 128, sbo);
-              const uint32_t first = (j == 0 && s == 0) ? 0u : 1u;
+              const uint32_t first = (jq == 0 && s == 0) ? 0u : 1u;
               if (nh > 1) {
                 mma_bf16_ss_pair(dcol, alo, bhi, id, first);
                 mma_bf16_ss_pair(dcol, ahi, blo, id, 1u);
@@ -161,7 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               }
             }
             mma_commit_pair(&empty_bar[stage]);
-            if (j == n_kb - 1) mma_commit_pair(&tfull_bar[acc]);
+            if (jq == n_kb * kSub - 1) mma_commit_pair(&tfull_bar[acc]);
           }
           __syncwarp();
           if (++stage == P.stages) { stage = 0; phase ^= 1; }
@@ -234,15 +243,16 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// bytes -> 2-D view of 128-byte rows, box = box_rows rows
-bool encode_rows(CUtensorMap* m, const void* base, size_t bytes, int box_rows) {
+// K-block operand bytes -> 3-D view {64 elements (128 B), 8 channel
+// groups, 8-row groups}; box = KS / 8 channel groups of box_rows rows
+bool encode_kblocks(CUtensorMap* m, const void* base, size_t bytes, int ks, int box_rows) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
-  if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) || box_rows < 1 || box_rows > 256) return false;
-  const cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(bytes / 128)};
-  const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) || box_rows < 8 || box_rows > 2048 || box_rows % 8) return false;
+  const cuuint64_t dims[3] = {64, 8, static_cast<cuuint64_t>(bytes / 1024)};
+  const cuuint64_t strides[2] = {128, 1024};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(ks / 8), static_cast<cuuint32_t>(box_rows / 8)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -266,20 +276,24 @@ cudaError_t launch_position_gemm_pair(const GemmParams& P0, const Geo& g, int sm
   const int v_rows = P.cplx ? P.Cph : P.Cppad;
   const size_t u_bytes = static_cast<size_t>(P.n_pos) * P.n_blk * 2 * kBlockTiles * P.Cpad * 2;
   const size_t v_bytes = static_cast<size_t>(P.n_pos) * 2 * v_rows * P.Cpad * 2;
+  const int ks = tuning_knob("WF_PAIR_KS", 32) == 64 ? 64 : 32;   // channels per stage
   CUtensorMap tmA, tmB;
-  if (!encode_rows(&tmA, P.U, u_bytes, kBlockTiles) || !encode_rows(&tmB, P.V, v_bytes, P.NC / 2))
+  if (!encode_kblocks(&tmA, P.U, u_bytes, ks, kBlockTiles) || !encode_kblocks(&tmB, P.V, v_bytes, ks, P.NC / 2))
     return cudaErrorInvalidValue;
-  const int stage_bytes = 2 * kBlockTiles * kKBlock * 2 + 2 * (P.NC / 2) * kKBlock * 2;
+  const int stage_bytes = 2 * kBlockTiles * ks * 2 + 2 * (P.NC / 2) * ks * 2;
   P.stages = 200 * 1024 / stage_bytes;
   if (P.stages > kPairMaxStages) P.stages = kPairMaxStages;
   const int smem = P.stages * stage_bytes;
-  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(position_gemm_pair_kernel), smem);
+  const void* kern = ks == 64 ? reinterpret_cast<const void*>(position_gemm_pair_kernel<64>)
+                              : reinterpret_cast<const void*>(position_gemm_pair_kernel<32>);
+  cudaError_t e = set_smem_attr(kern, smem);
   if (e != cudaSuccess) return e;
   const int n_items = P.n_pos * n_bp * P.n_nc;
   int pairs = sm_count / 2;
   if (pairs > n_items) pairs = n_items;
   note_launch();
-  position_gemm_pair_kernel<<<2 * pairs, kPairThreads, smem, st>>>(P, n_bp, tmA, tmB);
+  if (ks == 64) position_gemm_pair_kernel<64><<<2 * pairs, kPairThreads, smem, st>>>(P, n_bp, tmA, tmB);
+  else position_gemm_pair_kernel<32><<<2 * pairs, kPairThreads, smem, st>>>(P, n_bp, tmA, tmB);
   return cudaGetLastError();
 }
 

@@ -234,14 +234,14 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
-// 2-D tensor copy global -> this CTA's shared memory whose completion bytes
+// 3-D tensor copy global -> this CTA's shared memory whose completion bytes
 // are counted on the mbarrier at `bar_cluster` (the leader CTA's barrier).
-__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tmap, int x, int y,
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const void* tmap, int x, int y, int z,
                                                  uint32_t bar_cluster) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
-      "l"(tmap), "r"(x), "r"(y), "r"(bar_cluster)
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(bar_cluster)
       : "memory");
 }
 template <uint32_t NCOLS>
