@@ -60,46 +60,66 @@ __global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __rest
     if (tvalid) tile_coords(g, tile, b, ty, tx);
     const int iy = ty * g.m - g.pad_lo + r, ox = tx * g.m - g.pad_lo;
     const bool rvalid = tvalid && iy >= 0 && iy < g.H;
-    // the group's 4 channel rows are loaded one channel ahead of the FFT
-    // that uses them (double-buffered in registers): the global-load latency
-    // of channel c + 1 overlaps the transforms of channel c
+    // The group's 4 channel rows: with 16-byte aligned rows (W % 4 == 0)
+    // all four are fetched up front as five aligned float4s each (a float4
+    // lies wholly inside or outside the row; outside ones are not loaded),
+    // so 20 independent loads per thread are in flight before the first FFT
+    // (one row ahead measured load-latency bound); other widths load
+    // per element, one channel at a time.
+    const bool vec = (g.W & 3) == 0;
+    const int sh = ox & 3, base = ox - sh;           // window start inside its 16-byte word
+    float4 raw[kFftCh / 2][5];
+    if (vec) {
+#pragma unroll
+      for (int ci4 = 0; ci4 < kFftCh / 2; ++ci4) {
+        const int ch = cg0 + (grp >> 3) * (kFftCh / 2) + ci4;
+        const float* src = x + ((static_cast<size_t>(b) * g.C + ch) * g.H + iy) * g.W;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          const int c4 = base + 4 * i;
+          raw[ci4][i] = (rvalid && ch < g.C && c4 >= 0 && c4 < g.W)
+                            ? __ldg(reinterpret_cast<const float4*>(src + c4))
+                            : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+      }
+    }
+    auto f4c = [](const float4& q, int c) { return c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w)); };
     auto load_row = [&](int ci4, float (&row)[16]) {
+      if (vec) {
+        // columns [base, base + 20) -> window columns [ox, ox + 16)
+        // (out-of-row float4s are zeros already; the in-row ones hold only
+        // in-row columns)
+        switch (sh) {
+#define WF_FFT_PICK(SH)                                                            \
+  case SH:                                                                         \
+    _Pragma("unroll") for (int s2 = 0; s2 < 16; ++s2) row[s2] = f4c(raw[ci4][(s2 + SH) >> 2], (s2 + SH) & 3); \
+    break;
+          WF_FFT_PICK(0)
+          WF_FFT_PICK(1)
+          WF_FFT_PICK(2)
+          WF_FFT_PICK(3)
+#undef WF_FFT_PICK
+        }
+        return;
+      }
       const int ch = cg0 + (grp >> 3) * (kFftCh / 2) + ci4;
       if (rvalid && ch < g.C) {
         const float* src = x + ((static_cast<size_t>(b) * g.C + ch) * g.H + iy) * g.W;
-        const int sh = ox & 3;                       // window start inside its 16-byte word
-        if ((g.W & 3) == 0 && ox >= 0 && ox - sh + 20 <= g.W) {
-          // interior window of a 16-byte aligned row: five 16-byte loads
-          // cover columns [ox - sh, ox - sh + 20) (instead of 16 scalar loads)
-          float v[20];
-          const float4* s4 = reinterpret_cast<const float4*>(src + ox - sh);
 #pragma unroll
-          for (int i = 0; i < 5; ++i) {
-            const float4 q = __ldg(s4 + i);
-            v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
-          }
-#pragma unroll
-          for (int s = 0; s < 16; ++s)
-            row[s] = sh == 0 ? v[s] : sh == 1 ? v[s + 1] : sh == 2 ? v[s + 2] : v[s + 3];
-        } else {
-#pragma unroll
-          for (int s = 0; s < 16; ++s) {
-            const int ix = ox + s;
-            row[s] = (ix >= 0 && ix < g.W) ? __ldg(src + ix) : 0.0f;
-          }
+        for (int s2 = 0; s2 < 16; ++s2) {
+          const int ix = ox + s2;
+          row[s2] = (ix >= 0 && ix < g.W) ? __ldg(src + ix) : 0.0f;
         }
       } else {
 #pragma unroll
-        for (int s = 0; s < 16; ++s) row[s] = 0.0f;
+        for (int s2 = 0; s2 < 16; ++s2) row[s2] = 0.0f;
       }
     };
-    float rows[2][16];
-    load_row(0, rows[0]);
 #pragma unroll
     for (int ci4 = 0; ci4 < kFftCh / 2; ++ci4) {
       const int c = (grp >> 3) * (kFftCh / 2) + ci4;
-      if (ci4 + 1 < kFftCh / 2) load_row(ci4 + 1, rows[(ci4 + 1) & 1]);
-      float (&row)[16] = rows[ci4 & 1];
+      float row[16];
+      load_row(ci4, row);
       float fr[9], fi[9];
       fft::rfft16(row, fr, fi);
 #pragma unroll
@@ -138,12 +158,16 @@ __global__ void __launch_bounds__(256, 2) fft_forward_kernel(const float* __rest
       const int blk = tl / kBlockTiles, row = tl % kBlockTiles;
       const uint32_t off = slab_off(row, (part ? g.C : 0) + cg0 + 2 * q, kBlockTiles, g.Cpad);
       const float* sa = part ? sim : sre;
+      // (running pointer: a 64-bit multiply per bin was most of this loop)
+      uint8_t* base = u + ((static_cast<size_t>(pp) * nblk_local + blk) * 2) * slab + off;
+      const size_t bstep = static_cast<size_t>(4) * nblk_local * 2 * slab;
+#pragma unroll 4
       for (int p = pp; p < kBins; p += 4) {
         uint32_t hi, lo;
         split2<F16>(sa[stage_idx(p, 2 * q, t)], sa[stage_idx(p, 2 * q + 1, t)], hi, lo);
-        uint8_t* base = u + ((static_cast<size_t>(p) * nblk_local + blk) * 2) * slab + off;
         *reinterpret_cast<uint32_t*>(base) = hi;
         *reinterpret_cast<uint32_t*>(base + slab) = lo;
+        base += bstep;
       }
     }
   } else {
@@ -208,11 +232,15 @@ __global__ void __launch_bounds__(kInvThreads) fft_inverse_kernel(const float* _
   for (int c = 0; c < kInvCh; ++c) {
     const int cp = cg0 + c;
     if (tvalid && cp < g.Cp) {
+      // bins u * 9 + v, u = 0..15: a running pointer (stride 9 bins)
+      const float* pr = M + (static_cast<size_t>(v) * g.Nout + cp) * ldm + tl;
+      const size_t im_off = static_cast<size_t>(g.Cp) * ldm;
+      const size_t ustep = static_cast<size_t>(9) * g.Nout * ldm;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const size_t row = static_cast<size_t>(u * 9 + v) * g.Nout;
-        rec[c][u] = __ldcg(M + (row + cp) * ldm + tl);
-        imc[c][u] = __ldcg(M + (row + g.Cp + cp) * ldm + tl);
+        rec[c][u] = __ldcg(pr);
+        imc[c][u] = __ldcg(pr + im_off);
+        pr += ustep;
       }
     } else {
 #pragma unroll

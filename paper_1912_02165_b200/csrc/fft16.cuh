@@ -31,6 +31,23 @@ __device__ __forceinline__ int bitrev4(int i) {
   return ((i & 1) << 3) | ((i & 2) << 1) | ((i & 4) >> 1) | ((i & 8) >> 3);
 }
 
+// t = w * z for a compile-time twiddle w = (wr, wi) (after unrolling):
+// IEEE semantics keep x * 0 from folding away (NaN, -0), so the trivial
+// twiddles -- (+-1, 0) and (0, +-1) -- take the multiplication-free forms
+// explicitly (in fft16 they are 17 of the 32 butterflies).
+__device__ __forceinline__ void twiddle(float wr, float wi, float zr, float zi, float& tr, float& ti) {
+  if (wi == 0.0f) {
+    tr = zr * wr;              // wr = +-1: a (negated) copy
+    ti = zi * wr;
+  } else if (wr == 0.0f) {
+    tr = -zi * wi;             // wi = +-1
+    ti = zr * wi;
+  } else {
+    tr = zr * wr - zi * wi;
+    ti = zr * wi + zi * wr;
+  }
+}
+
 // In-place radix-2 DIT complex FFT of 16 points held in registers.
 // sign = -1: forward (exp(-i...)), +1: inverse (no scaling).
 template <int SIGN>
@@ -53,8 +70,8 @@ __device__ __forceinline__ void fft16(float (&re)[16], float (&im)[16]) {
         const float wr = kc(k * step);
         const float wi = SIGN * ks(k * step);
         const int a = base + k, b = a + half;
-        const float tr = r[b] * wr - q[b] * wi;
-        const float ti = r[b] * wi + q[b] * wr;
+        float tr, ti;
+        twiddle(wr, wi, r[b], q[b], tr, ti);
         r[b] = r[a] - tr;
         q[b] = q[a] - ti;
         r[a] = r[a] + tr;
@@ -90,8 +107,8 @@ __device__ __forceinline__ void fft8(float (&r)[8], float (&q)[8]) {
         const float wr = kc(k * step);
         const float wi = SIGN * ks(k * step);
         const int u = base + k, v = u + half;
-        const float tr = a[v] * wr - b[v] * wi;
-        const float ti = a[v] * wi + b[v] * wr;
+        float tr, ti;
+        twiddle(wr, wi, a[v], b[v], tr, ti);
         a[v] = a[u] - tr;
         b[v] = b[u] - ti;
         a[u] = a[u] + tr;
@@ -127,8 +144,13 @@ __device__ __forceinline__ void rfft16(const float (&x)[16], float (&re)[9], flo
     const float er = 0.5f * (zr[k] + zr[j]), ei = 0.5f * (zi[k] - zi[j]);
     const float orr = 0.5f * (zi[k] + zi[j]), oi = 0.5f * (zr[j] - zr[k]);
     const float c = kc(k), s = ks(k);
-    re[k] = fmaf(s, oi, fmaf(c, orr, er));
-    im[k] = fmaf(-s, orr, fmaf(c, oi, ei));
+    if (c == 0.0f) {           // k = 4: W16^4 = -i
+      re[k] = fmaf(s, oi, er);
+      im[k] = fmaf(-s, orr, ei);
+    } else {
+      re[k] = fmaf(s, oi, fmaf(c, orr, er));
+      im[k] = fmaf(-s, orr, fmaf(c, oi, ei));
+    }
   }
 }
 
@@ -149,8 +171,13 @@ __device__ __forceinline__ void irfft16(const float (&re)[9], const float (&im)[
     const float sr = re[k] + re[j], si = im[k] - im[j];
     const float dr = re[k] - re[j], di = im[k] + im[j];
     const float c = kc(k), s = ks(k);
-    zr[k] = sr - fmaf(dr, s, di * c);
-    zi[k] = si + fmaf(dr, c, -di * s);
+    if (c == 0.0f) {           // k = 4
+      zr[k] = sr - dr * s;
+      zi[k] = si - di * s;
+    } else {
+      zr[k] = sr - fmaf(dr, s, di * c);
+      zi[k] = si + fmaf(dr, c, -di * s);
+    }
   }
   fft8<1>(zr, zi);
 #pragma unroll

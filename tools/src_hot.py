@@ -1,18 +1,30 @@
 """Aggregate an ncu report's SASS-level stall samples by CUDA source line.
 
-    python tools/src_hot.py gpurun_out/x.ncu-rep build/fused_ws.o [kernel-substring] [top]
-The object must be the one the report was taken from (same build).
+    python tools/src_hot.py gpurun_out/x.ncu-rep build/fused_ws.o [kernel-substring] [top] [ncu-kernel-regex]
+The object must be the one the report was taken from (same build); the
+optional regex picks one kernel of a report that holds several.
 """
 import csv, io, re, subprocess, sys, tempfile, os, collections
 
 rep, obj = sys.argv[1], sys.argv[2]
 ksub = sys.argv[3] if len(sys.argv) > 3 else ""
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+kfilt = len(sys.argv) > 5
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-h = rows[1]
-data = [r for r in rows[2:] if len(r) == len(h)]
+# one section per profiled launch ("Kernel Name" row, header row, data):
+# the first whose kernel name matches
+sections, cur = [], None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        cur = [r[1] if len(r) > 1 else "", []]
+        sections.append(cur)
+    elif cur is not None:
+        cur[1].append(r)
+pick = next((sec for sec in sections if not kfilt or re.search(sys.argv[5], sec[0])), sections[0])
+h = pick[1][0]
+data = [r for r in pick[1][1:] if len(r) == len(h)]
 ai, si, ei = h.index("Address"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
 reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
 # address -> line from nvdisasm
