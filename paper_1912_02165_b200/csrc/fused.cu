@@ -45,6 +45,11 @@ static size_t block_bytes(const Geo& g) {
 static int wave_blocks(const Geo& g) {
   if (const int k = tuning_knob("WF_WAVE_BLOCKS", 0)) return std::max(1, std::min(g.n_blk, k));
   size_t nb = budget_cfg() / lanes_cfg() / block_bytes(g);
+  // CTA-pair GEMM layers whose single block already overflows a lane's L2
+  // share (C' >= 512: 14-19 MB per block) gain nothing from waves; one wave
+  // of all blocks keeps every pair GEMM full-width (VGG 512->512 @28: waves
+  // of 6 + 6 + 1 blocks 0.155 ms, one wave 0.149 ms)
+  if (nb == 0 && gemm_pair_layer(g) && !gemm_resident_fits(g)) return g.n_blk;
   const int n_nc = ceil_div(g.Cppad, gemm_nc(g.Cppad));
   // FFT-16 layers with a resident-V GEMM (C'pad <= 128): the forward and
   // inverse kernels (128 CTAs per block) want larger waves (measured c4
