@@ -119,6 +119,8 @@ def parse():
     ap.add_argument("--no-per-config", action="store_true", help="headline config only")
     ap.add_argument("--per-config-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=4, help="batch slices of the host-buffer pipeline")
+    ap.add_argument("--e2e-stream-chunks", type=int, default=1,
+                    help="batch slices per step of the streaming (submit / wait) pipeline")
     ap.add_argument("--cpu-stub", action="store_true",
                     help="launcher self-test without GPUs: gloo ranks, the CPU oracle on each rank's batch shard "
                          "of a small layer (tests/test_bench_launcher.py)")
@@ -569,24 +571,49 @@ def run_ours(args):
         x_host = it["x"].cpu().pin_memory()
         y_host = torch.empty(it["spec"].output_dims(), dtype=torch.float32, pin_memory=True)
         chunks = min(args.e2e_chunks, it["spec"].batch)
+        stream = torch.cuda.current_stream(dev)
+        e2e_steps = max(3, min(args.steps, 20))
+        # (1) one call at a time: HostPipeline(...)(x_host, y_host) returns
+        # when the result is in y_host (the latency of a single call)
         pipe = wf.HostPipeline(it["spec"], it["pack"], it["cfg"], chunks=chunks)
         for _ in range(2):
             pipe(x_host, y_host)
         torch.cuda.synchronize(dev)
-        e2e_steps = max(3, min(args.steps, 10))
         if world > 1:
             dist.barrier()
-        stream = torch.cuda.current_stream(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e2e_steps):
             pipe(x_host, y_host)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
-        e2e = {"ms_per_step": e2e_ms, "h2d": int(x_host.numel() * 4), "d2h": int(y_host.numel() * 4),
-               "api": f"HostPipeline(chunks={chunks}): pinned host in/out, per-slice H2D / layer / D2H on three "
-                      f"streams, CUDA-graph replay"}
+        sync_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+        del pipe
+        # (2) streaming: every step is submit()ted with its own upload and
+        # download; step k + 1 uploads into the second staging set while step
+        # k computes and downloads (the throughput of a serving loop)
+        depth = 2
+        y_hosts = [y_host] + [torch.empty_like(y_host).pin_memory() for _ in range(depth - 1)]
+        spipe = wf.HostPipeline(it["spec"], it["pack"], it["cfg"], chunks=args.e2e_stream_chunks, graph=False,
+                                depth=depth)
+        for k in range(2 * depth):
+            spipe.submit(x_host, y_hosts[k % depth])
+        spipe.wait()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            spipe.submit(x_host, y_hosts[k % depth])
+        spipe.wait()
+        e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
+        e2e = {"ms_per_step": e2e_ms, "sync_ms_per_step": sync_ms,
+               "h2d": int(x_host.numel() * 4), "d2h": int(y_host.numel() * 4),
+               "api": f"HostPipeline(chunks={args.e2e_stream_chunks}, depth={depth}).submit(x_host, y_host) per "
+                      f"step + wait(): pinned host in/out, every step's H2D / layer / D2H on three streams, step "
+                      f"k + 1 uploading while step k downloads (host wall clock over {e2e_steps} steps); "
+                      f"sync_ms_per_step = one HostPipeline(chunks={chunks})(x_host, y_host) call at a time "
+                      f"(CUDA-graph replay)"}
     else:
         # multi-layer configs: every layer's input uploaded and output read back per step
         stream = torch.cuda.current_stream(dev)
@@ -682,7 +709,8 @@ def run_ours(args):
             "layers": layers,
             "e2e": {"value": flops_step / (e2e["ms_per_step"] * 1e-3) / 1e12, "unit": "TFLOP/s",
                     "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
-                    "ms_per_step": e2e["ms_per_step"], "api": e2e["api"]},
+                    "ms_per_step": e2e["ms_per_step"], "api": e2e["api"],
+                    **({"sync_ms_per_step": e2e["sync_ms_per_step"]} if "sync_ms_per_step" in e2e else {})},
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

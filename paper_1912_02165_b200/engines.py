@@ -623,7 +623,7 @@ class HostPipeline:
     """
 
     def __init__(self, spec: LayerSpec, pack: KernelPack, config: EngineConfig | None = None, chunks: int = 8,
-                 graph: bool = True, split=None):
+                 graph: bool = True, split=None, depth: int = 1):
         cfg = config or EngineConfig(kind="fused")
         self.use_graph = graph
         self._graph = None
@@ -658,12 +658,21 @@ class HostPipeline:
             shared = max((p.scratch for p in self.plans.values()), key=lambda t: t.numel())
             for plan in self.plans.values():
                 plan.share_scratch(shared)
-        self.x_dev = torch.empty(spec.input_dims(), dtype=torch.float32, device=self.dev)
-        self.y_dev = torch.empty(spec.output_dims(), dtype=torch.float32, device=self.dev)
+        # `depth` sets of device staging buffers: submit() of call k + 1 uploads
+        # while call k computes and downloads (depth 1: one call at a time)
+        if depth < 1:
+            raise InvalidParameterError("depth must be >= 1")
+        self.depth = depth
+        self.x_devs = [torch.empty(spec.input_dims(), dtype=torch.float32, device=self.dev) for _ in range(depth)]
+        self.y_devs = [torch.empty(spec.output_dims(), dtype=torch.float32, device=self.dev) for _ in range(depth)]
+        self.x_dev, self.y_dev = self.x_devs[0], self.y_devs[0]
         self.streams = [torch.cuda.Stream(self.dev) for _ in range(3)]
         n = len(self.bounds)
-        self.ev_in = [torch.cuda.Event() for _ in range(n)]
-        self.ev_comp = [torch.cuda.Event() for _ in range(n)]
+        self.ev_in = [[torch.cuda.Event() for _ in range(n)] for _ in range(depth)]
+        self.ev_comp = [[torch.cuda.Event() for _ in range(n)] for _ in range(depth)]
+        self.ev_done = [None] * depth       # last download of the call that used buffer set k
+        self.ev_comp_done = [None] * depth  # last layer launch of that call
+        self._calls = 0
 
     def __call__(self, x_host, y_host):
         """x_host (B, C, H, W) and y_host (B, C', H', W'): CPU f32 tensors, ideally pinned.
@@ -690,21 +699,59 @@ class HostPipeline:
         self.streams[2].synchronize()
         return y_host
 
-    def _issue(self, x_host, y_host):
+    def _issue(self, x_host, y_host, k=0, fork=True):
         torch = _dev.torch
         s_in, s_comp, s_out = self.streams
+        x_dev, y_dev = self.x_devs[k], self.y_devs[k]
+        ev_in, ev_comp = self.ev_in[k], self.ev_comp[k]
         cur = torch.cuda.current_stream(self.dev)
-        for s in self.streams:
-            s.wait_stream(cur)
+        if fork:
+            for s in self.streams:
+                s.wait_stream(cur)
         for i, (lo, hi) in enumerate(self.bounds):
             with torch.cuda.stream(s_in):
-                self.x_dev[lo:hi].copy_(x_host[lo:hi], non_blocking=True)
-                self.ev_in[i].record(s_in)
+                x_dev[lo:hi].copy_(x_host[lo:hi], non_blocking=True)
+                ev_in[i].record(s_in)
             with torch.cuda.stream(s_comp):
-                s_comp.wait_event(self.ev_in[i])
-                self.plans[hi - lo](self.x_dev[lo:hi], out=self.y_dev[lo:hi])
-                self.ev_comp[i].record(s_comp)
+                s_comp.wait_event(ev_in[i])
+                self.plans[hi - lo](x_dev[lo:hi], out=y_dev[lo:hi])
+                ev_comp[i].record(s_comp)
             with torch.cuda.stream(s_out):
-                s_out.wait_event(self.ev_comp[i])
-                y_host[lo:hi].copy_(self.y_dev[lo:hi], non_blocking=True)
-        cur.wait_stream(s_out)
+                s_out.wait_event(ev_comp[i])
+                y_host[lo:hi].copy_(y_dev[lo:hi], non_blocking=True)
+        if fork:
+            cur.wait_stream(s_out)
+
+    def submit(self, x_host, y_host):
+        """Queue one call without waiting for it (streaming use: a serving
+        loop that feeds batches back to back).  Call k + 1 uploads into the
+        next of the ``depth`` staging sets while call k computes and
+        downloads, so in the steady state a call costs max(upload, download,
+        compute) instead of their pipelined sum.  The three streams keep the
+        calls in order; the only extra edges are the reuse of a staging set
+        (upload after the layer launches that read it, layer launches after
+        the downloads that read their output).  ``wait()`` returns when every
+        submitted call has landed in its ``y_host``; the caller must not
+        reuse a ``y_host`` (or change an ``x_host``) of a call still in flight.
+        """
+        torch = _dev.torch
+        k = self._calls % self.depth
+        s_in, s_comp, s_out = self.streams
+        if self._calls == 0:
+            cur = torch.cuda.current_stream(self.dev)
+            for s in self.streams:
+                s.wait_stream(cur)
+        if self.ev_comp_done[k] is not None:
+            s_in.wait_event(self.ev_comp_done[k])
+            s_comp.wait_event(self.ev_done[k])
+        self._issue(x_host, y_host, k, fork=False)
+        self.ev_comp_done[k] = self.ev_comp[k][-1]
+        ev = self.ev_done[k] or torch.cuda.Event()
+        ev.record(s_out)
+        self.ev_done[k] = ev
+        self._calls += 1
+        return ev
+
+    def wait(self):
+        """Block until every submitted call has been downloaded."""
+        self.streams[2].synchronize()

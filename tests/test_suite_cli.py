@@ -137,6 +137,35 @@ def test_host_pipeline_matches_single_call(cuda_dev):
         assert np.array_equal(y_host.numpy(), ref), chunks
 
 
+@pytest.mark.gpu
+def test_host_pipeline_streaming_submit_wait(cuda_dev):
+    """submit() / wait(): calls queued back to back over two staging sets
+    (call k + 1 uploads while call k downloads) give, for every call, bitwise
+    the single-call result -- different inputs per call, so a staging set
+    reused too early would show."""
+    import torch
+    spec = wf.LayerSpec(6, 64, 64, 24, 24, 3, 1, 1)
+    w = wf.new_tensor(spec.kernel_dims(), seed=4)
+    pack = wf.transform_kernels(w, wf.make_basis(6))
+    cfg = wf.EngineConfig(kind="fused", tile=6, device=cuda_dev)
+    plan = wf.LayerPlan(spec, pack, cfg)
+    xs = [wf.new_tensor(spec.input_dims(), seed=10 + i).data for i in range(5)]
+    refs = [plan(torch.from_numpy(x).to(cuda_dev)).cpu().numpy() for x in xs]
+    x_hosts = [torch.from_numpy(x).pin_memory() for x in xs]
+    y_hosts = [torch.zeros(spec.output_dims(), dtype=torch.float32).pin_memory() for _ in xs]
+    for chunks, depth in ((1, 2), (3, 2), (2, 3), (1, 1)):
+        for y in y_hosts:
+            y.zero_()
+        pipe = wf.HostPipeline(spec, pack, cfg, chunks=chunks, graph=False, depth=depth)
+        for xh, yh in zip(x_hosts, y_hosts):
+            pipe.submit(xh, yh)
+        pipe.wait()
+        for i, (yh, ref) in enumerate(zip(y_hosts, refs)):
+            assert np.array_equal(yh.numpy(), ref), (chunks, depth, i)
+    with pytest.raises(wf.InvalidParameterError):
+        wf.HostPipeline(spec, pack, cfg, depth=0)
+
+
 def test_b200_model_fitted_to_measured_layers():
     """The B200 planner's rates are fitted to measured layer times (the
     warp-specialised fused kernel and the three-stage engine, bench.py
