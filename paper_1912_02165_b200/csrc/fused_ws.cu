@@ -260,6 +260,14 @@ template <uint32_t N> __device__ __forceinline__ void regs_dec() {
 template <uint32_t N> __device__ __forceinline__ void regs_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
 }
+// Pin a pointer in registers: without it ptxas re-derives "kernel parameter
+// + lane offset" (LDC.64 + two adds) in front of every store of an unrolled
+// store sequence -- 36 constant-bank loads on the F units' critical path --
+// instead of keeping the 64-bit base and using the stores' immediate offsets.
+template <class T>
+__device__ __forceinline__ void keep_in_regs(T*& p) {
+  asm volatile("" : "+l"(p));
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -475,6 +483,7 @@ __device__ __forceinline__ void f_unit8(const Params& P, const uint8_t* src, Syn
   uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 / S::kKBW) * S::kAHalf +
                  (row >> 3) * (16 * S::kKBW) + ((c0 % S::kKBW) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
                  (cq & 1) * (S::kKB * S::kAHalf) + (cq >> 1) * 8 * S::kUPos;
+  keep_in_regs(dst);
   const bool odd = cq & 1, upper = cq & 2;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
@@ -694,6 +703,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
         uint8_t* dst = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + (c0 / S::kKBW) * S::kAHalf +
                        (row >> 3) * (16 * S::kKBW) + ((c0 % S::kKBW) >> 3) * 128 + (row & 7) * 16 + (c0 & 7) * 2 +
                        (odd ? S::kKB * S::kAHalf : 0);
+        keep_in_regs(dst);
 #pragma unroll
         for (int s = 0; s < kT; ++s) {
           bt6_line<PairOps>(w[0][s], w[1][s], w[2][s], w[3][s], w[4][s], w[5][s]);
