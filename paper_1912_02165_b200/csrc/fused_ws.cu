@@ -629,6 +629,17 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       for (int i = wtid; i < static_cast<int>(S::kMUnit / 128); i += 256) discard_l2(m + static_cast<size_t>(i) * 128);
     }
     if (PROF && lane == 0) trace<PROF>(b, kind == 0 ? 0 : 4, true);
+#ifdef WF_TUNING_AIDS
+    if (P.dbg == 4 || P.dbg == 7 || (P.dbg == 5 && kind == 0) || (P.dbg == 6 && kind == 2)) {
+      // tuning aid: no transform work (4, 7: none, 5: no F, 6: no I); results invalid
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sy.fi_empty[slot]);
+        red_release_cta_smem(&sy.fi_cnt[it & 3], 1);
+      }
+      continue;
+    }
+#endif
 
     if constexpr (S::kT == 8) {
       if (kind == 0) f_unit8<S, F16>(P, src, sy, slot, b, sub, wl, lane);
@@ -1044,7 +1055,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
   const int n_g = P.g.n_blk * S::kNGG;
   if (warp < 4) {
     regs_dec<kRegsLight>();
-    if (P.dbg == 3) {
+    if (P.dbg == 3 || P.dbg == 7) {
       // tuning aid: no GEMM work, every G unit is published at once (results invalid)
       if (warp == 0) {
         if (lane_id() == 0)
@@ -1065,7 +1076,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
     }
   } else if (warp < 8) {
     regs_dec<kRegsEpi>();
-    if (P.dbg != 3) g_epilogue<S, PROF>(P, sy, n_g);
+    if (P.dbg != 3 && P.dbg != 7) g_epilogue<S, PROF>(P, sy, n_g);
   } else {
     regs_inc<kRegsFI>();
     fi_workers<S, PROF, F16>(P, smem, sy);
@@ -1157,6 +1168,9 @@ static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
   // (VGG's RGB layer); C' = C'pad
   if (g.fft || g.Cp != g.Cppad || (g.C != g.Cpad && g.Cpad != 16)) return R();
   switch (g.T * 1000000 + g.Cpad * 1000 + g.Cp) {
+#ifdef WF_WS_ONLY   // tuning builds (tools/build_alt.sh): one instance, compiles in 40 s
+    case WF_WS_ONLY: return f(Shape<WF_WS_ONLY / 1000000, (WF_WS_ONLY / 1000) % 1000, WF_WS_ONLY % 1000>());
+#else
     case 6016064: return f(Shape<6, 16, 64>());
     case 6064064: return f(Shape<6, 64, 64>());
     case 6064128: return f(Shape<6, 64, 128>());
@@ -1171,6 +1185,7 @@ static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
     case 8032032: return f(Shape<8, 32, 32>());
     case 8064064: return f(Shape<8, 64, 64>());
     case 8128128: return f(Shape<8, 128, 128>());
+#endif
   }
   return R();
 }
@@ -1234,7 +1249,8 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
   P.discard = tuning_knob("WF_WS_DISCARD", g.T == 8 ? 2 : (g.Cpad > 16 ? 1 : 0));
   P.dbg = 0;
 #ifdef WF_TUNING_AIDS
-  P.dbg = tuning_knob("WF_WS_DBG", 0);     // 3: no GEMM work (results invalid)
+  // ablations (results invalid): 3 no GEMM work, 4 no transform work, 5 no F, 6 no I, 7 = 3 + 4
+  P.dbg = tuning_knob("WF_WS_DBG", 0);
 #endif
   P.plane = pl.plane;
   P.grid = sm_count;
