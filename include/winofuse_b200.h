@@ -112,6 +112,10 @@ int wf_conv_fused(const float* x, const void* mma_pack, float* y, void* scratch,
 #define WF_FUSED_WS 1    /* warp-specialised persistent dataflow kernel (fused_ws.cu)  */
 #define WF_FUSED_ITEMQ 2 /* item-queue persistent dataflow kernel (fused_persistent.cu)*/
 #define WF_FUSED_WAVES 3 /* the stage kernels per L2-resident wave of blocks (fused.cu) */
+#define WF_FUSED_WS_ROW 4 /* warp-specialised kernel, row units: a CTA owns a row of      */
+                          /* transform positions and runs the inverse transform's row    */
+                          /* pass in the GEMM epilogue (F(4x4,3x3), C = C' = 64, inputs   */
+                          /* whose F units stage in 48 KB); never picked by AUTO (slower) */
 
 /* Flags.  COUNTERS_CLEAN: the caller asserts that the scratch's dependency
  * counters are zero -- it zero-filled the scratch once and only runs this

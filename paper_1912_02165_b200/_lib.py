@@ -22,7 +22,7 @@ WF_OK, WF_ERR_PARAM, WF_ERR_SHAPE, WF_ERR_UNSUPPORTED, WF_ERR_CUDA, WF_ERR_SCRAT
 WF_WINOGRAD, WF_FFT16 = 0, 1
 WF_PREC_3XBF16, WF_PREC_BF16, WF_PREC_3XFP16 = 0, 1, 2
 WF_PHASE_FORWARD, WF_PHASE_MULTIPLY, WF_PHASE_INVERSE = 1, 2, 4
-WF_FUSED_AUTO, WF_FUSED_WS, WF_FUSED_ITEMQ, WF_FUSED_WAVES = 0, 1, 2, 3
+WF_FUSED_AUTO, WF_FUSED_WS, WF_FUSED_ITEMQ, WF_FUSED_WAVES, WF_FUSED_WS_ROW = 0, 1, 2, 3, 4
 WF_FUSED_COUNTERS_CLEAN, WF_FUSED_INSTRUMENT = 1, 2
 
 PRECISIONS = {"3xbf16": WF_PREC_3XBF16, "bf16": WF_PREC_BF16, "3xfp16": WF_PREC_3XFP16}
@@ -30,7 +30,8 @@ PRECISIONS = {"3xbf16": WF_PREC_3XBF16, "bf16": WF_PREC_BF16, "3xfp16": WF_PREC_
 PACK_FORMAT = {"3xbf16": "bf16", "bf16": "bf16", "3xfp16": "fp16"}
 TRANSFORMS = {"winograd": WF_WINOGRAD, "fft": WF_FFT16}
 # fused-engine variants (EngineConfig.fused_variant <-> WF_FUSED_*)
-VARIANTS = {"auto": WF_FUSED_AUTO, "ws": WF_FUSED_WS, "itemq": WF_FUSED_ITEMQ, "waves": WF_FUSED_WAVES}
+VARIANTS = {"auto": WF_FUSED_AUTO, "ws": WF_FUSED_WS, "itemq": WF_FUSED_ITEMQ, "waves": WF_FUSED_WAVES,
+            "ws_row": WF_FUSED_WS_ROW}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 
 

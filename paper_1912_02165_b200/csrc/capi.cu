@@ -476,7 +476,7 @@ int wf_conv_three_stage(const float* x, const void* mma_pack, float* y, void* sc
 static int fused_opts(const wf_fused_opts* in, FusedOpts& o) {
   o = FusedOpts();
   if (!in) return WF_OK;
-  if (in->variant < WF_FUSED_AUTO || in->variant > WF_FUSED_WAVES) return fail(WF_ERR_PARAM, "variant %d", in->variant);
+  if (in->variant < WF_FUSED_AUTO || in->variant > WF_FUSED_WS_ROW) return fail(WF_ERR_PARAM, "variant %d", in->variant);
   if (in->flags & ~(WF_FUSED_COUNTERS_CLEAN | WF_FUSED_INSTRUMENT)) return fail(WF_ERR_PARAM, "flags %d", in->flags);
   if (in->lag < 0 || in->gbatch < 0) return fail(WF_ERR_PARAM, "negative lag / gbatch");
   o.variant = in->variant;
@@ -526,7 +526,7 @@ int wf_conv_fused_ex(const float* x, const void* mma_pack, float* y, void* scrat
   if (passes == 0) return fail(WF_ERR_PARAM, "precision %d", precision);
   if (fused_pick_variant(g, o) == 0)
     return fail(WF_ERR_UNSUPPORTED, "fused variant %d cannot run this layer", o.variant);
-  if ((o.flags & WF_FUSED_INSTRUMENT) && fused_pick_variant(g, o) != kVarWS)
+  if ((o.flags & WF_FUSED_INSTRUMENT) && fused_pick_variant(g, o) != kVarWS && fused_pick_variant(g, o) != kVarWSRow)
     return fail(WF_ERR_UNSUPPORTED, "instrumentation is implemented by the warp-specialised variant only");
   const size_t need = fused_scratch_bytes(g, o);
   if (need && (!scratch || scratch_bytes < need))

@@ -299,26 +299,31 @@ __device__ __forceinline__ void forward6(const V (&x)[6][6], V (&u)[6][6]) {
     for (int s = 0; s < 6; ++s) u[r][s] = x[r][s];
   forward6_inplace<O>(u);
 }
-// same operations as inverse6, with the column pass written over mm
+// Inverse order: every row of products first (A^T along the row: 6 -> 4
+// values), then every column of the 6 x 4 result.  The row pass of a
+// position row needs only that row's six products -- the warp-specialised
+// kernel's row-unit instance runs it in the GEMM epilogue -- so every T = 6
+// path uses this order and stays bitwise equal to it.
+// (same operations as inverse6, with the row pass written over mm)
 template <class O, class V>
 __device__ __forceinline__ void inverse6_inplace(V (&mm)[6][6], V (&y)[4][4]) {
 #pragma unroll
-  for (int s = 0; s < 6; ++s) {
+  for (int r = 0; r < 6; ++r) {
     V t0, t1, t2, t3;
-    at6_line<O>(mm[0][s], mm[1][s], mm[2][s], mm[3][s], mm[4][s], mm[5][s], t0, t1, t2, t3);
-    mm[0][s] = t0; mm[1][s] = t1; mm[2][s] = t2; mm[3][s] = t3;
+    at6_line<O>(mm[r][0], mm[r][1], mm[r][2], mm[r][3], mm[r][4], mm[r][5], t0, t1, t2, t3);
+    mm[r][0] = t0; mm[r][1] = t1; mm[r][2] = t2; mm[r][3] = t3;
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r) at6_line<O>(mm[r][0], mm[r][1], mm[r][2], mm[r][3], mm[r][4], mm[r][5], y[r][0], y[r][1], y[r][2], y[r][3]);
+  for (int j = 0; j < 4; ++j) at6_line<O>(mm[0][j], mm[1][j], mm[2][j], mm[3][j], mm[4][j], mm[5][j], y[0][j], y[1][j], y[2][j], y[3][j]);
 }
 template <class O, class V>
 __device__ __forceinline__ void inverse6(const V (&mm)[6][6], V (&y)[4][4]) {
-  V t[4][6];
+  V z[6][4];
 #pragma unroll
-  for (int s = 0; s < 6; ++s)
-    at6_line<O>(mm[0][s], mm[1][s], mm[2][s], mm[3][s], mm[4][s], mm[5][s], t[0][s], t[1][s], t[2][s], t[3][s]);
+  for (int r = 0; r < 6; ++r)
+    at6_line<O>(mm[r][0], mm[r][1], mm[r][2], mm[r][3], mm[r][4], mm[r][5], z[r][0], z[r][1], z[r][2], z[r][3]);
 #pragma unroll
-  for (int r = 0; r < 4; ++r) at6_line<O>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], y[r][0], y[r][1], y[r][2], y[r][3]);
+  for (int j = 0; j < 4; ++j) at6_line<O>(z[0][j], z[1][j], z[2][j], z[3][j], z[4][j], z[5][j], y[0][j], y[1][j], y[2][j], y[3][j]);
 }
 template <>
 __device__ __forceinline__ void forward_transform<6>(const float (&x)[6][6], float (&u)[6][6]) {

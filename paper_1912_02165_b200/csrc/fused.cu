@@ -73,6 +73,7 @@ size_t waves_scratch_bytes(const Geo& g) {
 int fused_pick_variant(const Geo& g, const FusedOpts& o) {
   switch (o.variant) {
     case kVarWS: return ws_fits(g, o) ? kVarWS : 0;
+    case kVarWSRow: return ws_fits(g, o) ? kVarWSRow : 0;
     case kVarItemQueue: return persistent_fits(g, o, false) ? kVarItemQueue : 0;
     case kVarWaves: return kVarWaves;
     case kVarAuto: break;
@@ -86,7 +87,7 @@ int fused_pick_variant(const Geo& g, const FusedOpts& o) {
 size_t fused_scratch_bytes(const Geo& g, const FusedOpts& o) {
   const int v = fused_pick_variant(g, o);
   size_t own = 0;
-  if (v == kVarWS) own = ws_scratch_bytes(g, o);
+  if (v == kVarWS || v == kVarWSRow) own = ws_scratch_bytes(g, o);
   if (v == kVarItemQueue) own = persistent_scratch_bytes(g, o);
   return std::max(own, waves_scratch_bytes(g));
 }
@@ -121,7 +122,7 @@ cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* s
   const int v = fused_pick_variant(g, o);
   if (v == 0) return cudaErrorInvalidValue;
   cudaError_t e = cudaSuccess;
-  if (v == kVarWS) e = run_fused_ws(x, vpack, y, scratch, g, passes, sm_count, st, o);
+  if (v == kVarWS || v == kVarWSRow) e = run_fused_ws(x, vpack, y, scratch, g, passes, sm_count, st, o);
   else if (v == kVarItemQueue) e = run_fused_persistent(x, vpack, y, scratch, g, passes, sm_count, st, o);
   if (v != kVarWaves && e != cudaErrorCooperativeLaunchTooLarge) {
     if (ran) *ran = v;
@@ -135,7 +136,7 @@ cudaError_t run_fused(const float* x, const uint8_t* vpack, float* y, uint8_t* s
   // the waves overwrite the warp-specialised kernel's dependency counters
   // (3 n_blk + 1 ints at the start of the scratch); a caller that keeps them
   // clean between calls gets them back zeroed
-  if (e == cudaSuccess && v == kVarWS && (o.flags & kFusedCountersClean))
+  if (e == cudaSuccess && (v == kVarWS || v == kVarWSRow) && (o.flags & kFusedCountersClean))
     e = cudaMemsetAsync(scratch, 0, static_cast<size_t>(3 * g.n_blk + 1) * sizeof(int), st);
   return e;
 }

@@ -8,7 +8,7 @@
 namespace wf {
 
 // Fused-engine variants (include/winofuse_b200.h WF_FUSED_*).
-constexpr int kVarAuto = 0, kVarWS = 1, kVarItemQueue = 2, kVarWaves = 3;
+constexpr int kVarAuto = 0, kVarWS = 1, kVarItemQueue = 2, kVarWaves = 3, kVarWSRow = 4;
 constexpr int kFusedCountersClean = 1, kFusedInstrument = 2;
 
 // Per-call options of the fused engine (the C ABI's wf_fused_opts).  Every

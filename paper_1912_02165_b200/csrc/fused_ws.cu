@@ -41,27 +41,33 @@ constexpr uint32_t kRegsLight = WF_WS_REGS ? 40 : 128;
 constexpr uint32_t kRegsEpi = WF_WS_REGS ? 64 : 128;
 constexpr uint32_t kRegsFI = WF_WS_REGS ? 200 : 128;
 static_assert(4 * 32 * kRegsLight + 4 * 32 * kRegsEpi + 8 * 32 * kRegsFI <= 65536, "register file");
-#ifndef WF_WS_GP
-#define WF_WS_GP 1
-#endif
-constexpr int kGP = WF_WS_GP;                            // positions per G unit
-static_assert(kGP == 1, "G units own one position (position-affine CTAs keep V resident)");
-constexpr int kNAcc = 8;                                 // TMEM accumulator buffers (units in flight)
+constexpr int kNAcc = 8;                                 // TMEM accumulator buffers (units in flight), at most
+constexpr int kMaxGP = 6;                                // positions per G unit, at most
 constexpr int kMaxAStages = 4;
 
 // Layer shape: window T (6: F(4x4,3x3), 8: F(6x6,3x3)), C input channels
 // (GEMM K, 32-channel K blocks), CP output channels (GEMM N, 64-wide G
 // units).  Shared memory: A stages + the V slab of the CTA's (position, c'
 // group) + two 72 KB F/I slots <= 227 KB.
-template <int T_, int C_, int CP_, int SL_ = 2>
+// GP_ = positions per G unit: 1 (a CTA owns one position) or T (the "row
+// unit" instance, T = 6 with C, C' <= 64: a CTA owns one ROW of positions
+// (r, 0..5), keeps their six V slabs resident, accumulates the row's six
+// products of a block in TMEM and runs the inverse transform's row pass in
+// the GEMM epilogue, so the M ring carries 4 instead of 6 values per row
+// and the I units only run the column pass).
+template <int T_, int C_, int CP_, int SL_ = 2, int GP_ = 1>
 struct Shape {
+  static constexpr int kGP = GP_;
+  static constexpr bool kRow = GP_ > 1;
+  static constexpr int kAcc = kRow ? 1 : kNAcc;          // TMEM buffers in flight (6 x 64 columns fill TMEM)
+  static_assert(!kRow || (T_ == 6 && GP_ == 6 && C_ <= 64 && CP_ == 64 && SL_ == 2), "row units");
   // F/I staging slots: 2 x 72 KB.  (3 x 48 KB with 2-channel I units was
   // measured on c2: 98 vs 80 us -- twice the I units and a shorter lag)
   static constexpr int kSlots = SL_;
   static constexpr int kT = T_, kP = T_ * T_;
   static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
   static constexpr int kN = CP < 64 ? CP : 64;           // output channels per G unit (MMA N)
-  static constexpr int kTmemCols = kNAcc * kGP * kN;     // 128, 256 or 512
+  static constexpr int kTmemCols = kRow ? 512 : kNAcc * kN;     // 128, 256 or 512
   // F unit: kFT tiles x 8 channels (one core-matrix k group, so that a
   // warp's U stores fill whole 32-byte sectors): 64 tiles with a thread per
   // (tile, channel pair) for T = 6, 32 tiles with a thread per (tile,
@@ -70,13 +76,15 @@ struct Shape {
   static constexpr int kFT = T_ == 6 ? 64 : 32;
   // F staging or I staging slot (two of them)
   // (C = 256, T = 6: 48 KB, room for the 64 KB V slab; 2-channel I units)
-  static constexpr uint32_t kFISlot = (SL_ == 3 ? 48 : T_ == 6 ? (C_ >= 256 ? 48 : 72) : 73) * 1024;
+  static constexpr uint32_t kFISlot = (SL_ == 3 || kRow ? 48 : T_ == 6 ? (C_ >= 256 ? 48 : 72) : 73) * 1024;
   // I unit: kIPairs c' pairs.  M ring slot layout: [I unit][position][c' pair
   // in unit][tile][2]: the products one I unit needs are one contiguous
   // range (72 KB for T = 6, 64 KB for T = 8) -- one bulk copy
+  // (row units: [I unit][row r][output column j][c' pair][tile][2], 6 x 4
+  // values per (tile, c'): 48 KB)
   static constexpr int kIPairs = (T_ == 6 && C_ < 256 && SL_ == 2) ? 2 : 1;
   static constexpr uint32_t kIPos = kIPairs * kBlockTiles * 8;
-  static constexpr uint32_t kMUnit = kP * kIPos;
+  static constexpr uint32_t kMUnit = (kRow ? T_ * (T_ - 2) : kP) * kIPos;
   static constexpr int kKBW = C < 32 ? C : 32;           // K block width (channels per A stage)
   static constexpr int kKB = C / kKBW;                   // K blocks
   static constexpr uint32_t kAHalf = kBlockTiles * kKBW * 2;   // hi or lo of one K block
@@ -84,18 +92,19 @@ struct Shape {
   static constexpr int kVKW = C < 64 ? C : 64;           // K block width of the MMA pack (kblock layout)
   static constexpr uint32_t kVChunk = kN * kVKW * 2;     // one c' group's rows of one pack K block
   static constexpr int kNG = CP / kN;                    // c' groups (G units per position)
-  static constexpr int kNGG = kP * kNG;                  // G units per block
+  static constexpr int kNGG = kP / kGP * kNG;            // G units per block
   static constexpr int kNCG = (kBlockTiles / kFT) * (C / kCPC);   // F units per block
   static constexpr int kNIG = CP / (2 * kIPairs);                 // I units per block
-  static constexpr int kAStages = C >= 128 ? 3 : 4;
+  // (2 stages measured equal to 4 on c2: the G units wait for their inputs, not for stage space)
+  static constexpr int kAStages = kRow ? 2 : C >= 128 ? 3 : 4;
   static constexpr uint32_t kVHalf = kN * C * 2;         // V hi (or lo) of one (position, c' group)
   static constexpr uint32_t kVGroup = 2 * kVHalf;
   static constexpr size_t kUPos = 2 * kKB * kAHalf;      // U of one position: [hl][K block]
   static constexpr size_t kUSlot = kP * kUPos;
   static constexpr size_t kMPos = static_cast<size_t>(CP) * kBlockTiles * 4;
-  static constexpr size_t kMSlot = kP * kMPos;
+  static constexpr size_t kMSlot = kRow ? static_cast<size_t>(CP / (2 * kIPairs)) * kMUnit : kP * kMPos;
   static constexpr uint32_t kOffB = kAStages * kAStage;
-  static constexpr uint32_t kOffFI = kOffB + kVGroup;
+  static constexpr uint32_t kOffFI = kOffB + kGP * kVGroup;
   static constexpr uint32_t kSmem = kOffFI + kSlots * kFISlot;
   static_assert(kSmem <= 227 * 1024 && kAStages <= kMaxAStages && C % 16 == 0 && CP % kN == 0, "shape");
   static_assert((T_ == 6 || T_ == 8) && kMUnit <= kFISlot, "window");
@@ -199,7 +208,7 @@ struct ProfT {
 struct Sync {
   uint64_t a_full[kMaxAStages], a_empty[kMaxAStages];
   uint64_t b_full[2], b_empty[2];
-  uint64_t tfull[kNAcc][kGP], tempty[kNAcc];
+  uint64_t tfull[kNAcc][kMaxGP], tempty[kNAcc];
   uint64_t fi_full[3], fi_empty[3];
   // completion counts: F/I unit k adds 8 (one per worker warp) to fi_cnt[k % 4],
   // G unit k adds 4 (one per epilogue warp) to g_cnt[k % kNAcc].  A warp can
@@ -517,16 +526,22 @@ __device__ __forceinline__ void i_unit6s(const Params& P, const uint8_t* src, Sy
   const int tl = wtid & (kBlockTiles - 1), cq = wtid >> 7;
   const int tile = b * kBlockTiles + tl;
   const float* ms = reinterpret_cast<const float*>(src) + tl * 2 + cq;
-  float t[4][6];
+  // row pass as the staged products are read (A^T along each row), then
+  // the column pass one output column at a time (== inverse6)
+  float z[6][4];
 #pragma unroll
-  for (int s = 0; s < 6; ++s) {
+  for (int r = 0; r < 6; ++r) {
     float m[6];
 #pragma unroll
-    for (int r = 0; r < 6; ++r) m[r] = ms[(r * 6 + s) * (S::kIPos / 4)];
-    at6_line<ScalarOps>(m[0], m[1], m[2], m[3], m[4], m[5], t[0][s], t[1][s], t[2][s], t[3][s]);
+    for (int s = 0; s < 6; ++s) m[s] = ms[(r * 6 + s) * (S::kIPos / 4)];
+    at6_line<ScalarOps>(m[0], m[1], m[2], m[3], m[4], m[5], z[r][0], z[r][1], z[r][2], z[r][3]);
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
+  float t[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    at6_line<ScalarOps>(z[0][j], z[1][j], z[2][j], z[3][j], z[4][j], z[5][j], t[0][j], t[1][j], t[2][j], t[3][j]);
   if (tile < g.n_tile) {
     const int per_img = g.tiles_y * g.tiles_x;
     const int bi = tile / per_img;
@@ -538,8 +553,7 @@ __device__ __forceinline__ void i_unit6s(const Params& P, const uint8_t* src, Sy
     float* ybase = P.y + ((static_cast<size_t>(bi) * g.Cp + cp) * g.Ho + oy) * g.Wo + ox;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      float o[4];
-      at6_line<ScalarOps>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], o[0], o[1], o[2], o[3]);
+      const float o[4] = {t[r][0], t[r][1], t[r][2], t[r][3]};
       if (vec) {
         out_store<S>(reinterpret_cast<float4*>(ybase + r * g.Wo), make_float4(o[0], o[1], o[2], o[3]));
       } else if (oy + r < g.Ho) {
@@ -735,20 +749,32 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
       // ---- I(b, sub): thread = (tile, c' pair); 36 staged float2 per thread
       const int tl = wtid & (kBlockTiles - 1), pr = wtid >> 7;
       const int tile = b * kBlockTiles + tl;
-      // column pass as the staged products are read (A^T down each column),
-      // then one output row at a time (== inverse_transform2<6>)
+      // row pass as the staged products are read (A^T along each row; the
+      // row-unit instance stages its result, computed in the GEMM epilogue),
+      // then the column pass (== inverse_transform2<6>)
       constexpr int MO = kT - 2;
-      float2 t[MO][kT];
+      float2 z[kT][MO];
       const float2* ms = reinterpret_cast<const float2*>(src + pr * kBlockTiles * 8) + tl;
+      if constexpr (S::kRow) {
 #pragma unroll
-      for (int s = 0; s < kT; ++s) {
-        float2 m[kT];
+        for (int r = 0; r < kT; ++r)
 #pragma unroll
-        for (int r = 0; r < kT; ++r) m[r] = ms[(r * kT + s) * (kIPos / 8)];
-        at6_line<PairOps>(m[0], m[1], m[2], m[3], m[4], m[5], t[0][s], t[1][s], t[2][s], t[3][s]);
+          for (int j = 0; j < MO; ++j) z[r][j] = ms[(r * MO + j) * (kIPos / 8)];
+      } else {
+#pragma unroll
+        for (int r = 0; r < kT; ++r) {
+          float2 m[kT];
+#pragma unroll
+          for (int s = 0; s < kT; ++s) m[s] = ms[(r * kT + s) * (kIPos / 8)];
+          at6_line<PairOps>(m[0], m[1], m[2], m[3], m[4], m[5], z[r][0], z[r][1], z[r][2], z[r][3]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
+      float2 t[MO][MO];
+#pragma unroll
+      for (int j = 0; j < MO; ++j)
+        at6_line<PairOps>(z[0][j], z[1][j], z[2][j], z[3][j], z[4][j], z[5][j], t[0][j], t[1][j], t[2][j], t[3][j]);
       if (tile < g.n_tile) {
         const int per_img = g.tiles_y * g.tiles_x;
         const int bi = tile / per_img;
@@ -761,8 +787,7 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
         float* ybase = P.y + (static_cast<size_t>(bi) * g.Cp + cp) * plane + static_cast<size_t>(oy) * g.Wo + ox;
 #pragma unroll
         for (int r = 0; r < MO; ++r) {
-          float2 o[MO];
-          at6_line<PairOps>(t[r][0], t[r][1], t[r][2], t[r][3], t[r][4], t[r][5], o[0], o[1], o[2], o[3]);
+          const float2 o[MO] = {t[r][0], t[r][1], t[r][2], t[r][3]};
           if (vec) {
             out_store<S>(reinterpret_cast<float4*>(ybase + r * g.Wo), make_float4(o[0].x, o[1].x, o[2].x, o[3].x));
             out_store<S>(reinterpret_cast<float4*>(ybase + plane + r * g.Wo),
@@ -797,11 +822,11 @@ template <class S>
 struct GUnits {
   int p, ng, b0, step;
   __device__ GUnits(const Params& P) {
-    constexpr int combos = S::kP * S::kNG;               // (position, c' group) pairs
+    constexpr int combos = S::kNGG;                      // (position or position row, c' group) pairs
     step = P.grid / combos;
     const int c = blockIdx.x % combos;
-    p = c % S::kP;
-    ng = c / S::kP;
+    p = c % (S::kP / S::kGP);
+    ng = c / (S::kP / S::kGP);
     b0 = static_cast<int>(blockIdx.x) < step * combos ? blockIdx.x / combos : P.g.n_blk;
   }
 };
@@ -820,14 +845,15 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
     // V of this CTA's (position, c' group), once: in the MMA pack (per
     // position a hi and a lo slab of CP x C, K blocks of 64) the group's 64
     // rows of one K block are 8 KB contiguous; smem holds [hl][K block of 64]
-    mbar_expect_tx(&sy.b_full[0], S::kVGroup);
+    mbar_expect_tx(&sy.b_full[0], S::kGP * S::kVGroup);
     const size_t slab = static_cast<size_t>(S::CP) * S::C * 2;
-    for (int hl = 0; hl < 2; ++hl)
-      for (int j = 0; j < S::C / S::kVKW; ++j)
-        bulk_g2s(smem + S::kOffB + (hl * (S::C / S::kVKW) + j) * S::kVChunk,
-                 P.vpack + (static_cast<size_t>(gu.p) * 2 + hl) * slab +
-                     static_cast<size_t>(j) * S::CP * S::kVKW * 2 + static_cast<size_t>(gu.ng) * S::kVChunk,
-                 S::kVChunk, &sy.b_full[0]);
+    for (int pl = 0; pl < S::kGP; ++pl)
+      for (int hl = 0; hl < 2; ++hl)
+        for (int j = 0; j < S::C / S::kVKW; ++j)
+          bulk_g2s(smem + S::kOffB + pl * S::kVGroup + (hl * (S::C / S::kVKW) + j) * S::kVChunk,
+                   P.vpack + (static_cast<size_t>(gu.p * S::kGP + pl) * 2 + hl) * slab +
+                       static_cast<size_t>(j) * S::CP * S::kVKW * 2 + static_cast<size_t>(gu.ng) * S::kVChunk,
+                   S::kVChunk, &sy.b_full[0]);
   }
   __syncwarp();
   int a_it = 0;
@@ -839,8 +865,8 @@ __device__ void g_producer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
     if (lane == 0) trace<PROF>(b, 2, true);
     fence_proxy_async_global();
     const uint8_t* uslot = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot;
-    {
-      const int p = gu.p;
+    for (int pl = 0; pl < S::kGP; ++pl) {
+      const int p = gu.p * S::kGP + pl;
       for (int kb = 0; kb < S::kKB; ++kb) {
         const int st = a_it % S::kAStages;
         long long t2 = pf.now();
@@ -874,12 +900,14 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
   const uint32_t sb = smem_u32(smem + S::kOffB);
   int a_it = 0, k = 0;
   for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
-    const int buf = k % kNAcc;
+    const int buf = k % S::kAcc;
     long long t0 = pf.now();
-    mbar_wait(&sy.tempty[buf], ((k / kNAcc) & 1) ^ 1);
+    mbar_wait(&sy.tempty[buf], ((k / S::kAcc) & 1) ^ 1);
     pf.add(kGITempty, t0);
     tc_fence_after();
-    const uint32_t dcol = sy.tmem + buf * kN;
+   for (int pl = 0; pl < S::kGP; ++pl) {
+    const uint32_t dcol = sy.tmem + (buf * S::kGP + pl) * kN;
+    const uint32_t sbp = sb + pl * S::kVGroup;             // the unit's pl-th position
     for (int kb = 0; kb < S::kKB; ++kb) {
       const int st = a_it % S::kAStages;
       long long t2 = pf.now();
@@ -896,8 +924,8 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
           // V: [hl][pack K block][64 rows x kVKW k]; channel k0 of this K step
           const int k0 = kb * S::kKBW + s * 16;
           const uint32_t voff = (k0 / S::kVKW) * S::kVChunk + ((k0 % S::kVKW) >> 3) * 128;
-          const uint64_t bhi = smem_desc(sb + voff, 128, 16 * S::kVKW);
-          const uint64_t blo = smem_desc(sb + S::kVHalf + voff, 128, 16 * S::kVKW);
+          const uint64_t bhi = smem_desc(sbp + voff, 128, 16 * S::kVKW);
+          const uint64_t blo = smem_desc(sbp + S::kVHalf + voff, 128, 16 * S::kVKW);
           const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
           if (prec_passes(P.passes) > 1) {
             mma_bf16_ss(dcol, alo, bhi, idesc, first);
@@ -908,11 +936,12 @@ __device__ void g_issuer(const Params& P, uint8_t* smem, Sync& sy, int n_g) {
           }
         }
         mma_commit(&sy.a_empty[st]);
-        if (kb == S::kKB - 1) mma_commit(&sy.tfull[buf][0]);
+        if (kb == S::kKB - 1) mma_commit(&sy.tfull[buf][pl]);
       }
       __syncwarp();
       ++a_it;
     }
+   }
   }
   pf.end(kEndGI);
 }
@@ -928,19 +957,54 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
   constexpr int kN = S::kN;
   int k = 0;
   for (int b = gu.b0; b < P.g.n_blk; b += gu.step, ++k) {
-    const int buf = k % kNAcc;
+    const int buf = k % S::kAcc;
     const bool live = b * kBlockTiles + row < P.g.n_tile;
     float* mslot = P.mring + static_cast<size_t>(b % P.NM) * (S::kMSlot / 4);
-    for (int pl = 0; pl < kGP; ++pl) {
+    if constexpr (S::kRow) {
+      // ---- row unit: the six products (r, 0..5) of this thread's tile, 4
+      // output channels at a time -> row pass of the inverse transform
+      // (A^T along the row, == the first pass of inverse6) -> M ring, 4
+      // values per (tile, c'): [I unit c' / 4][r][j][pair][tile][2]
       long long t0 = pf.now();
-      mbar_wait(&sy.tfull[buf][pl], (k / kNAcc) & 1);
+      for (int pl = 0; pl < S::kGP; ++pl) mbar_wait(&sy.tfull[buf][pl], (k / S::kAcc) & 1);
       pf.add(kGEWait, t0);
       t0 = pf.now();
       tc_fence_after();
-      const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (kGP * kN) + pl * kN;
+      const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (S::kGP * kN);
+      float2* mrow = reinterpret_cast<float2*>(mslot) + row;
+#pragma unroll 2
+      for (int c = 0; c < kN; c += 4) {
+        float m[6][4];
+#pragma unroll
+        for (int pl = 0; pl < 6; ++pl) tmem_ld4(taddr + pl * kN + c, m[pl]);
+        tmem_ld_wait();
+        float z[4][4];                                   // [c' in chunk][j]
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+          at6_line<ScalarOps>(m[0][cc], m[1][cc], m[2][cc], m[3][cc], m[4][cc], m[5][cc], z[cc][0], z[cc][1], z[cc][2],
+                              z[cc][3]);
+        if (live) {
+          // I unit c / 4 (C' = 64: one c' group), pairs (c, c + 1) and (c + 2, c + 3)
+          float2* mu = mrow + static_cast<size_t>(c / 4) * (S::kMUnit / 8) + static_cast<size_t>(gg) * (4 * S::kIPos / 8);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr)
+              ring_store<S>(mu + (j * 2 + pr) * kBlockTiles, make_float2(z[2 * pr][j], z[2 * pr + 1][j]));
+        }
+      }
+      pf.add(kGEBusy, t0);
+    } else
+    for (int pl = 0; pl < S::kGP; ++pl) {
+      long long t0 = pf.now();
+      mbar_wait(&sy.tfull[buf][pl], (k / S::kAcc) & 1);
+      pf.add(kGEWait, t0);
+      t0 = pf.now();
+      tc_fence_after();
+      const uint32_t taddr = sy.tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * (S::kGP * kN) + pl * kN;
       // pair k of position p: [k / kIPairs][p][k % kIPairs][tile][2] (see
       // Shape::kMUnit); this unit's 64 outputs are the pairs 32 ng .. 32 ng + 31
-      float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * kGP + pl) * (S::kIPos / 4)) + row;
+      float2* mrow = reinterpret_cast<float2*>(mslot + static_cast<size_t>(gg * S::kGP + pl) * (S::kIPos / 4)) + row;
 #pragma unroll
       for (int c = 0; c < kN; c += 16) {
         float vv[16];
@@ -962,8 +1026,8 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
       // the unit's U (one position, read by this unit only when C' = 64) is
       // dead: drop its L2 lines before the unit is published (publishing
       // lets the next F units of the ring slot write it again)
-      const uint8_t* u = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + gg * S::kUPos;
-      constexpr int lines = static_cast<int>(S::kUPos / 128);
+      const uint8_t* u = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + gg * S::kGP * S::kUPos;
+      constexpr int lines = static_cast<int>(S::kGP * S::kUPos / 128);
       for (int i = qd * 32 + lane; i < lines; i += 128) discard_l2(u + static_cast<size_t>(i) * 128);
     }
     __syncwarp();
@@ -971,7 +1035,7 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
       // the last of the 4 epilogue warps to finish publishes the unit (counted
       // before the buffer is released, so no warp can count a later use of
       // this buffer first)
-      if (atom_acqrel_cta_smem(&sy.g_cnt[buf], 1) == 4 * (k / kNAcc) + 3) {
+      if (atom_acqrel_cta_smem(&sy.g_cnt[buf], 1) == 4 * (k / S::kAcc) + 3) {
         const long long t1 = pf.now();
         trace<PROF>(b, 3, false);    // before the release that publishes it
         if (P.gbatch == 1) {
@@ -981,7 +1045,7 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
           // G roles): acquire the batch's earlier units through their
           // completion counts, one fence, then the counts of every unit
           const int k0 = k - k % P.gbatch;
-          for (int j = k0; j < k; ++j) (void)ld_acquire_cta_smem(&sy.g_cnt[j % kNAcc]);
+          for (int j = k0; j < k; ++j) (void)ld_acquire_cta_smem(&sy.g_cnt[j % S::kAcc]);
           fence_acq_rel_gpu();
           for (int j = k0; j <= k; ++j) red_relaxed_gpu(P.counters + P.g.n_blk + gu.b0 + j * gu.step, 1);
         }
@@ -1034,7 +1098,7 @@ __global__ void __launch_bounds__(NT, 1) fused_ws_kernel(Params P) {
       mbar_init(&sy.fi_empty[s], 8);
     }
     for (int s = 0; s < kNAcc; ++s) {
-      for (int p = 0; p < kGP; ++p) mbar_init(&sy.tfull[s][p], 1);
+      for (int p = 0; p < kMaxGP; ++p) mbar_init(&sy.tfull[s][p], 1);
       mbar_init(&sy.tempty[s], 4);
     }
     for (int i = 0; i < 4; ++i) sy.fi_cnt[i] = 0;
@@ -1112,18 +1176,31 @@ struct Plan {
   size_t counters_bytes, u_slot, m_slot;
 };
 
+// floats per staged channel of an F unit of kft tiles: the largest unit's rows
+static int fi_plane(const Geo& g, int kft) {
+  int max_rows = 0;
+  for (int t0 = 0; t0 < g.n_tile; t0 += kft) {
+    const FGeo fg(g, t0, std::min(t0 + kft, g.n_tile) - 1);
+    max_rows = std::max(max_rows, fg.total());
+  }
+  return round_up(max_rows * g.W, 32) + 16;
+}
+// The row-unit instance (F(4x4,3x3), C = C' = 64) has 48 KB F/I slots next to
+// its six resident V slabs: it runs where an F unit's input rows fit them
+// (W = 56: yes; W = 224: no) and the device has a CTA per position row.
+static bool row_units_fit(const Geo& g) {
+  if (g.T != 6 || g.fft || g.Cpad != 64 || g.C != 64 || g.Cp != 64 || g.Cppad != 64) return false;
+  if (g.W % 4 != 0 || g.pad_lo != 1 || g.W < 8) return false;
+  return static_cast<size_t>(8) * fi_plane(g, 64) * 4 <= 48 * 1024;
+}
+
 template <class S>
 static Plan plan_t(const Geo& g, const FusedOpts& o) {
   Plan pl = {};
   // the bulk-copied input rows must be 16-byte aligned (W % 4 == 0); the
   // branch-free window loads assume pad_lo = 1
   if (g.W % 4 != 0 || g.m != S::kT - 2 || g.pad_lo != 1 || g.W < 8) return pl;
-  int max_rows = 0;                        // union staging: the largest unit
-  for (int t0 = 0; t0 < g.n_tile; t0 += S::kFT) {
-    const FGeo fg(g, t0, std::min(t0 + S::kFT, g.n_tile) - 1);
-    max_rows = std::max(max_rows, fg.total());
-  }
-  pl.plane = round_up(max_rows * g.W, 32) + 16;
+  pl.plane = fi_plane(g, S::kFT);
   if (static_cast<size_t>(S::kCPC) * pl.plane * 4 > S::kFISlot) return pl;
   // ring budget 140 MB (the U + M rings of c2 take 70 MB: inside the 126 MB
   // L2 next to the streamed input and output).  Measured (tools/ring_sweep.py,
@@ -1162,8 +1239,9 @@ static Plan plan_t(const Geo& g, const FusedOpts& o) {
 // -- every (position, c' group) pair gets a CTA of its own (T^2 x C'/64 <=
 // 148), and A stages + V + two F/I slots fit smem.
 template <class F>
-static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
+static auto with_shape(const Geo& g, const FusedOpts& o, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
   using R = decltype(f(Shape<6, 64, 64>()));
+  if (o.variant == kVarWSRow) return row_units_fit(g) ? f(Shape<6, 64, 64, 2, 6>()) : R();
   // C = Cpad except for the 16-channel instance, which zero-pads C <= 16
   // (VGG's RGB layer); C' = C'pad
   if (g.fft || g.Cp != g.Cppad || (g.C != g.Cpad && g.Cpad != 16)) return R();
@@ -1191,7 +1269,7 @@ static auto with_shape(const Geo& g, F&& f) -> decltype(f(Shape<6, 64, 64>())) {
 }
 
 static Plan plan(const Geo& g, const FusedOpts& o) {
-  return with_shape(g, [&](auto s) { return plan_t<decltype(s)>(g, o); });
+  return with_shape(g, o, [&](auto s) { return plan_t<decltype(s)>(g, o); });
 }
 
 template <class S>
@@ -1216,7 +1294,7 @@ bool ws_fits(const Geo& g, const FusedOpts& o) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // a CTA per (position, c' group)
-  return ws::with_shape(g, [&](auto s) { return sms >= decltype(s)::kP * decltype(s)::kNG; });
+  return ws::with_shape(g, o, [&](auto s) { return sms >= decltype(s)::kNGG; });
 }
 
 size_t ws_scratch_bytes(const Geo& g, const FusedOpts& o) {
@@ -1265,14 +1343,14 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
     cudaError_t e = cudaMemsetAsync(P.counters, 0, pl.counters_bytes, st);
     if (e != cudaSuccess) return e;
   }
-  return ws::with_shape(g, [&](auto s) {
+  return ws::with_shape(g, o, [&](auto s) {
     using S = decltype(s);
     P.n_fi = g.n_blk * (S::kNCG + S::kNIG);
     // G publishes batched for C' <= 32 (4 units per fence).  A batch delays
     // the publish of its first unit until its last unit (step * (batch - 1)
     // blocks later) is done, which must stay inside the ring and lag slack
     // the deadlock-freedom argument uses.
-    const int step = std::max(1, sm_count / (S::kP * S::kNG));
+    const int step = std::max(1, sm_count / S::kNGG);
     int gb = S::CP <= 16 ? 8 : S::CP <= 32 ? 4 : 1;
     if (o.gbatch > 0) gb = std::min(ws::kNAcc, o.gbatch);
     else if (const int k = tuning_knob("WF_WS_GBATCH", 0)) gb = std::max(1, std::min(ws::kNAcc, k));

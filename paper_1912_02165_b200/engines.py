@@ -19,7 +19,7 @@ launching stream (transfers excluded, like the reference's timers).
 GPU additions to :class:`EngineConfig`: ``device`` (None = current CUDA
 device), ``transform`` ("winograd" | "fft"), ``precision`` ("3xbf16" |
 "3xfp16" | "bf16"), ``fused_variant`` (which fused kernel runs: "auto" | "ws" |
-"itemq" | "waves") and ``ring_bytes`` (L2 ring budget of the persistent
+"itemq" | "waves" | "ws_row", the last never picked by "auto") and ``ring_bytes`` (L2 ring budget of the persistent
 fused kernels).  There is no CPU fallback: without the CUDA extension or a
 GPU every engine raises :class:`NativeLibraryError`.
 """
@@ -127,7 +127,7 @@ class ConvStats:
     device: str = ""
     precision: str = ""
     transform: str = ""
-    variant: str = ""           # fused kernel that ran: "ws" | "itemq" | "waves"
+    variant: str = ""           # fused kernel that ran: "ws" | "itemq" | "waves" | "ws_row"
     blocks: int = 0             # 128-tile blocks (the GPU's tasks: one MMA M each)
 
 
@@ -390,7 +390,7 @@ def conv_fused(inp, pack: KernelPack, spec: LayerSpec, config: EngineConfig | No
         variant = lib.wf_fused_variant(layer, cfg.tile, tf, opts)
         if variant < 0:
             _lib.check(-variant, "wf_fused_variant")
-        if flags and variant != _lib.WF_FUSED_WS:
+        if flags and variant not in (_lib.WF_FUSED_WS, _lib.WF_FUSED_WS_ROW):
             warnings.append(f"instrumented mode is implemented by the warp-specialised kernel; the "
                             f"{_lib.VARIANT_NAMES[variant]!r} variant ran uninstrumented")
             flags = 0

@@ -287,6 +287,40 @@ def test_instrumented_fused_protocol_check(ring_mb):
     assert sb.overlap_violations is None and sb.task_trace is None
 
 
+@pytest.mark.parametrize("dims,ring_mb", [((16, 64, 64, 56, 56, 3, 1, 1), None), ((16, 64, 64, 56, 56, 3, 1, 1), 10),
+                                          ((3, 64, 64, 28, 36, 3, 1, 1), None), ((2, 64, 64, 21, 24, 3, 1, 0), None)])
+def test_ws_row_units_match_three_stage_and_fp64(dims, ring_mb):
+    """The row-unit instance of the warp-specialised kernel (a CTA owns a row
+    of transform positions; the inverse transform's row pass runs in the GEMM
+    epilogue, the M ring carries 4 values per row, the I units only run the
+    column pass): bitwise the three-stage result -- every T = 6 path applies
+    the inverse as rows, then columns -- within the FP64 bar, clean under
+    the instrumented protocol check, and never the automatic choice."""
+    spec = wf.LayerSpec(*dims)
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(spec.input_dims()).astype(np.float32)
+    w = _he(rng, spec)
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(6))
+    rb = None if ring_mb is None else ring_mb << 20
+    r, rs = _run("fused", x, pack, spec, 6, fused_variant="ws_row", ring_bytes=rb)
+    assert rs.variant == "ws_row"
+    t, _ = _run("three_stage", x, pack, spec, 6)
+    assert np.array_equal(r, t)
+    a, st = _run("fused", x, pack, spec, 6)
+    assert st.variant in ("ws", "itemq", "waves") and np.array_equal(a, r)
+    assert O.max_rel_error(r, O.direct_conv_f64(x, w, spec)) <= 1e-3
+    i, ist = _run("fused", x, pack, spec, 6, fused_variant="ws_row", ring_bytes=rb, instrumented=True)
+    assert ist.variant == "ws_row" and ist.overlap_violations == 0 and np.array_equal(i, r)
+
+
+def test_ws_row_units_reject_other_shapes():
+    spec = wf.LayerSpec(2, 128, 128, 28, 28, 3, 1, 1)
+    x = wf.new_tensor(spec.input_dims(), seed=1)
+    pack = wf.transform_kernels(wf.new_tensor(spec.kernel_dims(), seed=2), wf.make_basis(6))
+    with pytest.raises(wf.UnsupportedConfigError):
+        wf.conv_fused(x, pack, spec, wf.EngineConfig(tile=6, fused_variant="ws_row"))
+
+
 def test_three_stage_phase_times():
     spec = wf.LayerSpec(8, 64, 64, 56, 56, 3, 1, 1)
     x = wf.new_tensor(spec.input_dims(), seed=1)
