@@ -769,12 +769,15 @@ __device__ void fi_workers(const Params& P, uint8_t* smem, Sync& sy) {
           at6_line<PairOps>(m[0], m[1], m[2], m[3], m[4], m[5], z[r][0], z[r][1], z[r][2], z[r][3]);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
+      // (the slot is released after the column pass has consumed every
+      // staged value: the row-unit instance's loads feed no arithmetic
+      // before it)
       float2 t[MO][MO];
 #pragma unroll
       for (int j = 0; j < MO; ++j)
         at6_line<PairOps>(z[0][j], z[1][j], z[2][j], z[3][j], z[4][j], z[5][j], t[0][j], t[1][j], t[2][j], t[3][j]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sy.fi_empty[slot]);
       if (tile < g.n_tile) {
         const int per_img = g.tiles_y * g.tiles_x;
         const int bi = tile / per_img;
@@ -1025,7 +1028,23 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
     if ((P.discard & 1) && S::kNG == 1) {
       // the unit's U (one position, read by this unit only when C' = 64) is
       // dead: drop its L2 lines before the unit is published (publishing
-      // lets the next F units of the ring slot write it again)
+      // lets the next F units of the ring slot write it again).
+      // Row units: every epilogue warp fences (gpu scope) between its M
+      // stores and its burst of discards (12 per thread).  Without it about
+      // one call in 500 had an I unit read lines of M that another warp of
+      // the publishing CTA had stored (evict-last hint) but that were not
+      // yet visible -- the publishing warp's release covered its own
+      // stores only, and the other CTAs' discard bursts delayed the rest
+      // (tools/stress_repeat.py, tools/diag_row.py: 0 in 20000 calls with
+      // the fence; plain stores instead of hinted ones also cure it).  The
+      // one-position units (2 discards per thread) show 0 mismatches in
+      // 60000 calls with and without ring-slot reuse and keep the cheaper
+      // chain (a fence per warp costs them 80 -> 92 us on c2).
+      if constexpr (S::kRow) {
+        __syncwarp();
+        if (lane == 0) fence_acq_rel_gpu();
+        __syncwarp();
+      }
       const uint8_t* u = P.uring + static_cast<size_t>(b % P.NU) * S::kUSlot + gg * S::kGP * S::kUPos;
       constexpr int lines = static_cast<int>(S::kGP * S::kUPos / 128);
       for (int i = qd * 32 + lane; i < lines; i += 128) discard_l2(u + static_cast<size_t>(i) * 128);

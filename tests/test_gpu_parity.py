@@ -313,6 +313,29 @@ def test_ws_row_units_match_three_stage_and_fp64(dims, ring_mb):
     assert ist.variant == "ws_row" and ist.overlap_violations == 0 and np.array_equal(i, r)
 
 
+@pytest.mark.parametrize("variant,ring_mb", [("ws", None), ("ws", 12), ("ws_row", None), ("ws_row", 12)])
+def test_persistent_kernels_repeat_calls_bitwise_stable(variant, ring_mb):
+    """400 calls of one plan, every result bitwise the three-stage one: a
+    completion published before its data is visible, or a ring slot reused
+    too early, shows up as a rare differing call (tools/stress_repeat.py
+    found one of these in the row-unit instance at ~1 call in 500)."""
+    import torch
+    spec = wf.LayerSpec(24, 64, 64, 56, 56, 3, 1, 1)
+    rng = np.random.default_rng(5)
+    dev = torch.device("cuda", 0)
+    x = torch.from_numpy(rng.standard_normal(spec.input_dims()).astype(np.float32)).to(dev)
+    pack = wf.transform_kernels(wf.Tensor4D(_he(rng, spec)), wf.make_basis(6))
+    ref = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="three_stage", tile=6, device=dev))(x).clone()
+    plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=6, device=dev, fused_variant=variant,
+                                                    ring_bytes=(ring_mb << 20) if ring_mb else None))
+    out = torch.empty_like(ref)
+    bad = 0
+    for _ in range(400):
+        plan(x, out=out)
+        bad += int(not torch.equal(out, ref))
+    assert plan.variant == variant and bad == 0, bad
+
+
 def test_ws_row_units_reject_other_shapes():
     spec = wf.LayerSpec(2, 128, 128, 28, 28, 3, 1, 1)
     x = wf.new_tensor(spec.input_dims(), seed=1)

@@ -1,0 +1,44 @@
+import os, sys
+import numpy as np, torch
+sys.path.insert(0, os.getcwd())
+import paper_1912_02165_b200 as wf
+dev = torch.device("cuda", 0)
+dims=(24, 64, 64, 56, 56, 3, 1, 1); t=6
+spec = wf.LayerSpec(*dims)
+rng = np.random.default_rng(5)
+x = torch.from_numpy(rng.standard_normal(spec.input_dims()).astype(np.float32)).to(dev)
+w = (rng.standard_normal(spec.kernel_dims()) * np.sqrt(2.0 / (9 * 64))).astype(np.float32)
+pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
+ref = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="three_stage", tile=t, device=dev))(x).clone()
+plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=t, device=dev, fused_variant=os.environ.get("VARIANT", "ws_row"), ring_bytes=(int(os.environ["RING_MB"]) << 20) if "RING_MB" in os.environ else None))
+out = torch.empty_like(ref)
+plan(x, out=out); torch.cuda.synchronize()
+assert torch.equal(out, ref)
+good = plan.scratch.clone()
+found = 0
+for i in range(int(os.environ.get("CALLS", "3000"))):
+    plan(x, out=out)
+    if not torch.equal(out, ref):
+        d = (out != ref).cpu().numpy()
+        idx = np.argwhere(d)
+        b = np.unique(idx[:,0]); c = np.unique(idx[:,1]); yy = np.unique(idx[:,2]); xx = np.unique(idx[:,3])
+        err = (out-ref).abs().max().item()
+        print(f"call {i}: {d.sum()} elements differ, max abs {err:.3e}; images {b.tolist()} channels {c.tolist()[:20]}{'...' if len(c)>20 else ''} rows {yy.tolist()} cols {xx.tolist()}")
+        # tiles
+        tiles = set((int(a[0]), int(a[2])//4, int(a[3])//4) for a in idx)
+        tl = sorted(bb*196 + ty*14 + tx for bb,ty,tx in tiles)
+        print("   tile indices", tl[:40], "blocks", sorted(set(v//128 for v in tl)))
+        sc = plan.scratch
+        dd = (sc.view(torch.uint8) != good.view(torch.uint8)).nonzero().flatten().cpu().numpy()
+        if len(dd):
+            print(f"   scratch bytes differing: {len(dd)}, first {dd[0]} last {dd[-1]} (scratch {sc.numel() * sc.element_size()} B)")
+            # runs
+            runs = np.split(dd, np.where(np.diff(dd) > 64)[0] + 1)
+            for r in runs[:12]:
+                a0 = int(r[0]) & ~7
+                v_bad = sc.view(torch.uint8)[a0:a0 + 16].cpu().numpy().view(np.float32)
+                v_good = good.view(torch.uint8)[a0:a0 + 16].cpu().numpy().view(np.float32)
+                print(f"     run [{r[0]}, {r[-1]}] len {r[-1] - r[0] + 1}: bad {v_bad} good {v_good}")
+        found += 1
+        if found >= 6: break
+print("calls", i+1, "found", found)
