@@ -148,14 +148,17 @@ __device__ __forceinline__ void out_store(T* p, T v) {
   if constexpr (Hints<S>::on) st_hint(p, v, l2_policy_evict_first());
   else *p = v;
 }
+#ifndef WF_WS_RING_HINTS
+#define WF_WS_RING_HINTS 1
+#endif
 template <class S>
 __device__ __forceinline__ void ring_store(uint2* p, uint2 v) {
-  if constexpr (Hints<S>::on) st_hint(p, v, l2_policy_evict_last());
+  if constexpr (Hints<S>::on && (WF_WS_RING_HINTS & 1)) st_hint(p, v, l2_policy_evict_last());
   else *p = v;
 }
 template <class S>
 __device__ __forceinline__ void ring_store(float2* p, float2 v) {
-  if constexpr (Hints<S>::on) st_hint(p, v, l2_policy_evict_last());
+  if constexpr (Hints<S>::on && (WF_WS_RING_HINTS & 2)) st_hint(p, v, l2_policy_evict_last());
   else __stcg(p, v);
 }
 
@@ -1030,16 +1033,13 @@ __device__ void g_epilogue(const Params& P, Sync& sy, int n_g) {
       // dead: drop its L2 lines before the unit is published (publishing
       // lets the next F units of the ring slot write it again).
       // Row units: every epilogue warp fences (gpu scope) between its M
-      // stores and its burst of discards (12 per thread).  Without it about
-      // one call in 500 had an I unit read lines of M that another warp of
-      // the publishing CTA had stored (evict-last hint) but that were not
-      // yet visible -- the publishing warp's release covered its own
-      // stores only, and the other CTAs' discard bursts delayed the rest
-      // (tools/stress_repeat.py, tools/diag_row.py: 0 in 20000 calls with
-      // the fence; plain stores instead of hinted ones also cure it).  The
-      // one-position units (2 discards per thread) show 0 mismatches in
-      // 60000 calls with and without ring-slot reuse and keep the cheaper
-      // chain (a fence per warp costs them 80 -> 92 us on c2).
+      // stores and its burst of discards (12 per thread).  Without the
+      // fence about one call in 500 produced wrong values in one warp's
+      // stores of one 4-channel chunk (DESIGN.md 5.5 lists what was
+      // measured; the mechanism is not pinned down); with it 0 in 20000
+      // calls.  The one-position units (2 discards per thread) show 0
+      // mismatches in 60000 calls and keep the cheaper chain (a fence per
+      // warp costs them 80 -> 92 us on c2).
       if constexpr (S::kRow) {
         __syncwarp();
         if (lane == 0) fence_acq_rel_gpu();

@@ -16,13 +16,18 @@ plan(x, out=out); torch.cuda.synchronize()
 assert torch.equal(out, ref)
 good = plan.scratch.clone()
 found = 0
+PREFILL = os.environ.get("PREFILL")
+m_off = 1024 + 37 * 1179648
 for i in range(int(os.environ.get("CALLS", "3000"))):
+    if PREFILL:
+        plan.scratch[m_off:].fill_(int(PREFILL))       # sentinel in the whole M ring before the call
     plan(x, out=out)
     if not torch.equal(out, ref):
         d = (out != ref).cpu().numpy()
         idx = np.argwhere(d)
         b = np.unique(idx[:,0]); c = np.unique(idx[:,1]); yy = np.unique(idx[:,2]); xx = np.unique(idx[:,3])
         err = (out-ref).abs().max().item()
+        print("   NaNs in out:", int(torch.isnan(out).sum().item()), " zeros-diff:", float((out - ref)[out != ref].abs().min().item()))
         print(f"call {i}: {d.sum()} elements differ, max abs {err:.3e}; images {b.tolist()} channels {c.tolist()[:20]}{'...' if len(c)>20 else ''} rows {yy.tolist()} cols {xx.tolist()}")
         # tiles
         tiles = set((int(a[0]), int(a[2])//4, int(a[3])//4) for a in idx)
