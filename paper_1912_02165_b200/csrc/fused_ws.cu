@@ -132,7 +132,7 @@ struct Params {
 // Stores with the kernel's L2 eviction priorities (Params::hints).
 // Stores with the kernel's L2 eviction priorities, per window size (compile
 // time: a runtime switch in the store paths measured 12-16% slower even when
-// off): layer input and output evict-first, ring stores evict-last.
+// off): layer input and output evict-first, U ring stores evict-last (WF_WS_RING_HINTS bit 1; bit 2 = the M ring stores, measured neutral, off).
 #ifndef WF_WS_L2_HINTS_T6
 #define WF_WS_L2_HINTS_T6 1
 #endif
