@@ -28,6 +28,11 @@ cases = [
     ((16, 128, 128, 28, 28, 3, 1, 1), 8, "ws", 40),
     ((24, 48, 80, 56, 56, 3, 1, 1), 6, "itemq", None),
     ((8, 96, 96, 56, 56, 3, 1, 1), 8, "itemq", None),
+    ((16, 512, 512, 28, 28, 3, 1, 1), 6, "waves", None),   # three wave lanes, CTA-pair GEMM
+    ((16, 256, 512, 28, 28, 3, 1, 1), 6, "waves", None),
+    ((32, 512, 512, 14, 14, 3, 1, 1), 6, "waves", None),
+    ((32, 64, 64, 56, 56, 3, 1, 1), 16, "waves", None),    # FFT-16
+    ((32, 256, 256, 14, 14, 3, 1, 1), 16, "waves", None),
 ]
 failed = 0
 for dims, t, variant, ring_mb in cases:
@@ -35,9 +40,10 @@ for dims, t, variant, ring_mb in cases:
     rng = np.random.default_rng(5)
     x = torch.from_numpy(rng.standard_normal(spec.input_dims()).astype(np.float32)).to(dev)
     w = (rng.standard_normal(spec.kernel_dims()) * np.sqrt(2.0 / (9 * dims[1]))).astype(np.float32)
-    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_basis(t))
-    ref = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="three_stage", tile=t, device=dev))(x).clone()
-    plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=t, device=dev, fused_variant=variant,
+    tf = "fft" if t == 16 else "winograd"
+    pack = wf.transform_kernels(wf.Tensor4D(w), wf.make_fft_basis() if t == 16 else wf.make_basis(t))
+    ref = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="three_stage", tile=t, device=dev, transform=tf))(x).clone()
+    plan = wf.LayerPlan(spec, pack, wf.EngineConfig(kind="fused", tile=t, device=dev, fused_variant=variant, transform=tf,
                                                     ring_bytes=(ring_mb << 20) if ring_mb else None))
     bad = 0
     out = torch.empty_like(ref)
