@@ -57,17 +57,21 @@ constexpr int kMaxAStages = 4;
 // and the I units only run the column pass).
 template <int T_, int C_, int CP_, int SL_ = 2, int GP_ = 1>
 struct Shape {
+  // (other GP_ > 1: a G unit covers GP_ consecutive positions with the
+  // one-position M layout -- fewer, larger units for the narrow layers,
+  // whose G roles are bound by the per-unit latency)
   static constexpr int kGP = GP_;
-  static constexpr bool kRow = GP_ > 1;
+  static constexpr bool kRow = T_ == 6 && GP_ == 6;
   static constexpr int kAcc = kRow ? 1 : kNAcc;          // TMEM buffers in flight (6 x 64 columns fill TMEM)
-  static_assert(!kRow || (T_ == 6 && GP_ == 6 && C_ <= 64 && CP_ == 64 && SL_ == 2), "row units");
+  static_assert(!kRow || (C_ <= 64 && CP_ == 64 && SL_ == 2), "row units");
+  static_assert((T_ * T_) % GP_ == 0 && kAcc * GP_ * (CP_ < 64 ? CP_ : 64) <= 512, "positions per G unit");
   // F/I staging slots: 2 x 72 KB.  (3 x 48 KB with 2-channel I units was
   // measured on c2: 98 vs 80 us -- twice the I units and a shorter lag)
   static constexpr int kSlots = SL_;
   static constexpr int kT = T_, kP = T_ * T_;
   static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
   static constexpr int kN = CP < 64 ? CP : 64;           // output channels per G unit (MMA N)
-  static constexpr int kTmemCols = kRow ? 512 : kNAcc * kN;     // 128, 256 or 512
+  static constexpr int kTmemCols = kRow ? 512 : kNAcc * kGP * kN;     // 128, 256 or 512
   // F unit: kFT tiles x 8 channels (one core-matrix k group, so that a
   // warp's U stores fill whole 32-byte sectors): 64 tiles with a thread per
   // (tile, channel pair) for T = 6, 32 tiles with a thread per (tile,
@@ -1266,7 +1270,10 @@ static auto with_shape(const Geo& g, const FusedOpts& o, F&& f) -> decltype(f(Sh
   if (g.fft || g.Cp != g.Cppad || (g.C != g.Cpad && g.Cpad != 16)) return R();
   switch (g.T * 1000000 + g.Cpad * 1000 + g.Cp) {
 #ifdef WF_WS_ONLY   // tuning builds (tools/build_alt.sh): one instance, compiles in 40 s
-    case WF_WS_ONLY: return f(Shape<WF_WS_ONLY / 1000000, (WF_WS_ONLY / 1000) % 1000, WF_WS_ONLY % 1000>());
+#ifndef WF_WS_ONLY_GP
+#define WF_WS_ONLY_GP 1
+#endif
+    case WF_WS_ONLY: return f(Shape<WF_WS_ONLY / 1000000, (WF_WS_ONLY / 1000) % 1000, WF_WS_ONLY % 1000, 2, WF_WS_ONLY_GP>());
 #else
     case 6016064: return f(Shape<6, 16, 64>());
     case 6064064: return f(Shape<6, 64, 64>());
@@ -1278,8 +1285,19 @@ static auto with_shape(const Geo& g, const FusedOpts& o, F&& f) -> decltype(f(Sh
     case 6256256: return f(Shape<6, 256, 256>());   // VGG conv3_2/3_3 (36 x 4 = 144 CTAs)
     // F(6x6,3x3): the c5 sweep's layers (64 x C'/64 <= 148); C' < 64 runs
     // G units of N = C'
-    case 8016016: return f(Shape<8, 16, 16>());
-    case 8032032: return f(Shape<8, 32, 32>());
+    // positions per G unit of the narrow instances: the 16-channel layers'
+    // G roles are bound by the per-unit latency (dependency poll, 8 KB of
+    // U, 3 MMAs, publish); two positions per unit measured 15-21% faster
+    // on the c5 16 -> 16 layers (419 -> 331 us @112), four slower; the
+    // 32-channel layers show no difference
+#ifndef WF_WS_GP16
+#define WF_WS_GP16 2
+#endif
+#ifndef WF_WS_GP32
+#define WF_WS_GP32 1
+#endif
+    case 8016016: return f(Shape<8, 16, 16, 2, WF_WS_GP16>());
+    case 8032032: return f(Shape<8, 32, 32, 2, WF_WS_GP32>());
     case 8064064: return f(Shape<8, 64, 64>());
     case 8128128: return f(Shape<8, 128, 128>());
 #endif
