@@ -62,16 +62,19 @@ struct Shape {
   // whose G roles are bound by the per-unit latency)
   static constexpr int kGP = GP_;
   static constexpr bool kRow = T_ == 6 && GP_ == 6;
-  static constexpr int kAcc = kRow ? 1 : kNAcc;          // TMEM buffers in flight (6 x 64 columns fill TMEM)
+  static constexpr int kNcols = GP_ * (CP_ < 64 ? CP_ : 64);     // TMEM columns of one unit
+  // TMEM buffers in flight (row units: 6 x 64 columns, one buffer)
+  static constexpr int kAcc = kRow ? 1 : (512 / kNcols < kNAcc ? 512 / kNcols : kNAcc);
   static_assert(!kRow || (C_ <= 64 && CP_ == 64 && SL_ == 2), "row units");
-  static_assert((T_ * T_) % GP_ == 0 && kAcc * GP_ * (CP_ < 64 ? CP_ : 64) <= 512, "positions per G unit");
+  static_assert((T_ * T_) % GP_ == 0 && kAcc >= 1 && kAcc * kNcols <= 512, "positions per G unit");
   // F/I staging slots: 2 x 72 KB.  (3 x 48 KB with 2-channel I units was
   // measured on c2: 98 vs 80 us -- twice the I units and a shorter lag)
   static constexpr int kSlots = SL_;
   static constexpr int kT = T_, kP = T_ * T_;
   static constexpr int C = C_, CP = CP_;               // C = Cpad (input channels may be fewer)
   static constexpr int kN = CP < 64 ? CP : 64;           // output channels per G unit (MMA N)
-  static constexpr int kTmemCols = kRow ? 512 : kNAcc * kGP * kN;     // 128, 256 or 512
+  static constexpr int kTmemColsUsed = kAcc * kGP * kN;
+  static constexpr int kTmemCols = kTmemColsUsed <= 128 ? 128 : kTmemColsUsed <= 256 ? 256 : 512;
   // F unit: kFT tiles x 8 channels (one core-matrix k group, so that a
   // warp's U stores fill whole 32-byte sectors): 64 tiles with a thread per
   // (tile, channel pair) for T = 6, 32 tiles with a thread per (tile,
@@ -100,7 +103,8 @@ struct Shape {
   static constexpr int kNCG = (kBlockTiles / kFT) * (C / kCPC);   // F units per block
   static constexpr int kNIG = CP / (2 * kIPairs);                 // I units per block
   // (2 stages measured equal to 4 on c2: the G units wait for their inputs, not for stage space)
-  static constexpr int kAStages = kRow ? 2 : C >= 128 ? 3 : 4;
+  // (every extra resident V slab of a multi-position unit takes one stage's room)
+  static constexpr int kAStages = kRow ? 2 : (C >= 128 ? 3 : 4) - (C == 64 ? GP_ - 1 : 0);
   static constexpr uint32_t kVHalf = kN * C * 2;         // V hi (or lo) of one (position, c' group)
   static constexpr uint32_t kVGroup = 2 * kVHalf;
   static constexpr size_t kUPos = 2 * kKB * kAHalf;      // U of one position: [hl][K block]
@@ -1275,9 +1279,12 @@ static auto with_shape(const Geo& g, const FusedOpts& o, F&& f) -> decltype(f(Sh
 #endif
     case WF_WS_ONLY: return f(Shape<WF_WS_ONLY / 1000000, (WF_WS_ONLY / 1000) % 1000, WF_WS_ONLY % 1000, 2, WF_WS_ONLY_GP>());
 #else
-    case 6016064: return f(Shape<6, 16, 64>());
+    // (two positions per G unit where it measured faster and the V slabs
+    // fit: VGG 3 -> 64 @224 359 -> 332 us, 64 -> 128 @112 224 -> 211 us;
+    // 64 -> 64 and F(6x6,3x3) 32 -> 32 / 64 -> 64 measured equal or slower)
+    case 6016064: return f(Shape<6, 16, 64, 2, 2>());
     case 6064064: return f(Shape<6, 64, 64>());
-    case 6064128: return f(Shape<6, 64, 128>());
+    case 6064128: return f(Shape<6, 64, 128, 2, 2>());
     case 6064256: return f(Shape<6, 64, 256>());
     case 6128064: return f(Shape<6, 128, 64>());
     case 6128128: return f(Shape<6, 128, 128>());
@@ -1389,8 +1396,8 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
     // the deadlock-freedom argument uses.
     const int step = std::max(1, sm_count / S::kNGG);
     int gb = S::CP <= 16 ? 8 : S::CP <= 32 ? 4 : 1;
-    if (o.gbatch > 0) gb = std::min(ws::kNAcc, o.gbatch);
-    else if (const int k = tuning_knob("WF_WS_GBATCH", 0)) gb = std::max(1, std::min(ws::kNAcc, k));
+    if (o.gbatch > 0) gb = std::min(S::kAcc, o.gbatch);
+    else if (const int k = tuning_knob("WF_WS_GBATCH", 0)) gb = std::max(1, std::min(S::kAcc, k));
     while (gb > 1 && (gb - 1) * step >= std::min(P.L2, std::min(P.NU, P.NM))) --gb;
     P.gbatch = gb;
     return ws::launch_t<S>(P, sm_count, st);

@@ -21,6 +21,8 @@ cases = [
     ((24, 64, 64, 56, 56, 3, 1, 1), 6, "ws_row", None),
     ((24, 64, 64, 56, 56, 3, 1, 1), 6, "ws_row", 12),
     ((8, 3, 64, 112, 112, 3, 1, 1), 6, "ws", None),
+    ((8, 64, 128, 56, 56, 3, 1, 1), 6, "ws", None),       # two positions per G unit
+    ((8, 64, 128, 56, 56, 3, 1, 1), 6, "ws", 16),
     ((8, 128, 256, 56, 56, 3, 1, 1), 6, "ws", None),
     ((8, 256, 256, 28, 28, 3, 1, 1), 6, "ws", None),
     ((64, 16, 16, 56, 56, 3, 1, 1), 8, "ws", None),        # batched G publishes
