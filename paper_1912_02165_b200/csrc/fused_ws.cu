@@ -1401,6 +1401,12 @@ cudaError_t run_fused_ws(const float* x, const uint8_t* vpack, float* y, uint8_t
     if (o.gbatch > 0) gb = std::min(S::kAcc, o.gbatch);
     else if (const int k = tuning_knob("WF_WS_GBATCH", 0)) gb = std::max(1, std::min(S::kAcc, k));
     while (gb > 1 && (gb - 1) * step >= std::min(P.L2, std::min(P.NU, P.NM))) --gb;
+    // ... and a batch makes G(b)'s publish wait for F(b + (batch - 1) * step):
+    // the largest deadlock-free lag (plan_t: NU + NM - 2 when F waits on G)
+    // shrinks by that many blocks.  A requested lag beyond it (wf_fused_opts.
+    // lag, WF_WS_LAG) shrinks the batch, not the other way round.
+    if (P.NU < g.n_blk)
+      while (gb > 1 && P.L2 > P.NU + P.NM - 2 - (gb - 1) * step) --gb;
     P.gbatch = gb;
     return ws::launch_t<S>(P, sm_count, st);
   });

@@ -336,6 +336,26 @@ def test_persistent_kernels_repeat_calls_bitwise_stable(variant, ring_mb):
     assert plan.variant == variant and bad == 0, bad
 
 
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("dims,t", [((96, 32, 32, 56, 56, 3, 1, 1), 8), ((128, 16, 16, 56, 56, 3, 1, 1), 8),
+                                    ((24, 64, 64, 56, 56, 3, 1, 1), 6)])
+@pytest.mark.parametrize("lag", [2, 1000])
+def test_extreme_lags_complete_and_stay_bitwise(dims, t, lag):
+    """wf_fused_opts.lag is a caller's choice: the smallest and an absurdly
+    large one (clamped to the rings) must neither deadlock nor change the
+    result -- with batched G publishes (narrow layers) the largest safe lag
+    shrinks by the blocks a batch spans, and the batch now yields to the lag
+    (a lag of 64+ on the 32-channel layers used to hang the GPU)."""
+    spec = wf.LayerSpec(*dims)
+    rng = np.random.default_rng(13)
+    x = rng.uniform(-1, 1, spec.input_dims()).astype(np.float32)
+    pack = wf.transform_kernels(wf.Tensor4D(_he(rng, spec)), wf.make_basis(t))
+    ref, _ = _run("three_stage", x, pack, spec, t)
+    for ring in (None, 24 << 20):
+        y, v = _fused_ex(x, pack, spec, t, variant="ws", lag=lag, **({"ring_bytes": ring} if ring else {}))
+        assert v == "ws" and np.array_equal(y, ref), (lag, ring)
+
+
 def test_ws_row_units_reject_other_shapes():
     spec = wf.LayerSpec(2, 128, 128, 28, 28, 3, 1, 1)
     x = wf.new_tensor(spec.input_dims(), seed=1)
