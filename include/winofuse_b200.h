@@ -131,7 +131,7 @@ typedef struct wf_fused_opts {
   int variant;       /* WF_FUSED_*                                                    */
   int flags;         /* WF_FUSED_COUNTERS_CLEAN | WF_FUSED_INSTRUMENT                 */
   size_t ring_bytes; /* L2 ring budget of the persistent kernels (EngineConfig.l2_budget_bytes), 0 = default */
-  int lag;           /* steps between a block's producer and consumer units, 0 = default */
+  int lag;           /* steps between a block's producer and consumer units, 0 = default; any value is safe (clamped to the rings) */
   int gbatch;        /* G completions per publish (warp-specialised), 0 = default    */
 } wf_fused_opts;
 
